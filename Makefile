@@ -1,0 +1,47 @@
+# Top-level build: the product library (sm_100a CUDA + C++ host API), the
+# meshgen library and the oracle checkers.  `make` here is what
+# __graft_entry__.build() runs.
+NVCC ?= nvcc
+CXX ?= g++
+PKG := paper_2502_00778_b200
+CSRC := $(PKG)/csrc
+LIBDIR := $(PKG)/lib
+
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# -fmad=false: no FMA contraction, so fp64 results round like the
+# -ffp-contract=off oracle.
+NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -Iinclude \
+           -Xptxas -warn-spills --expt-relaxed-constexpr
+CXXFLAGS := -O2 -fPIC -std=c++20 -ffp-contract=off -Iinclude
+
+CU_SRCS := $(CSRC)/capi.cu $(CSRC)/primitives.cu $(CSRC)/edges.cu $(CSRC)/navs.cu \
+           $(CSRC)/volumes.cu $(CSRC)/verify.cu $(CSRC)/validate.cu
+CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
+HDRS := $(wildcard $(CSRC)/*.cuh) include/dm_capi.h
+
+all: $(LIBDIR)/libdualmesh.so $(LIBDIR)/libdm_meshgen.so oracle
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+build/host_api.o: $(CSRC)/host_api.cpp include/dualmesh/mesh.hpp include/dualmesh/metrics.hpp include/dm_capi.h
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libdualmesh.so: $(CU_OBJS) build/host_api.o
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -o $@ $^
+
+$(LIBDIR)/libdm_meshgen.so: $(CSRC)/meshgen.cpp include/dm_meshgen.h
+	@mkdir -p $(LIBDIR)
+	$(CXX) $(CXXFLAGS) -O3 -shared -o $@ $<
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIBDIR)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,376 @@
+#!/usr/bin/env python3
+"""Benchmark of the dual-free grid-metric hot path on B200.
+
+Metric (BASELINE.json): tets/s for lumped directed-area vectors + median-dual
+volumes (fp64), and the fraction of the HBM roofline.  One "step" is one pass
+of the SPEC timed region over the resident grid: the
+dual-free element loop + boundary pass (one fused kernel) and the edge-based
+volume loop, with the edge structures prebuilt.  Workload: BASELINE config 5
+(256^3 Kuhn cube, 100,663,296 tets, +-0.15h jitter), the configuration the
+metric is quoted on; seeded synthetic grid (SPEC meshgen, splitmix64 seed 42).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: the path is single-GPU (north_star); N>1 runs N independent
+replicas (one per rank, torchrun), whole-job tets/s = N*K*N_E / max-over-ranks
+time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tets/s for directed-area vectors + dual volumes (fp64); % of HBM roofline"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def algorithmic_bytes(mesh, n_edges, n_bnd_nodes, n_bnd_edges):
+    """SURVEY.md 8(d) canonical bytes (each quantity counted once)."""
+    D = mesh.dim
+    L = D * (D + 1) // 2
+    nE, nv, nB = mesh.num_elements(), mesh.num_nodes(), mesh.num_boundary()
+    b_elem = 4 * (D + 1) * nE + 4 * L * nE + 8 * D * nv + 8 * D * n_edges
+    b_bnd = 4 * D * nB + 8 * D * n_bnd_nodes + 16 * D * n_bnd_edges
+    b_vol = 8 * n_edges + 8 * D * n_edges + 8 * D * nv + 8 * nv
+    b_edges = (4 * (D + 1) * nE + 8 * n_edges + 8 * (nv + 1) + 4 * L * nE + 4 * L * nE
+               + 4 * (n_edges + 1))
+    return {"elem": b_elem, "bnd": b_bnd, "vol": b_vol, "metrics": b_elem + b_bnd + b_vol,
+            "edges": b_edges}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local, dist
+
+
+def max_over_ranks(dist, value, device=None):
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU baseline
+def cpu_sample(steps, warmup, n=64):
+    """Serial oracle (port of SPEC.md:157-178) on a bounded sample of the same
+    grid family: dual-free navs + edge-based volumes, edge list prebuilt."""
+    from oracle.oracle import Oracle
+    from paper_2502_00778_b200 import meshgen
+    O = Oracle()
+    m = meshgen.tet_cube(n, amp=0.15)
+    e, o = O.build_edges(m)
+    e2l, _, _ = O.edge_maps(m, e, o)
+
+    def step():
+        nv = O.navs_dualfree(m, e, o, e2l)
+        O.volumes_edge(m, e, nv)
+
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    return m.num_elements() / dt, dt, m
+
+
+def run_reference(args, world, rank, dist):
+    if rank != 0:
+        return
+    steps, warmup = args.steps, args.warmup
+    value, dt, m = cpu_sample(steps, warmup, n=args.cpu_n)
+    sample = (f"serial oracle port (oracle/oracle.c, -O2 -ffp-contract=off) on a {args.cpu_n}^3 "
+              f"Kuhn cube ({m.num_elements()} tets), dual-free navs + edge volumes, "
+              f"{steps} steps after {warmup} warm-up")
+    line = {"metric": METRIC, "value": value, "unit": "tets/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": steps, "warmup": warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "C5 family (256^3 Kuhn, +-0.15h); "
+                                            f"timed on a {args.cpu_n}^3 sample"},
+            "cpu_baseline": {"value": value, "unit": "tets/s", "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tets/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args, world, rank, local, dist):
+    import torch
+    from paper_2502_00778_b200 import Engine, _lib, meshgen
+
+    torch.cuda.set_device(local)
+    t0 = time.perf_counter()
+    mesh = meshgen.baseline_config(args.config, args.scale)
+    gen_s = time.perf_counter() - t0
+    eng = Engine(local)
+    eng.set_mesh(mesh)
+    # K1 edge extraction (outside the SPEC timed region; reported separately)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.ExternalStream(eng.stream())
+    ev0.record(stream)
+    ne = eng.build_edges()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    edges_ms = ev0.elapsed_time(ev1)
+    variant = _lib.DM_VARIANT_SCATTER if args.variant == "scatter" else _lib.DM_VARIANT_GATHER
+    DF, TR, EDGE = _lib.DM_NAV_DUALFREE, _lib.DM_NAV_TRADITIONAL, _lib.DM_VOL_EDGE
+    # derived structures (bedge, incoming CSR) are built by the first call
+    eng.navs(DF, variant)
+    eng.volumes(EDGE)
+    bmask = eng.boundary_node_mask()
+    bd = mesh.boundary.reshape(-1, mesh.dim)
+    if mesh.dim == 3:
+        pairs = np.concatenate([bd[:, [0, 1]], bd[:, [1, 2]], bd[:, [2, 0]]])
+    else:
+        pairs = bd[:, [0, 1]]
+    pairs = np.sort(pairs, axis=1).astype(np.int64)
+    n_bnd_edges = int(np.unique(pairs[:, 0] * (1 << 32) + pairs[:, 1]).size)
+    B = algorithmic_bytes(mesh, ne, int(bmask.sum()), n_bnd_edges)
+    peak, peak_kind = hbm_peak()
+
+    def step(evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        eng.navs(DF, variant)
+        if evs is not None:
+            evs[1].record(stream)
+        eng.volumes(EDGE)
+        if evs is not None:
+            evs[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    launches0 = eng.launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(dist)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(K):
+        step(evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    clk = clocks.stop()
+    launches = eng.launches() - launches0
+    total_ms = start.elapsed_time(end)
+    total_ms = max_over_ranks(dist, total_ms, device=torch.device("cuda", local))
+    ms_step = total_ms / K
+    nav_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+    vol_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    value = world * K * mesh.num_elements() / (total_ms / 1e3)
+
+    # GPU traditional comparator (north_star (e)), same harness, not the headline
+    for _ in range(max(1, args.warmup // 2)):
+        eng.navs(TR, _lib.DM_VARIANT_GATHER)
+    torch.cuda.synchronize()
+    t_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    t_ev[0].record(stream)
+    for _ in range(K):
+        eng.navs(TR, _lib.DM_VARIANT_GATHER)
+        eng.volumes(EDGE)
+    t_ev[1].record(stream)
+    torch.cuda.synchronize()
+    trad_ms = t_ev[0].elapsed_time(t_ev[1]) / K
+
+    # e2e: the public C-ABI step with host buffers (pinned), H2D coords + D2H navs/volumes
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        nb_c = mesh.coords.nbytes
+        nb_n = 8 * mesh.dim * ne
+        nb_v = 8 * mesh.num_nodes()
+        hp = [C.c_void_p() for _ in range(3)]
+        for p, nb in zip(hp, (nb_c, nb_n, nb_v)):
+            if _lib.capi().dm_host_alloc(nb, C.byref(p)) != 0:
+                raise MemoryError("pinned allocation failed")
+        hc = np.ctypeslib.as_array(C.cast(hp[0], C.POINTER(C.c_double)), shape=(mesh.coords.size,))
+        hc[:] = mesh.coords
+        dp = lambda p: C.cast(p, C.POINTER(C.c_double))  # noqa: E731
+        for _ in range(2):
+            eng.metrics_host(dp(hp[0]), DF, variant, EDGE, dp(hp[1]), dp(hp[2]))
+        barrier(dist)
+        t0 = time.perf_counter()
+        ke = max(3, K // 2)
+        for _ in range(ke):
+            eng.metrics_host(dp(hp[0]), DF, variant, EDGE, dp(hp[1]), dp(hp[2]))
+        t_e2e = (time.perf_counter() - t0) / ke
+        t_e2e = max_over_ranks(dist, t_e2e, device=torch.device("cuda", local))
+        e2e = {"value": world * mesh.num_elements() / t_e2e, "unit": "tets/s",
+               "h2d_bytes_per_step": nb_c, "d2h_bytes_per_step": nb_n + nb_v,
+               "ms_per_step": t_e2e * 1e3,
+               "api": "dm_metrics_host (include/dm_capi.h), pinned host buffers"}
+        for p in hp:
+            _lib.capi().dm_host_free(p)
+
+    kernel_bytes = B["elem"] + B["bnd"]
+    achieved = kernel_bytes / (nav_ms / 1e3) / 1e9
+    step_achieved = B["metrics"] / (ms_step / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("navs_kernel_dram_bytes")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cv, cdt, cm = cpu_sample(args.cpu_steps, 1, n=args.cpu_n)
+        cpu = {"value": cv, "unit": "tets/s", "cores": 1, "kind": "port",
+               "sample": f"serial oracle (oracle/oracle.c) on a {args.cpu_n}^3 Kuhn cube "
+                         f"({cm.num_elements()} tets, same +-0.15h family), dual-free navs + "
+                         f"edge volumes, {args.cpu_steps} steps, {cdt * 1e3:.1f} ms/step"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: 256^3 Kuhn cube, +-0.15h jitter (seed 42)"
+                                   if args.config == "C5" and args.scale == 1 else
+                                   f"{args.config}/scale {args.scale}",
+                       "n_elements": mesh.num_elements(), "n_nodes": mesh.num_nodes(),
+                       "n_edges": ne, "n_boundary": mesh.num_boundary(),
+                       "nav_variant": args.variant,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (no flush): "
+                             f"{B['metrics'] / 1e9:.2f} GB algorithmic per step"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_navs_gather<3,dualfree> (K2+K3 fused, + s_e)",
+                         "bytes_per_launch": kernel_bytes, "ms_per_launch": nav_ms,
+                         "peak_source": peak_kind},
+            "step_roofline": {"achieved": step_achieved, "frac": step_achieved / peak,
+                              "bytes_per_step": B["metrics"], "unit": "GB/s",
+                              "nav_ms": nav_ms, "vol_ms": vol_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "extra": {"edges_ms": edges_ms, "edges_bytes": B["edges"],
+                      "edges_GBps": B["edges"] / (edges_ms / 1e3) / 1e9,
+                      "traditional_ms_per_step": trad_ms,
+                      "gpu_speedup_dualfree_over_traditional": trad_ms / ms_step,
+                      "meshgen_s": gen_s},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--variant", choices=["gather", "scatter"], default="gather")
+    ap.add_argument("--cpu-n", type=int, default=64)
+    ap.add_argument("--cpu-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank, dist)
+        else:
+            run_ours(args, world, rank, local, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

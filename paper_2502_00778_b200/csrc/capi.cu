@@ -1,0 +1,333 @@
+// capi.cu -- the extern "C" surface of libdualmesh.so (include/dm_capi.h):
+// context lifetime, mesh upload, result download, timing and plumbing.
+#include <cstring>
+
+#include "dm_internal.cuh"
+
+using namespace dm;
+
+namespace {
+
+const char* kStatus[] = {"ok",           "invalid argument", "mesh/edge mismatch",
+                         "boundary edge absent from EdgeList", "CUDA error", "out of device memory",
+                         "call order",   "unsupported size"};
+
+int check_device(dm_ctx* c) {
+  int n = 0;
+  cudaError_t st = cudaGetDeviceCount(&n);
+  if (st != cudaSuccess || n == 0)
+    return fail(c, DM_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(st));
+  if (c->device < 0 || c->device >= n) return fail(c, DM_ERR_INVALID_ARG, "bad device ordinal");
+  cudaDeviceProp prop;
+  DM_CK(c, cudaGetDeviceProperties(&prop, c->device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(c, DM_ERR_CUDA, std::string("libdualmesh is built for sm_100a only; device is ") +
+                                    prop.name);
+  return DM_OK;
+}
+
+void drop_derived(dm_ctx* c) {
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = false;
+  c->have_navs = c->have_vols = false;
+  c->navs_algo = -1;
+  c->ne = 0;
+  c->n_bedge = 0;
+  c->n_derived = 0;
+}
+
+float ev_ms(dm_ctx* c, int a, int b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) ms = -1.f;
+  return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dm_version(void) { return 1; }
+
+const char* dm_status_string(int status) {
+  if (status > 0 || status < -7) return "unknown status";
+  return kStatus[-status];
+}
+
+int dm_create(dm_ctx** out, int device) {
+  if (!out) return DM_ERR_INVALID_ARG;
+  *out = nullptr;
+  auto* c = new dm_ctx;
+  c->device = device;
+  int st = check_device(c);
+  if (st == DM_OK) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+    if (e != cudaSuccess) st = fail(c, DM_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (st != DM_OK) {
+    // keep the context so dm_last_error can explain the failure
+    *out = c;
+    return st;
+  }
+  *out = c;
+  return DM_OK;
+}
+
+void dm_destroy(dm_ctx* c) {
+  if (!c) return;
+  if (c->stream) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+  }
+  delete c;
+}
+
+const char* dm_last_error(const dm_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int dm_set_mesh(dm_ctx* c, int dim, const double* coords, int64_t n_nodes, const int32_t* elements,
+                int64_t n_elements, const int32_t* boundary, int64_t n_boundary) {
+  if (!c || !c->stream) return DM_ERR_INVALID_ARG;
+  if ((dim != 2 && dim != 3) || n_nodes < 0 || n_elements < 0 || n_boundary < 0)
+    return fail(c, DM_ERR_INVALID_ARG, "dim must be 2 or 3 and counts non-negative");
+  if ((n_nodes && !coords) || (n_elements && !elements) || (n_boundary && !boundary))
+    return fail(c, DM_ERR_INVALID_ARG, "null array with non-zero count");
+  if (n_nodes >= (1ll << 31)) return fail(c, DM_ERR_UNSUPPORTED, "node ids are 32-bit");
+  drop_derived(c);
+  c->dim = dim;
+  c->nv = n_nodes;
+  c->nE = n_elements;
+  c->nB = n_boundary;
+  DM_CK(c, c->coords.ensure(static_cast<size_t>(dim * n_nodes)));
+  DM_CK(c, c->elems.ensure(static_cast<size_t>((dim + 1) * n_elements)));
+  DM_CK(c, c->bnd.ensure(static_cast<size_t>(dim * n_boundary)));
+  if (n_nodes)
+    DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * dim * n_nodes,
+                             cudaMemcpyHostToDevice, c->stream));
+  if (n_elements)
+    DM_CK(c, cudaMemcpyAsync(c->elems.p, elements, sizeof(int32_t) * (dim + 1) * n_elements,
+                             cudaMemcpyHostToDevice, c->stream));
+  if (n_boundary)
+    DM_CK(c, cudaMemcpyAsync(c->bnd.p, boundary, sizeof(int32_t) * dim * n_boundary,
+                             cudaMemcpyHostToDevice, c->stream));
+  int st = pad_coords(c);
+  if (st) return st;
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_set_coords(dm_ctx* c, const double* coords) {
+  if (!c || !coords) return DM_ERR_INVALID_ARG;
+  if (c->dim == 0) return fail(c, DM_ERR_STATE, "dm_set_coords before dm_set_mesh");
+  DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * c->dim * c->nv,
+                           cudaMemcpyHostToDevice, c->stream));
+  c->have_navs = c->have_vols = false;
+  return pad_coords(c);
+}
+
+int dm_set_coords_device(dm_ctx* c, const double* d_coords) {
+  if (!c || !d_coords) return DM_ERR_INVALID_ARG;
+  if (c->dim == 0) return fail(c, DM_ERR_STATE, "dm_set_coords_device before dm_set_mesh");
+  DM_CK(c, cudaMemcpyAsync(c->coords.p, d_coords, sizeof(double) * c->dim * c->nv,
+                           cudaMemcpyDeviceToDevice, c->stream));
+  c->have_navs = c->have_vols = false;
+  return pad_coords(c);
+}
+
+int dm_build_edges(dm_ctx* c, int64_t* n_edges) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  if (c->dim == 0) return fail(c, DM_ERR_STATE, "dm_build_edges before dm_set_mesh");
+  int st = build_edges_impl(c);
+  if (st) return st;
+  if (n_edges) *n_edges = c->ne;
+  return DM_OK;
+}
+
+int dm_get_edges(dm_ctx* c, int32_t* edges, uint64_t* origin_start) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  if (edges && c->ne)
+    DM_CK(c, cudaMemcpyAsync(edges, c->edges.p, sizeof(int2) * c->ne, cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (origin_start) {
+    // widen the 32-bit device CSR to the reference's size_t (mesh.hpp:50)
+    std::uint32_t* tmp = nullptr;
+    DM_CK(c, cudaMallocHost(&tmp, sizeof(std::uint32_t) * (c->nv + 1)));
+    cudaError_t e = cudaMemcpyAsync(tmp, c->os.p, sizeof(std::uint32_t) * (c->nv + 1),
+                                    cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess)
+      for (int64_t v = 0; v <= c->nv; ++v) origin_start[v] = tmp[v];
+    cudaFreeHost(tmp);
+    DM_CK(c, e);
+  }
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_get_e2l(dm_ctx* c, int32_t* e2l) {
+  if (!c || !e2l) return DM_ERR_INVALID_ARG;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  const int L = c->dim == 3 ? 6 : 3;
+  DM_CK(c, cudaMemcpyAsync(e2l, c->e2l.p, sizeof(int32_t) * L * c->nE, cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_get_incidence(dm_ctx* c, int32_t* inc_ptr, int32_t* inc) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  const int L = c->dim == 3 ? 6 : 3;
+  if (inc_ptr)
+    DM_CK(c, cudaMemcpyAsync(inc_ptr, c->inc_ptr.p, sizeof(int32_t) * (c->ne + 1),
+                             cudaMemcpyDeviceToHost, c->stream));
+  if (inc && c->nE)
+    DM_CK(c, cudaMemcpyAsync(inc, c->inc.p, sizeof(int32_t) * L * c->nE, cudaMemcpyDeviceToHost,
+                             c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_navs(dm_ctx* c, int nav_algo, int variant) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  return navs_impl(c, nav_algo, variant);
+}
+
+int dm_volumes(dm_ctx* c, int vol_algo) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  if (c->dim == 0) return fail(c, DM_ERR_STATE, "no mesh");
+  return volumes_impl(c, vol_algo);
+}
+
+int dm_get_navs(dm_ctx* c, double* navs) {
+  if (!c || !navs) return DM_ERR_INVALID_ARG;
+  if (!c->have_navs) return fail(c, DM_ERR_STATE, "navs not computed");
+  DM_CK(c, cudaMemcpyAsync(navs, c->navs.p, sizeof(double) * c->dim * c->ne,
+                           cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_put_navs(dm_ctx* c, const double* navs) {
+  if (!c || !navs) return DM_ERR_INVALID_ARG;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  DM_CK(c, c->navs.ensure(static_cast<size_t>(c->dim * c->ne)));
+  DM_CK(c, cudaMemcpyAsync(c->navs.p, navs, sizeof(double) * c->dim * c->ne,
+                           cudaMemcpyHostToDevice, c->stream));
+  DM_CK(c, c->svals.ensure(static_cast<size_t>(c->ne)));
+  int st = svals_from_navs(c);
+  if (st) return st;
+  c->have_navs = true;
+  c->have_vols = false;
+  c->navs_algo = -1;
+  return DM_OK;
+}
+
+int dm_put_volumes(dm_ctx* c, const double* volumes) {
+  if (!c || !volumes) return DM_ERR_INVALID_ARG;
+  if (c->dim == 0) return fail(c, DM_ERR_STATE, "no mesh");
+  DM_CK(c, c->vols.ensure(static_cast<size_t>(c->nv)));
+  DM_CK(c, cudaMemcpyAsync(c->vols.p, volumes, sizeof(double) * c->nv, cudaMemcpyHostToDevice,
+                           c->stream));
+  c->have_vols = true;
+  return DM_OK;
+}
+
+int dm_get_volumes(dm_ctx* c, double* volumes) {
+  if (!c || !volumes) return DM_ERR_INVALID_ARG;
+  if (!c->have_vols) return fail(c, DM_ERR_STATE, "volumes not computed");
+  DM_CK(c, cudaMemcpyAsync(volumes, c->vols.p, sizeof(double) * c->nv, cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_metrics_host(dm_ctx* c, const double* coords, int nav_algo, int variant, int vol_algo,
+                    double* navs, double* volumes) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "build the edge list first");
+  int st = DM_OK;
+  if (coords) {
+    st = dm_set_coords(c, coords);
+    if (st) return st;
+  }
+  st = navs_impl(c, nav_algo, variant);
+  if (st) return st;
+  st = volumes_impl(c, vol_algo);
+  if (st) return st;
+  if (navs)
+    DM_CK(c, cudaMemcpyAsync(navs, c->navs.p, sizeof(double) * c->dim * c->ne,
+                             cudaMemcpyDeviceToHost, c->stream));
+  if (volumes)
+    DM_CK(c, cudaMemcpyAsync(volumes, c->vols.p, sizeof(double) * c->nv, cudaMemcpyDeviceToHost,
+                             c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_stream(dm_ctx* c, void** stream) {
+  if (!c || !stream) return DM_ERR_INVALID_ARG;
+  *stream = c->stream;
+  return DM_OK;
+}
+
+int dm_device_views(dm_ctx* c, dm_device_view* v) {
+  if (!c || !v) return DM_ERR_INVALID_ARG;
+  std::memset(v, 0, sizeof(*v));
+  v->dim = c->dim;
+  v->n_nodes = c->nv;
+  v->n_elements = c->nE;
+  v->n_boundary = c->nB;
+  v->n_edges = c->ne;
+  v->coords = c->coords.p;
+  v->elements = c->elems.p;
+  v->boundary = c->bnd.p;
+  if (c->have_edges) {
+    v->edges = reinterpret_cast<const int32_t*>(c->edges.p);
+    v->origin_start = c->os.p;
+    v->e2l = c->e2l.p;
+    v->inc_ptr = c->inc_ptr.p;
+    v->inc = c->inc.p;
+  }
+  v->navs = c->have_navs ? c->navs.p : nullptr;
+  v->volumes = c->have_vols ? c->vols.p : nullptr;
+  return DM_OK;
+}
+
+int dm_sync(dm_ctx* c) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+int dm_set_timing(dm_ctx* c, int enable) {
+  if (!c) return DM_ERR_INVALID_ARG;
+  c->timing = enable != 0;
+  return DM_OK;
+}
+
+int dm_get_timings(dm_ctx* c, float* ms, int n) {
+  if (!c || !ms) return DM_ERR_INVALID_ARG;
+  if (!c->timing) return fail(c, DM_ERR_STATE, "timing disabled");
+  DM_CK(c, cudaEventSynchronize(c->ev[3]));
+  c->last_ms[0] = ev_ms(c, 0, 1);
+  c->last_ms[1] = ev_ms(c, 1, 2);
+  c->last_ms[2] = ev_ms(c, 2, 3);
+  c->last_ms[3] = ev_ms(c, 0, 3);
+  for (int i = 0; i < n && i < 4; ++i) ms[i] = c->last_ms[i];
+  return DM_OK;
+}
+
+int64_t dm_kernel_launches(const dm_ctx* c) { return c ? c->launches : -1; }
+
+int dm_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return DM_ERR_INVALID_ARG;
+  return cudaMallocHost(ptr, bytes) == cudaSuccess ? DM_OK : DM_ERR_OOM;
+}
+
+int dm_host_free(void* ptr) { return cudaFreeHost(ptr) == cudaSuccess ? DM_OK : DM_ERR_CUDA; }
+
+}  // extern "C"

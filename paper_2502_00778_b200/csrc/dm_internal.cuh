@@ -1,0 +1,220 @@
+// dm_internal.cuh -- context, device buffers and shared device helpers of
+// libdualmesh.so.  Everything here is sm_100a-only; the library is compiled
+// with -fmad=false so fp64 expressions round exactly like the serial oracle
+// built with -ffp-contract=off.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "dm_capi.h"
+
+namespace dm {
+
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+using i64 = std::int64_t;
+
+// ---------------------------------------------------------------- buffers
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;  // elements allocated
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  // (Re)allocate to exactly hold `count` elements; keeps the buffer when it
+  // is already large enough.
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    release();
+    size_t bytes = (count ? count : 1) * sizeof(T);
+    cudaError_t st = cudaMalloc(reinterpret_cast<void**>(&p), bytes);
+    if (st == cudaSuccess) n = count;
+    else p = nullptr;
+    return st;
+  }
+};
+
+// 3D node coordinates padded to one 32-byte sector per node; loaded with a
+// single 256-bit LDG (LDG.E.ENL2.256 on sm_100a).
+struct __align__(32) d4 {
+  double x, y, z, w;
+};
+
+}  // namespace dm
+
+// ---------------------------------------------------------------- context
+struct dm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  int dim = 0;
+  dm::i64 nv = 0, nE = 0, nB = 0;
+  dm::DevBuf<double> coords;  // caller layout, dim doubles per node
+  dm::DevBuf<dm::d4> x4;      // 3D padded copy
+  dm::DevBuf<int32_t> elems, bnd;
+
+  // edge structures (K1)
+  bool have_edges = false;
+  dm::i64 ne = 0;
+  dm::DevBuf<int2> edges;
+  dm::DevBuf<dm::u32> os;  // origin_start (32-bit on device)
+  dm::DevBuf<int32_t> e2l, inc_ptr, inc;
+  // derived: incoming-edge CSR per node, boundary (edge,facet) pairs, node->element CSR
+  bool have_in = false;
+  dm::DevBuf<dm::u32> in_ptr;
+  dm::DevBuf<int32_t> in_list;
+  bool have_bedge = false;
+  dm::i64 n_bedge = 0;
+  dm::DevBuf<dm::u64> bedge;
+  bool have_n2e = false;
+  dm::DevBuf<dm::u32> n2e_ptr;
+  dm::DevBuf<int32_t> n2e;
+
+  // metrics
+  bool have_navs = false, have_vols = false;
+  int navs_algo = -1;
+  dm::DevBuf<double> navs, svals, vols, velem;
+
+  // verify / reductions scratch
+  dm::DevBuf<double> red;
+  dm::DevBuf<dm::u64> redu;
+
+  // generic scratch
+  dm::DevBuf<dm::u32> cnt, fill;
+  dm::DevBuf<dm::u64> tmp64;
+  dm::DevBuf<dm::u32> scan_tmp;
+  dm::DevBuf<int> flag;
+
+  // derived boundary / validation
+  dm::i64 n_derived = 0;
+  dm::DevBuf<int32_t> derived;
+  dm::DevBuf<dm::i64> vlist;  // first offending ids per class
+  dm::i64 vlist_n[DM_VCOUNT] = {0};
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[8] = {nullptr};
+  float last_ms[4] = {0, 0, 0, 0};
+  dm::i64 launches = 0;
+};
+
+namespace dm {
+
+// ---------------------------------------------------------------- errors
+inline int fail(dm_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define DM_CK(ctx, call)                                                              \
+  do {                                                                                \
+    cudaError_t _st = (call);                                                         \
+    if (_st != cudaSuccess)                                                           \
+      return ::dm::fail((ctx), _st == cudaErrorMemoryAllocation ? DM_ERR_OOM : DM_ERR_CUDA, \
+                        std::string(#call) + ": " + cudaGetErrorString(_st));         \
+  } while (0)
+
+// Launch with bookkeeping: counts the launch and checks the launch error.
+#define DM_LAUNCH(ctx, kern, grid, block, smem, ...)                                  \
+  do {                                                                                \
+    if ((grid) > 0) {                                                                 \
+      kern<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                  \
+      (ctx)->launches++;                                                              \
+      DM_CK(ctx, cudaGetLastError());                                                 \
+    }                                                                                 \
+  } while (0)
+
+inline unsigned grid_for(i64 n, int per_block) {
+  return static_cast<unsigned>((n + per_block - 1) / per_block);
+}
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ d4 ld_d4(const d4* p) {
+  d4 r;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_d2(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ int4 ld_i4(const int4* p) { return __ldg(p); }
+
+// Select el[i] for a runtime i in 0..3 without local-memory indexing.
+__device__ __forceinline__ int sel4(int a0, int a1, int a2, int a3, int i) {
+  return i == 0 ? a0 : (i == 1 ? a1 : (i == 2 ? a2 : a3));
+}
+__device__ __forceinline__ int sel3(int a0, int a1, int a2, int i) {
+  return i == 0 ? a0 : (i == 1 ? a1 : a2);
+}
+
+// ref mesh.cpp:15 tet_opposite_face = {{1,2,3},{0,3,2},{0,1,3},{0,2,1}},
+// packed as 2-bit local ids, 6 bits per face.
+constexpr unsigned kOppPacked = (1u | 2u << 2 | 3u << 4) | (0u | 3u << 2 | 2u << 4) << 6 |
+                                (0u | 1u << 2 | 3u << 4) << 12 | (0u | 2u << 2 | 1u << 4) << 18;
+// ref mesh.cpp:17 tet_local_edges = {01,02,03,12,13,23}; 2D mesh.cpp:263-265 = {01,12,20}.
+constexpr unsigned kTetEdgePacked =
+    (0u | 1u << 2) | (0u | 2u << 2) << 4 | (0u | 3u << 2) << 8 | (1u | 2u << 2) << 12 |
+    (1u | 3u << 2) << 16 | (2u | 3u << 2) << 20;
+constexpr unsigned kTriEdgePacked = (0u | 1u << 2) | (1u | 2u << 2) << 4 | (2u | 0u << 2) << 8;
+
+__device__ __forceinline__ void cross3(double u0, double u1, double u2, double v0, double v1,
+                                       double v2, double& c0, double& c1, double& c2) {
+  // ref mesh.cpp:25-27, same operation order
+  c0 = u1 * v2 - u2 * v1;
+  c1 = u2 * v0 - u0 * v2;
+  c2 = u0 * v1 - u1 * v0;
+}
+
+// Warp-level inclusive scan of an int.
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------- host-side primitives
+// Exclusive scan of n u32 counts into out[0..n] (out[n] = total) on the ctx
+// stream.  in and out may alias.  Returns DM_OK or an error code.
+int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n);
+
+// Sort each segment [seg[s], seg[s+1]) of data ascending; segments up to
+// 4096 keys (larger ones set *flag = 1).  Keys are u32 or u64.
+int segment_sort_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg);
+int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg);
+
+// Derived structures, built lazily.
+int ensure_incoming(dm_ctx* c);
+int ensure_bedge(dm_ctx* c);
+int ensure_n2e(dm_ctx* c);
+int build_edges_impl(dm_ctx* c);
+int navs_impl(dm_ctx* c, int algo, int variant);
+int volumes_impl(dm_ctx* c, int algo);
+int pad_coords(dm_ctx* c);
+int compute_element_volumes(dm_ctx* c);
+int svals_from_navs(dm_ctx* c);
+
+// Read a device int flag (synchronises the stream).
+int read_flag(dm_ctx* c, int* value);
+
+// Timing helpers: record event slot i when timing is enabled.
+inline void tmark(dm_ctx* c, int i) {
+  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+}
+
+}  // namespace dm

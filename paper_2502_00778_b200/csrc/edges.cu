@@ -1,0 +1,375 @@
+// edges.cu -- K1: GPU edge extraction, bit-exact with the reference
+// build_edges (proj/src/mesh.cpp:256-285) and EdgeList::edge_of
+// (mesh.cpp:58-73), plus the element->local-edge map and the edge->element
+// CSR incidence of north_star (a).
+//
+// Algorithm (MSD bucket sort instead of the reference's hash set + sort):
+//   items     : one per (element e, local edge l) = L*N_E, local order of
+//               mesh.cpp:17 (3D) / mesh.cpp:263-265 (2D)
+//   bucket    : the origin j = min(a,b) of the pair (counting sort, atomics)
+//   payload   : (k << 32) | (e*L + l), k = max(a,b)
+//   per bucket: bitonic sort of the payloads -> (k, e*L+l) ascending
+// The concatenated buckets are then sorted by (j, k, e) -- exactly the
+// lexicographic edge order of the reference with, per edge, its incident
+// elements in ascending id.  Atomic placement order is erased by the sort
+// (payloads are unique), so every output is deterministic.
+#include "dm_internal.cuh"
+
+namespace dm {
+namespace {
+
+template <int D>
+__device__ __forceinline__ void load_elem(const int32_t* el, i64 e, int* v) {
+  if (D == 3) {
+    int4 t = ld_i4(reinterpret_cast<const int4*>(el) + e);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    v[0] = __ldg(el + 3 * e); v[1] = __ldg(el + 3 * e + 1); v[2] = __ldg(el + 3 * e + 2);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void local_edge(int l, int& la, int& lb) {
+  const unsigned p = D == 3 ? (kTetEdgePacked >> (4 * l)) : (kTriEdgePacked >> (4 * l));
+  la = p & 3;
+  lb = (p >> 2) & 3;
+}
+
+// Count items per origin bucket.
+template <int D>
+__global__ void k_count(const int32_t* el, i64 nE, u32* cnt) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nE) return;
+  constexpr int L = D == 3 ? 6 : 3;
+  int v[4];
+  load_elem<D>(el, e, v);
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    int la, lb;
+    local_edge<D>(l, la, lb);
+    const int a = v[la], b = v[lb];
+    atomicAdd(cnt + (a < b ? a : b), 1u);
+  }
+}
+
+template <int D>
+__global__ void k_scatter(const int32_t* el, i64 nE, const u32* bstart, u32* fill, u64* out) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nE) return;
+  constexpr int L = D == 3 ? 6 : 3;
+  int v[4];
+  load_elem<D>(el, e, v);
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    int la, lb;
+    local_edge<D>(l, la, lb);
+    const int a = v[la], b = v[lb];
+    const int j = a < b ? a : b, k = a < b ? b : a;
+    const u32 pos = bstart[j] + atomicAdd(fill + j, 1u);
+    out[pos] = (static_cast<u64>(static_cast<u32>(k)) << 32) | static_cast<u64>(e * L + l);
+  }
+}
+
+// Warp per bucket: number of distinct k (= edges with origin j).
+__global__ void k_count_unique(const u64* items, const u32* bstart, i64 nv, u32* ucnt) {
+  const int lane = threadIdx.x & 31;
+  const i64 j = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (j >= nv) return;
+  const u32 b = bstart[j], n = bstart[j + 1] - b;
+  u32 total = 0;
+  for (u32 i0 = 0; i0 < n; i0 += 32) {
+    const u32 i = i0 + lane;
+    bool head = false;
+    if (i < n) head = (i == 0) || ((items[b + i] >> 32) != (items[b + i - 1] >> 32));
+    total += __popc(__ballot_sync(0xffffffffu, head));
+  }
+  if (lane == 0) ucnt[j] = total;
+}
+
+// Warp per bucket: emit edges, inc_ptr, inc and e2l.
+template <int L>
+__global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 nv, int2* edges,
+                       int32_t* inc_ptr, int32_t* inc, int32_t* e2l) {
+  const int lane = threadIdx.x & 31;
+  const i64 j = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (j >= nv) return;
+  const u32 b = bstart[j], n = bstart[j + 1] - b;
+  u32 id_base = os[j];  // edge id of the first head in this chunk
+  for (u32 i0 = 0; i0 < n; i0 += 32) {
+    const u32 i = i0 + lane;
+    u64 it = 0;
+    bool head = false;
+    if (i < n) {
+      it = items[b + i];
+      head = (i == 0) || ((it >> 32) != (items[b + i - 1] >> 32));
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, head);
+    if (i < n) {
+      // heads at or before this lane within the chunk
+      const int before = __popc(hm & (0xffffffffu >> (31 - lane)));
+      const int32_t id = static_cast<int32_t>(id_base + before - 1);
+      const u32 val = static_cast<u32>(it);
+      if (head) {
+        edges[id] = make_int2(static_cast<int>(j), static_cast<int>(it >> 32));
+        inc_ptr[id] = static_cast<int32_t>(b + i);
+      }
+      inc[b + i] = static_cast<int32_t>(val / L);
+      e2l[val] = id;
+    }
+    id_base += __popc(hm);
+  }
+}
+
+__global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
+
+}  // namespace
+
+int build_edges_impl(dm_ctx* c) {
+  const int D = c->dim;
+  const int L = D == 3 ? 6 : 3;
+  const i64 M = static_cast<i64>(L) * c->nE;
+  if (M >= (1ll << 31) || c->nv >= (1ll << 31))
+    return fail(c, DM_ERR_UNSUPPORTED, "mesh exceeds the 32-bit item space of the device layout");
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = false;
+  c->have_navs = c->have_vols = false;
+  const i64 nv = c->nv;
+
+  DM_CK(c, c->cnt.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, c->fill.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, c->tmp64.ensure(static_cast<size_t>(M)));
+  DM_CK(c, cudaMemsetAsync(c->cnt.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->fill.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  const unsigned ge = grid_for(c->nE, 256);
+  if (D == 3) {
+    DM_LAUNCH(c, k_count<3>, ge, 256, 0, c->elems.p, c->nE, c->cnt.p);
+  } else {
+    DM_LAUNCH(c, k_count<2>, ge, 256, 0, c->elems.p, c->nE, c->cnt.p);
+  }
+  int st = scan_exclusive(c, c->cnt.p, c->cnt.p, nv);  // cnt := bucket starts
+  if (st) return st;
+  if (D == 3) {
+    DM_LAUNCH(c, k_scatter<3>, ge, 256, 0, c->elems.p, c->nE, c->cnt.p, c->fill.p, c->tmp64.p);
+  } else {
+    DM_LAUNCH(c, k_scatter<2>, ge, 256, 0, c->elems.p, c->nE, c->cnt.p, c->fill.p, c->tmp64.p);
+  }
+  st = segment_sort_u64(c, c->tmp64.p, c->cnt.p, nv);
+  if (st) return st;
+  // unique counts -> origin_start
+  DM_CK(c, c->os.ensure(static_cast<size_t>(nv + 1)));
+  DM_LAUNCH(c, k_count_unique, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, nv, c->fill.p);
+  st = scan_exclusive(c, c->fill.p, c->os.p, nv);
+  if (st) return st;
+  u32 ne32 = 0;
+  DM_CK(c, cudaMemcpyAsync(&ne32, c->os.p + nv, sizeof(u32), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  c->ne = ne32;
+  DM_CK(c, c->edges.ensure(static_cast<size_t>(c->ne)));
+  DM_CK(c, c->inc_ptr.ensure(static_cast<size_t>(c->ne + 1)));
+  DM_CK(c, c->inc.ensure(static_cast<size_t>(M)));
+  DM_CK(c, c->e2l.ensure(static_cast<size_t>(M)));
+  if (D == 3) {
+    DM_LAUNCH(c, k_emit<6>, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p, nv,
+              c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p);
+  } else {
+    DM_LAUNCH(c, k_emit<3>, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p, nv,
+              c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p);
+  }
+  DM_LAUNCH(c, k_set_i32, 1, 1, 0, c->inc_ptr.p + c->ne, static_cast<int32_t>(M));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  c->tmp64.release();
+  c->have_edges = true;
+  return DM_OK;
+}
+
+// ------------------------------------------------------------ derived CSRs
+namespace {
+
+// incoming edges: bucket by destination k, payload edge id
+__global__ void k_in_count(const int2* edges, i64 ne, u32* cnt) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < ne) atomicAdd(cnt + edges[e].y, 1u);
+}
+__global__ void k_in_scatter(const int2* edges, i64 ne, const u32* start, u32* fill, u32* out) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const int k = edges[e].y;
+  out[start[k] + atomicAdd(fill + k, 1u)] = static_cast<u32>(e);
+}
+
+// node -> element: bucket by every node of every element, payload element id
+template <int D>
+__global__ void k_n2e_count(const int32_t* el, i64 nE, u32* cnt) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < nE * (D + 1)) atomicAdd(cnt + el[t], 1u);
+}
+template <int D>
+__global__ void k_n2e_scatter(const int32_t* el, i64 nE, const u32* start, u32* fill, u32* out) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nE * (D + 1)) return;
+  const int v = el[t];
+  out[start[v] + atomicAdd(fill + v, 1u)] = static_cast<u32>(t / (D + 1));
+}
+
+// boundary (edge, facet) pairs: bucket by the edge's origin, payload (edge<<32 | b)
+__device__ __forceinline__ int dev_edge_of(const int2* edges, const u32* os, i64 nv, int a, int b) {
+  if (a > b) { int t = a; a = b; b = t; }
+  if (a < 0 || a >= nv) return -1;
+  u32 lo = os[a], hi = os[a + 1];
+  const u32 end = hi;
+  while (lo < hi) {
+    const u32 mid = lo + (hi - lo) / 2;
+    if (edges[mid].y < b) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < end && edges[lo].y == b) ? static_cast<int>(lo) : -1;
+}
+
+template <int D>
+__global__ void k_bedge_count(const int32_t* bnd, i64 nB, const int2* edges, const u32* os, i64 nv,
+                              u32* cnt, int* flag) {
+  constexpr int NEB = D == 3 ? 3 : 1;
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nB * NEB) return;
+  const i64 b = t / NEB;
+  const int q = static_cast<int>(t % NEB);
+  const int a = bnd[D * b + q], c = bnd[D * b + (q + 1) % D];
+  const int id = dev_edge_of(edges, os, nv, a, c);
+  if (id < 0) {
+    atomicExch(flag, 1);
+    return;
+  }
+  atomicAdd(cnt + (a < c ? a : c), 1u);
+}
+template <int D>
+__global__ void k_bedge_scatter(const int32_t* bnd, i64 nB, const int2* edges, const u32* os,
+                                i64 nv, const u32* start, u32* fill, u64* out) {
+  constexpr int NEB = D == 3 ? 3 : 1;
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nB * NEB) return;
+  const i64 b = t / NEB;
+  const int q = static_cast<int>(t % NEB);
+  const int a = bnd[D * b + q], c = bnd[D * b + (q + 1) % D];
+  const int id = dev_edge_of(edges, os, nv, a, c);
+  if (id < 0) return;
+  const int j = a < c ? a : c;
+  out[start[j] + atomicAdd(fill + j, 1u)] = (static_cast<u64>(id) << 32) | static_cast<u64>(b);
+}
+
+__global__ void k_edge_of(const int2* edges, const u32* os, i64 nv, const int32_t* a,
+                          const int32_t* b, i64 n, int32_t* out) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = dev_edge_of(edges, os, nv, a[i], b[i]);
+}
+
+}  // namespace
+
+int ensure_incoming(dm_ctx* c) {
+  if (c->have_in) return DM_OK;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  const i64 nv = c->nv, ne = c->ne;
+  DM_CK(c, c->in_ptr.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, c->in_list.ensure(static_cast<size_t>(ne)));
+  DM_CK(c, c->fill.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, cudaMemsetAsync(c->in_ptr.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->fill.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  DM_LAUNCH(c, k_in_count, grid_for(ne, 256), 256, 0, c->edges.p, ne, c->in_ptr.p);
+  int st = scan_exclusive(c, c->in_ptr.p, c->in_ptr.p, nv);
+  if (st) return st;
+  DM_LAUNCH(c, k_in_scatter, grid_for(ne, 256), 256, 0, c->edges.p, ne, c->in_ptr.p, c->fill.p,
+            reinterpret_cast<u32*>(c->in_list.p));
+  st = segment_sort_u32(c, reinterpret_cast<u32*>(c->in_list.p), c->in_ptr.p, nv);
+  if (st) return st;
+  c->have_in = true;
+  return DM_OK;
+}
+
+int ensure_n2e(dm_ctx* c) {
+  if (c->have_n2e) return DM_OK;
+  const i64 nv = c->nv, nt = c->nE * (c->dim + 1);
+  DM_CK(c, c->n2e_ptr.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, c->n2e.ensure(static_cast<size_t>(nt)));
+  DM_CK(c, c->fill.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, cudaMemsetAsync(c->n2e_ptr.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->fill.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  if (c->dim == 3) {
+    DM_LAUNCH(c, k_n2e_count<3>, grid_for(nt, 256), 256, 0, c->elems.p, c->nE, c->n2e_ptr.p);
+  } else {
+    DM_LAUNCH(c, k_n2e_count<2>, grid_for(nt, 256), 256, 0, c->elems.p, c->nE, c->n2e_ptr.p);
+  }
+  int st = scan_exclusive(c, c->n2e_ptr.p, c->n2e_ptr.p, nv);
+  if (st) return st;
+  u32* out = reinterpret_cast<u32*>(c->n2e.p);
+  if (c->dim == 3) {
+    DM_LAUNCH(c, k_n2e_scatter<3>, grid_for(nt, 256), 256, 0, c->elems.p, c->nE, c->n2e_ptr.p,
+              c->fill.p, out);
+  } else {
+    DM_LAUNCH(c, k_n2e_scatter<2>, grid_for(nt, 256), 256, 0, c->elems.p, c->nE, c->n2e_ptr.p,
+              c->fill.p, out);
+  }
+  st = segment_sort_u32(c, out, c->n2e_ptr.p, nv);
+  if (st) return st;
+  c->have_n2e = true;
+  return DM_OK;
+}
+
+int ensure_bedge(dm_ctx* c) {
+  if (c->have_bedge) return DM_OK;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  const int D = c->dim;
+  const int NEB = D == 3 ? 3 : 1;
+  const i64 nv = c->nv, n = c->nB * NEB;
+  DM_CK(c, c->cnt.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, c->fill.ensure(static_cast<size_t>(nv + 1)));
+  DM_CK(c, c->bedge.ensure(static_cast<size_t>(n)));
+  DM_CK(c, c->flag.ensure(4));
+  DM_CK(c, cudaMemsetAsync(c->cnt.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->fill.p, 0, (nv + 1) * sizeof(u32), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->stream));
+  if (D == 3) {
+    DM_LAUNCH(c, k_bedge_count<3>, grid_for(n, 256), 256, 0, c->bnd.p, c->nB, c->edges.p, c->os.p,
+              nv, c->cnt.p, c->flag.p);
+  } else {
+    DM_LAUNCH(c, k_bedge_count<2>, grid_for(n, 256), 256, 0, c->bnd.p, c->nB, c->edges.p, c->os.p,
+              nv, c->cnt.p, c->flag.p);
+  }
+  int f = 0;
+  int st = read_flag(c, &f);
+  if (st) return st;
+  if (f)
+    return fail(c, DM_ERR_EDGE_ABSENT, "boundary element references an edge absent from EdgeList");
+  st = scan_exclusive(c, c->cnt.p, c->cnt.p, nv);
+  if (st) return st;
+  if (D == 3) {
+    DM_LAUNCH(c, k_bedge_scatter<3>, grid_for(n, 256), 256, 0, c->bnd.p, c->nB, c->edges.p,
+              c->os.p, nv, c->cnt.p, c->fill.p, c->bedge.p);
+  } else {
+    DM_LAUNCH(c, k_bedge_scatter<2>, grid_for(n, 256), 256, 0, c->bnd.p, c->nB, c->edges.p,
+              c->os.p, nv, c->cnt.p, c->fill.p, c->bedge.p);
+  }
+  st = segment_sort_u64(c, c->bedge.p, c->cnt.p, nv);
+  if (st) return st;
+  c->n_bedge = n;
+  c->have_bedge = true;
+  return DM_OK;
+}
+
+}  // namespace dm
+
+// ------------------------------------------------------------ C-ABI pieces
+extern "C" int dm_edge_of(dm_ctx* c, const int32_t* a, const int32_t* b, int64_t n, int32_t* out) {
+  using namespace dm;
+  if (!c || (n > 0 && (!a || !b || !out)) || n < 0) return DM_ERR_INVALID_ARG;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "dm_edge_of before dm_build_edges");
+  if (n == 0) return DM_OK;
+  DevBuf<int32_t> da, db, dout;
+  DM_CK(c, da.ensure(n));
+  DM_CK(c, db.ensure(n));
+  DM_CK(c, dout.ensure(n));
+  DM_CK(c, cudaMemcpyAsync(da.p, a, n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  DM_CK(c, cudaMemcpyAsync(db.p, b, n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  DM_LAUNCH(c, k_edge_of, grid_for(n, 256), 256, 0, c->edges.p, c->os.p, c->nv, da.p, db.p, n,
+            dout.p);
+  DM_CK(c, cudaMemcpyAsync(out, dout.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}

@@ -1,0 +1,332 @@
+// host_api.cpp -- the reference C++ API (include/dualmesh/mesh.hpp, ref
+// proj/include/dualmesh/mesh.hpp) and the SPEC metrics API
+// (include/dualmesh/metrics.hpp) implemented over the C-ABI.
+//
+// Each host thread owns one dm_ctx (C-ABI threading rule).  The functions
+// are pure functions of their arguments, like the reference: every call
+// uploads the mesh it is given.  Status codes become exceptions here and
+// only here: DM_ERR_INVALID_ARG / MESH_EDGE_MISMATCH / EDGE_ABSENT ->
+// std::invalid_argument, everything else -> std::runtime_error.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+
+#include "dm_capi.h"
+#include "dualmesh/mesh.hpp"
+#include "dualmesh/metrics.hpp"
+
+namespace dualmesh {
+namespace {
+
+struct ThreadCtx {
+  dm_ctx* c = nullptr;
+  ~ThreadCtx() { dm_destroy(c); }
+};
+
+void check(dm_ctx* c, int st, const char* what) {
+  if (st == DM_OK) return;
+  std::string msg = std::string(what) + ": " + dm_status_string(st) + " (" + dm_last_error(c) + ")";
+  if (st == DM_ERR_INVALID_ARG || st == DM_ERR_MESH_EDGE_MISMATCH || st == DM_ERR_EDGE_ABSENT)
+    throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+dm_ctx* ctx() {
+  thread_local ThreadCtx t;
+  if (!t.c) {
+    const char* dev = std::getenv("DUALMESH_DEVICE");
+    int st = dm_create(&t.c, dev ? std::atoi(dev) : 0);
+    if (st != DM_OK) {
+      std::string msg = std::string("dualmesh: no usable sm_100a device: ") + dm_last_error(t.c);
+      dm_destroy(t.c);
+      t.c = nullptr;
+      throw std::runtime_error(msg);
+    }
+  }
+  return t.c;
+}
+
+dm_ctx* upload(const Mesh& m) {
+  dm_ctx* c = ctx();
+  if (m.dim != 2 && m.dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+  check(c,
+        dm_set_mesh(c, m.dim, m.coords.data(), static_cast<int64_t>(m.num_nodes()),
+                    m.elements.data(), static_cast<int64_t>(m.num_elements()), m.boundary.data(),
+                    static_cast<int64_t>(m.num_boundary())),
+        "dm_set_mesh");
+  return c;
+}
+
+// Upload + GPU edge extraction, then confirm the caller's EdgeList is the
+// one this mesh produces ("mesh/edge mismatch").
+dm_ctx* upload_with_edges(const Mesh& m, const EdgeList& given) {
+  dm_ctx* c = upload(m);
+  int64_t ne = 0;
+  check(c, dm_build_edges(c, &ne), "dm_build_edges");
+  if (static_cast<std::size_t>(ne) != given.size() ||
+      given.origin_start.size() != m.num_nodes() + 1)
+    throw std::invalid_argument("mesh/edge mismatch");
+  std::vector<int32_t> e(2 * static_cast<std::size_t>(ne));
+  check(c, dm_get_edges(c, e.data(), nullptr), "dm_get_edges");
+  for (std::size_t i = 0; i < given.size(); ++i)
+    if (e[2 * i] != given.edges[i][0] || e[2 * i + 1] != given.edges[i][1])
+      throw std::invalid_argument("mesh/edge mismatch");
+  return c;
+}
+
+const int kOpp[4][3] = {{1, 2, 3}, {0, 3, 2}, {0, 1, 3}, {0, 2, 1}};  // ref mesh.cpp:15
+
+Vec cross(const double* u, const double* v) {
+  return {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- mesh.hpp
+Index EdgeList::edge_of(Index a, Index b) const {
+  // Host lookup on the host-resident list (same contract as ref
+  // mesh.cpp:58-73); batched device lookups go through dm_edge_of.
+  if (a > b) std::swap(a, b);
+  if (a < 0 || static_cast<std::size_t>(a) + 1 >= origin_start.size()) return -1;
+  std::size_t lo = origin_start[static_cast<std::size_t>(a)];
+  const std::size_t end = origin_start[static_cast<std::size_t>(a) + 1];
+  std::size_t hi = end;
+  while (lo < hi) {
+    const std::size_t mid = lo + (hi - lo) / 2;
+    if (edges[mid][1] < b) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < end && edges[lo][1] == b) ? static_cast<Index>(lo) : -1;
+}
+
+EdgeList build_edges(const Mesh& mesh) {
+  dm_ctx* c = upload(mesh);
+  int64_t ne = 0;
+  check(c, dm_build_edges(c, &ne), "dm_build_edges");
+  EdgeList out;
+  out.edges.resize(static_cast<std::size_t>(ne));
+  std::vector<uint64_t> os(mesh.num_nodes() + 1);
+  check(c, dm_get_edges(c, reinterpret_cast<int32_t*>(out.edges.data()), os.data()),
+        "dm_get_edges");
+  out.origin_start.assign(os.begin(), os.end());
+  return out;
+}
+
+double element_volume(const Mesh& mesh, std::size_t e) {
+  const Index* el = mesh.element(e);
+  if (mesh.dim == 2) {
+    const double *a = mesh.node(el[0]), *b = mesh.node(el[1]), *c = mesh.node(el[2]);
+    return 0.5 * ((b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0]));
+  }
+  const double *a = mesh.node(el[0]), *b = mesh.node(el[1]), *c = mesh.node(el[2]),
+               *d = mesh.node(el[3]);
+  const double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+  const double v[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+  const Vec uv = cross(u, v);
+  return (uv[0] * (d[0] - a[0]) + uv[1] * (d[1] - a[1]) + uv[2] * (d[2] - a[2])) / 6.0;
+}
+
+Vec opposite_face_normal(const Mesh& mesh, std::size_t e, int i) {
+  const Index* el = mesh.element(e);
+  if (mesh.dim == 2) {
+    const double *p = mesh.node(el[(i + 1) % 3]), *q = mesh.node(el[(i + 2) % 3]);
+    return {q[1] - p[1], p[0] - q[0], 0.0};
+  }
+  const double *p0 = mesh.node(el[kOpp[i][0]]), *p1 = mesh.node(el[kOpp[i][1]]),
+               *p2 = mesh.node(el[kOpp[i][2]]);
+  const double d1[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+  const double d2[3] = {p2[0] - p0[0], p2[1] - p0[1], p2[2] - p0[2]};
+  const Vec c = cross(d1, d2);
+  return {0.5 * c[0], 0.5 * c[1], 0.5 * c[2]};
+}
+
+Vec boundary_normal(const Mesh& mesh, std::size_t b) {
+  const Index* bl = mesh.boundary_element(b);
+  if (mesh.dim == 2) {
+    const double *j = mesh.node(bl[0]), *k = mesh.node(bl[1]);
+    return {k[1] - j[1], j[0] - k[0], 0.0};
+  }
+  const double *j = mesh.node(bl[0]), *r = mesh.node(bl[1]), *l = mesh.node(bl[2]);
+  const double d1[3] = {r[0] - j[0], r[1] - j[1], r[2] - j[2]};
+  const double d2[3] = {l[0] - j[0], l[1] - j[1], l[2] - j[2]};
+  const Vec c = cross(d1, d2);
+  return {0.5 * c[0], 0.5 * c[1], 0.5 * c[2]};
+}
+
+ValidationOutcome validate_mesh(const Mesh& mesh) {
+  ValidationOutcome out;
+  if (mesh.dim != 2 && mesh.dim != 3) {
+    out.violations.push_back("dim must be 2 or 3, got " + std::to_string(mesh.dim));
+    return out;
+  }
+  if (mesh.coords.size() % static_cast<std::size_t>(mesh.dim) != 0)
+    out.violations.push_back("coordinate array length is not a multiple of dim");
+  if (mesh.elements.size() % static_cast<std::size_t>(mesh.dim + 1) != 0)
+    out.violations.push_back("element array length is not a multiple of dim+1");
+  if (mesh.boundary.size() % static_cast<std::size_t>(mesh.dim) != 0)
+    out.violations.push_back("boundary array length is not a multiple of dim");
+  if (!out.violations.empty()) return out;
+  dm_ctx* c = upload(mesh);
+  std::vector<int8_t> signs(mesh.num_elements());
+  int64_t counts[DM_VCOUNT] = {0};
+  int64_t exposed = 0;
+  check(c, dm_validate(c, signs.data(), counts, &exposed), "dm_validate");
+  auto ids = [&](int kind) {
+    std::vector<int64_t> v(static_cast<std::size_t>(counts[kind]));
+    int64_t n = 0;
+    if (!v.empty()) check(c, dm_validate_list(c, kind, v.data(), counts[kind], &n), "dm_validate_list");
+    return v;
+  };
+  const bool range_bad = counts[DM_V_OUT_OF_RANGE_ELEM] + counts[DM_V_OUT_OF_RANGE_BND] > 0;
+  for (int64_t e : ids(DM_V_OUT_OF_RANGE_ELEM))
+    out.violations.push_back("out-of-range node index in element " + std::to_string(e + 1));
+  for (int64_t b : ids(DM_V_OUT_OF_RANGE_BND))
+    out.violations.push_back("out-of-range node index in boundary element " + std::to_string(b + 1));
+  if (range_bad) return out;
+  out.volume_signs.assign(signs.begin(), signs.end());
+  for (int64_t e : ids(DM_V_NONPOSITIVE))
+    out.violations.push_back("nonpositive volume, element " + std::to_string(e + 1));
+  for (int64_t e : ids(DM_V_FACE_OVERSHARED))
+    out.violations.push_back("face shared by more than two elements, element " +
+                             std::to_string(e + 1));
+  // Boundary classes are reported in facet order, interleaved as in the
+  // reference loop: merge the per-class lists (payload: b << 32 | aux).
+  std::vector<std::pair<int64_t, std::string>> bmsgs;
+  for (int64_t q : ids(DM_V_BND_NOT_FACE))
+    bmsgs.push_back({q >> 32, "boundary element " + std::to_string((q >> 32) + 1) +
+                                  " is not a face of any element"});
+  for (int64_t q : ids(DM_V_BND_INTERIOR))
+    bmsgs.push_back({q >> 32, "boundary element " + std::to_string((q >> 32) + 1) +
+                                  " matches an interior face of element " +
+                                  std::to_string((q & 0xffffffff) + 1)});
+  for (int64_t q : ids(DM_V_BND_DUPLICATE))
+    bmsgs.push_back({q >> 32, "duplicate boundary element " + std::to_string((q >> 32) + 1)});
+  for (int64_t q : ids(DM_V_BND_INWARD))
+    bmsgs.push_back({q >> 32, "boundary element " + std::to_string((q >> 32) + 1) +
+                                  " has inward orientation (element " +
+                                  std::to_string((q & 0xffffffff) + 1) + ")"});
+  std::stable_sort(bmsgs.begin(), bmsgs.end(),
+                   [](const auto& x, const auto& y) { return x.first < y.first; });
+  for (auto& m : bmsgs) out.violations.push_back(std::move(m.second));
+  if (exposed > 0)
+    out.violations.push_back(std::to_string(exposed) +
+                             " mesh-boundary face(s) missing from the boundary list");
+  return out;
+}
+
+std::vector<Index> derive_boundary_faces(const Mesh& mesh) {
+  dm_ctx* c = upload(mesh);
+  int64_t n = 0;
+  check(c, dm_derive_boundary(c, &n), "dm_derive_boundary");
+  std::vector<Index> out(static_cast<std::size_t>(n) * static_cast<std::size_t>(mesh.dim));
+  if (n) check(c, dm_get_derived_boundary(c, out.data()), "dm_get_derived_boundary");
+  return out;
+}
+
+double max_face_area(const Mesh& mesh) {
+  double v = 0.0;
+  dm_ctx* c = upload(mesh);
+  check(c, dm_max_face_area(c, &v), "dm_max_face_area");
+  return v;
+}
+
+double max_element_volume(const Mesh& mesh) {
+  double v = 0.0;
+  dm_ctx* c = upload(mesh);
+  check(c, dm_max_element_volume(c, &v), "dm_max_element_volume");
+  return v;
+}
+
+double total_volume(const Mesh& mesh) {
+  double v = 0.0;
+  dm_ctx* c = upload(mesh);
+  check(c, dm_total_volume(c, &v), "dm_total_volume");
+  return v;
+}
+
+std::vector<bool> boundary_node_mask(const Mesh& mesh) {
+  dm_ctx* c = upload(mesh);
+  std::vector<uint8_t> m(mesh.num_nodes());
+  check(c, dm_boundary_node_mask(c, m.data()), "dm_boundary_node_mask");
+  return std::vector<bool>(m.begin(), m.end());
+}
+
+// ---------------------------------------------------------------- metrics.hpp
+namespace {
+LumpedNavField fetch_navs(dm_ctx* c, const Mesh& mesh, std::size_t ne) {
+  LumpedNavField f;
+  f.dim = mesh.dim;
+  f.navs.resize(ne * static_cast<std::size_t>(mesh.dim));
+  check(c, dm_get_navs(c, f.navs.data()), "dm_get_navs");
+  return f;
+}
+DualVolumeField fetch_vols(dm_ctx* c, const Mesh& mesh) {
+  DualVolumeField v;
+  v.volumes.resize(mesh.num_nodes());
+  check(c, dm_get_volumes(c, v.volumes.data()), "dm_get_volumes");
+  return v;
+}
+void put_navs(dm_ctx* c, const Mesh& mesh, const EdgeList& edges, const LumpedNavField& navs) {
+  if (navs.dim != mesh.dim || navs.size() != edges.size())
+    throw std::invalid_argument("field/edge-list mismatch");
+  check(c, dm_put_navs(c, navs.navs.data()), "dm_put_navs");
+}
+}  // namespace
+
+LumpedNavField lumped_navs_traditional(const Mesh& mesh, const EdgeList& edges) {
+  dm_ctx* c = upload_with_edges(mesh, edges);
+  check(c, dm_navs(c, DM_NAV_TRADITIONAL, DM_VARIANT_GATHER), "dm_navs");
+  return fetch_navs(c, mesh, edges.size());
+}
+
+LumpedNavField lumped_navs_dualfree(const Mesh& mesh, const EdgeList& edges) {
+  dm_ctx* c = upload_with_edges(mesh, edges);
+  check(c, dm_navs(c, DM_NAV_DUALFREE, DM_VARIANT_GATHER), "dm_navs");
+  return fetch_navs(c, mesh, edges.size());
+}
+
+DualVolumeField dual_volumes_edge_based(const Mesh& mesh, const EdgeList& edges,
+                                        const LumpedNavField& navs) {
+  dm_ctx* c = upload_with_edges(mesh, edges);
+  put_navs(c, mesh, edges, navs);
+  check(c, dm_volumes(c, DM_VOL_EDGE), "dm_volumes");
+  return fetch_vols(c, mesh);
+}
+
+DualVolumeField dual_volumes_element_based(const Mesh& mesh) {
+  dm_ctx* c = upload(mesh);
+  check(c, dm_volumes(c, DM_VOL_ELEMENT), "dm_volumes");
+  return fetch_vols(c, mesh);
+}
+
+MetricsResult compute_metrics(const Mesh& mesh, NavAlgo nav_algo, VolAlgo vol_algo) {
+  MetricsResult r;
+  r.edges = build_edges(mesh);  // uploads the mesh and leaves the edges resident
+  dm_ctx* c = ctx();
+  check(c, dm_navs(c, static_cast<int>(nav_algo), DM_VARIANT_GATHER), "dm_navs");
+  check(c, dm_volumes(c, static_cast<int>(vol_algo)), "dm_volumes");
+  r.navs = fetch_navs(c, mesh, r.edges.size());
+  r.volumes = fetch_vols(c, mesh);
+  return r;
+}
+
+double check_closure(const Mesh& mesh, const EdgeList& edges, const LumpedNavField& navs) {
+  dm_ctx* c = upload_with_edges(mesh, edges);
+  put_navs(c, mesh, edges, navs);
+  double r = 0.0, ri = 0.0;
+  check(c, dm_check_closure(c, &r, &ri), "dm_check_closure");
+  return r;
+}
+
+double check_total_volume(const Mesh& mesh, const DualVolumeField& volumes) {
+  if (volumes.size() != mesh.num_nodes()) throw std::invalid_argument("field/mesh mismatch");
+  dm_ctx* c = upload(mesh);
+  check(c, dm_put_volumes(c, volumes.volumes.data()), "dm_put_volumes");
+  double rel = 0.0;
+  check(c, dm_check_total_volume(c, &rel, nullptr, nullptr), "dm_check_total_volume");
+  return rel;
+}
+
+}  // namespace dualmesh

@@ -1,0 +1,207 @@
+// primitives.cu -- device scan and segmented sort used by edge extraction
+// and by the derived CSR structures.  Hand-written (no CUB/Thrust).
+#include "dm_internal.cuh"
+
+namespace dm {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanPerThread = 8;
+constexpr int kScanBlock = kScanThreads * kScanPerThread;
+
+// Block-local exclusive scan; writes the block total to bsum[blockIdx.x].
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_blocks(const u32* in, u32* out, u32* bsum, i64 n) {
+  __shared__ u32 wsum[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 base = static_cast<i64>(blockIdx.x) * kScanBlock + threadIdx.x * kScanPerThread;
+  u32 v[kScanPerThread];
+  u32 tot = 0;
+#pragma unroll
+  for (int q = 0; q < kScanPerThread; ++q) {
+    const i64 i = base + q;
+    v[q] = i < n ? in[i] : 0u;
+    tot += v[q];
+  }
+  u32 incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u32 w = lane < kScanThreads / 32 ? wsum[lane] : 0u;
+    u32 wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < kScanThreads / 32) wsum[lane] = wi - w;  // exclusive warp offsets
+    if (lane == kScanThreads / 32 - 1) bsum[blockIdx.x] = wi;
+  }
+  __syncthreads();
+  u32 run = incl - tot + wsum[warp];
+#pragma unroll
+  for (int q = 0; q < kScanPerThread; ++q) {
+    const i64 i = base + q;
+    if (i < n) out[i] = run;
+    run += v[q];
+  }
+}
+
+__global__ void k_scan_add(u32* out, const u32* boff, i64 n) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += boff[i / kScanBlock];
+}
+
+__global__ void k_copy_one(u32* dst, const u32* src) { *dst = *src; }
+
+int scan_rec(dm_ctx* c, const u32* in, u32* out, i64 n, u32* tmp) {
+  const i64 nb = (n + kScanBlock - 1) / kScanBlock;
+  if (n == 0) {
+    DM_CK(c, cudaMemsetAsync(out, 0, sizeof(u32), c->stream));
+    return DM_OK;
+  }
+  u32* lvl = tmp;  // nb + 1 entries
+  DM_LAUNCH(c, k_scan_blocks, static_cast<unsigned>(nb), kScanThreads, 0, in, out, lvl, n);
+  if (nb > 1) {
+    int st = scan_rec(c, lvl, lvl, nb, tmp + nb + 1);
+    if (st) return st;
+    DM_LAUNCH(c, k_scan_add, grid_for(n, 256), 256, 0, out, lvl, n);
+    DM_LAUNCH(c, k_copy_one, 1, 1, 0, out + n, lvl + nb);
+  } else {
+    DM_LAUNCH(c, k_copy_one, 1, 1, 0, out + n, lvl);
+  }
+  return DM_OK;
+}
+
+// ------------------------------------------------------------ segment sort
+template <typename K>
+__device__ __forceinline__ K key_max();
+template <>
+__device__ __forceinline__ u64 key_max<u64>() { return ~0ull; }
+template <>
+__device__ __forceinline__ u32 key_max<u32>() { return ~0u; }
+
+template <typename K, bool kWarp>
+__device__ void bitonic(K* buf, int P, int tid, int nthr) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += nthr) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          K a = buf[i], b = buf[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            buf[i] = b;
+            buf[ixj] = a;
+          }
+        }
+      }
+      if (kWarp) __syncwarp();
+      else __syncthreads();
+    }
+}
+
+constexpr int kWarpSeg = 128;
+constexpr int kBlockSeg = 4096;
+
+template <typename K>
+__global__ void __launch_bounds__(256)
+    k_segsort_warp(K* data, const u32* seg, i64 nseg, u32* big, int* nbig) {
+  __shared__ K sbuf[8][kWarpSeg];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 s = static_cast<i64>(blockIdx.x) * 8 + warp;
+  if (s >= nseg) return;
+  const u32 b = seg[s];
+  const int n = static_cast<int>(seg[s + 1] - b);
+  if (n <= 1) return;
+  if (n > kWarpSeg) {
+    if (lane == 0) big[atomicAdd(nbig, 1)] = static_cast<u32>(s);
+    return;
+  }
+  int P = 2;
+  while (P < n) P <<= 1;
+  K* buf = sbuf[warp];
+  for (int i = lane; i < P; i += 32) buf[i] = i < n ? data[b + i] : key_max<K>();
+  __syncwarp();
+  bitonic<K, true>(buf, P, lane, 32);
+  for (int i = lane; i < n; i += 32) data[b + i] = buf[i];
+}
+
+template <typename K>
+__global__ void __launch_bounds__(512)
+    k_segsort_block(K* data, const u32* seg, const u32* big, const int* nbig, int* flag) {
+  extern __shared__ unsigned char smem_raw[];
+  K* buf = reinterpret_cast<K*>(smem_raw);
+  const int count = *nbig;
+  for (int q = blockIdx.x; q < count; q += gridDim.x) {
+    const u32 s = big[q];
+    const u32 b = seg[s];
+    const int n = static_cast<int>(seg[s + 1] - b);
+    if (n > kBlockSeg) {
+      if (threadIdx.x == 0) atomicExch(flag, 1);
+      continue;
+    }
+    int P = 2;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) buf[i] = i < n ? data[b + i] : key_max<K>();
+    __syncthreads();
+    bitonic<K, false>(buf, P, threadIdx.x, blockDim.x);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) data[b + i] = buf[i];
+    __syncthreads();
+  }
+}
+
+template <typename K>
+int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg) {
+  if (nseg <= 0) return DM_OK;
+  DevBuf<u32> big;
+  DM_CK(c, big.ensure(static_cast<size_t>(nseg)));
+  DM_CK(c, c->flag.ensure(4));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
+  int* nbig = c->flag.p + 1;
+  DM_LAUNCH(c, k_segsort_warp<K>, grid_for(nseg, 8), 256, 0, data, seg, nseg, big.p, nbig);
+  const size_t smem = kBlockSeg * sizeof(K);
+  DM_CK(c, cudaFuncSetAttribute(k_segsort_block<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  DM_LAUNCH(c, k_segsort_block<K>, 296, 512, smem, data, seg, big.p, nbig, c->flag.p);
+  int f = 0;
+  int st = read_flag(c, &f);  // also keeps `big` alive until the sort finished
+  if (st) return st;
+  if (f) return fail(c, DM_ERR_UNSUPPORTED, "segment longer than 4096 keys (node valence too high)");
+  return DM_OK;
+}
+
+}  // namespace
+
+int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n) {
+  // temp: sum over levels of (nb+1)
+  i64 need = 0, m = n;
+  do {
+    const i64 nb = (m + kScanBlock - 1) / kScanBlock;
+    need += nb + 1;
+    m = nb;
+  } while (m > 1);
+  DM_CK(c, c->scan_tmp.ensure(static_cast<size_t>(need + 4)));
+  return scan_rec(c, in, out, n, c->scan_tmp.p);
+}
+
+int segment_sort_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg) {
+  return segment_sort<u64>(c, data, seg, nseg);
+}
+int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg) {
+  return segment_sort<u32>(c, data, seg, nseg);
+}
+
+int read_flag(dm_ctx* c, int* value) {
+  DM_CK(c, cudaMemcpyAsync(value, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  return DM_OK;
+}
+
+}  // namespace dm

@@ -1,0 +1,107 @@
+// volumes.cu -- median-dual volumes on the GPU.
+//
+//   K4 edge-based: V_j = (1/(2D)) sum of
+//      s_e over the edges touching j, with s_e = (x_k - x_j).n_jk produced by
+//      the nav kernel.  One thread per node folds its incoming edges (the
+//      transposed CSR, ascending edge id) and then its outgoing row
+//      (origin_start), which is the order in which the serial edge loop of
+//      the oracle updates V_j -- bitwise identical, no atomics.
+//   K6 element-based: V_E per element
+//      (coalesced pass), then one thread per node folds V_E over its
+//      incident elements in ascending id and scales by 1/(D+1).
+#include "geometry.cuh"
+
+namespace dm {
+namespace {
+
+template <int D>
+__global__ void __launch_bounds__(256)
+    k_vol_edge(const u32* __restrict__ in_ptr, const int32_t* __restrict__ in_list,
+               const u32* __restrict__ os, const double* __restrict__ svals, i64 nv,
+               double* __restrict__ V) {
+  const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double acc = 0.0;
+  const u32 ib = in_ptr[v], ie = in_ptr[v + 1];
+  for (u32 q = ib; q < ie; ++q) acc += svals[__ldg(in_list + q)];
+  const u32 ob = os[v], oe = os[v + 1];
+  for (u32 q = ob; q < oe; ++q) acc += svals[q];
+  V[v] = acc * (1.0 / static_cast<double>(2 * D));
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+    k_elem_vol(const int32_t* __restrict__ el, Coords<D> X, i64 nE, double* __restrict__ ve) {
+  const i64 E = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (E >= nE) return;
+  if constexpr (D == 3) {
+    const int4 t = ld_i4(reinterpret_cast<const int4*>(el) + E);
+    ve[E] = evol3(X, t.x, t.y, t.z, t.w);
+  } else {
+    ve[E] = evol2(X, __ldg(el + 3 * E), __ldg(el + 3 * E + 1), __ldg(el + 3 * E + 2));
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+    k_vol_elem(const u32* __restrict__ ptr, const int32_t* __restrict__ n2e,
+               const double* __restrict__ ve, i64 nv, double* __restrict__ V) {
+  const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double acc = 0.0;
+  for (u32 q = ptr[v]; q < ptr[v + 1]; ++q) acc += ve[__ldg(n2e + q)];
+  V[v] = acc * (1.0 / static_cast<double>(D + 1));
+}
+
+}  // namespace
+
+int compute_element_volumes(dm_ctx* c) {
+  DM_CK(c, c->velem.ensure(static_cast<size_t>(c->nE)));
+  if (c->dim == 3) {
+    Coords<3> X{c->x4.p};
+    DM_LAUNCH(c, k_elem_vol<3>, grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE, c->velem.p);
+  } else {
+    Coords<2> X{reinterpret_cast<const double2*>(c->coords.p)};
+    DM_LAUNCH(c, k_elem_vol<2>, grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE, c->velem.p);
+  }
+  return DM_OK;
+}
+
+int volumes_impl(dm_ctx* c, int algo) {
+  const i64 nv = c->nv;
+  DM_CK(c, c->vols.ensure(static_cast<size_t>(nv)));
+  if (algo == DM_VOL_EDGE) {
+    if (!c->have_navs) return fail(c, DM_ERR_STATE, "edge-based volumes need navs first");
+    int st = ensure_incoming(c);
+    if (st) return st;
+    tmark(c, 2);
+    if (c->dim == 3) {
+      DM_LAUNCH(c, k_vol_edge<3>, grid_for(nv, 256), 256, 0, c->in_ptr.p, c->in_list.p, c->os.p,
+                c->svals.p, nv, c->vols.p);
+    } else {
+      DM_LAUNCH(c, k_vol_edge<2>, grid_for(nv, 256), 256, 0, c->in_ptr.p, c->in_list.p, c->os.p,
+                c->svals.p, nv, c->vols.p);
+    }
+    tmark(c, 3);
+  } else if (algo == DM_VOL_ELEMENT) {
+    int st = ensure_n2e(c);
+    if (st) return st;
+    tmark(c, 2);
+    st = compute_element_volumes(c);
+    if (st) return st;
+    if (c->dim == 3) {
+      DM_LAUNCH(c, k_vol_elem<3>, grid_for(nv, 256), 256, 0, c->n2e_ptr.p, c->n2e.p, c->velem.p,
+                nv, c->vols.p);
+    } else {
+      DM_LAUNCH(c, k_vol_elem<2>, grid_for(nv, 256), 256, 0, c->n2e_ptr.p, c->n2e.p, c->velem.p,
+                nv, c->vols.p);
+    }
+    tmark(c, 3);
+  } else {
+    return fail(c, DM_ERR_INVALID_ARG, "unknown volume algorithm");
+  }
+  c->have_vols = true;
+  return DM_OK;
+}
+
+}  // namespace dm

@@ -1,0 +1,162 @@
+"""GPU parity tests: the sm_100a path (through the C-ABI) against the oracle
+and the committed golden fixtures.  Bars (north_star / SURVEY 8(c)):
+edge structures bit-exact; GATHER navs and volumes bitwise equal to the
+serial oracle; SCATTER navs within 1e-12 per edge vector
+(||x_gpu - x_ref||_inf <= 1e-12 ||x_ref||_inf); closure <= 1e-13 scaled;
+|sum V - sum V_E| / sum V_E <= 1e-12."""
+import numpy as np
+import pytest
+
+from paper_2502_00778_b200 import EdgeAbsent, Mesh, meshgen
+from paper_2502_00778_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+DF, TR = _lib.DM_NAV_DUALFREE, _lib.DM_NAV_TRADITIONAL
+GATHER, SCATTER = _lib.DM_VARIANT_GATHER, _lib.DM_VARIANT_SCATTER
+EDGE, ELEM = _lib.DM_VOL_EDGE, _lib.DM_VOL_ELEMENT
+
+
+def per_vector_rel(a, b, dim):
+    a, b = a.reshape(-1, dim), b.reshape(-1, dim)
+    num = np.abs(a - b).max(axis=1)
+    den = np.abs(b).max(axis=1)
+    den = np.where(den == 0, 1.0, den)
+    return float((num / den).max())
+
+
+def run_all(eng, mesh):
+    eng.set_mesh(mesh)
+    eng.build_edges()
+    out = {"edgelist": eng.edges(), "e2l": eng.e2l()}
+    out["inc_ptr"], out["inc"] = eng.incidence()
+    eng.navs(DF, GATHER)
+    out["navs_dualfree"] = eng.get_navs()
+    eng.volumes(EDGE)
+    out["vol_edge"] = eng.get_volumes()
+    eng.volumes(ELEM)
+    out["vol_element"] = eng.get_volumes()
+    eng.navs(TR, GATHER)
+    out["navs_traditional"] = eng.get_navs()
+    eng.navs(DF, SCATTER)
+    out["navs_scatter"] = eng.get_navs()
+    return out
+
+
+def test_fixtures_bit_exact(engine, fixtures, oracle):
+    for name, d in fixtures.items():
+        m = d["mesh_obj"]
+        g = run_all(engine, m)
+        assert g["edgelist"].edges.tolist() == d["ref_edges"], name
+        assert g["edgelist"].origin_start.tolist() == d["ref_origin_start"], name
+        e, o = np.array(d["ref_edges"], np.int32).reshape(-1, 2), np.array(d["ref_origin_start"], np.uint64)
+        np.testing.assert_array_equal(g["navs_dualfree"], oracle.navs_dualfree(m, e, o))
+        np.testing.assert_array_equal(g["navs_traditional"], oracle.navs_traditional(m, e, o))
+        np.testing.assert_array_equal(g["vol_edge"], oracle.volumes_edge(m, e, g["navs_dualfree"]))
+        np.testing.assert_array_equal(g["vol_element"], oracle.volumes_element(m))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_golden_configs_bit_exact(engine, golden_configs, name):
+    gd = golden_configs[name]
+    g = run_all(engine, gd["mesh"])
+    np.testing.assert_array_equal(g["edgelist"].edges, gd["edges"])
+    np.testing.assert_array_equal(g["edgelist"].origin_start, gd["origin_start"])
+    np.testing.assert_array_equal(g["e2l"], gd["e2l"])
+    np.testing.assert_array_equal(g["inc_ptr"], gd["inc_ptr"])
+    np.testing.assert_array_equal(g["inc"], gd["inc"])
+    for k in ("navs_dualfree", "navs_traditional", "vol_edge", "vol_element"):
+        np.testing.assert_array_equal(g[k], gd[k], err_msg=k)
+    assert per_vector_rel(g["navs_scatter"], gd["navs_dualfree"], gd["mesh"].dim) <= 1e-12
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 1), ("C2", 1), ("C3", 2), ("C4", 2)])
+def test_live_oracle_parity(engine, oracle, name, scale):
+    m = meshgen.baseline_config(name, scale)
+    g = run_all(engine, m)
+    e, o = oracle.build_edges(m)
+    np.testing.assert_array_equal(g["edgelist"].edges, e)
+    np.testing.assert_array_equal(g["edgelist"].origin_start, o)
+    e2l, ip, inc = oracle.edge_maps(m, e, o)
+    np.testing.assert_array_equal(g["e2l"], e2l)
+    np.testing.assert_array_equal(g["inc_ptr"], ip)
+    np.testing.assert_array_equal(g["inc"], inc)
+    nd = oracle.navs_dualfree(m, e, o, e2l)
+    np.testing.assert_array_equal(g["navs_dualfree"], nd)
+    np.testing.assert_array_equal(g["navs_traditional"], oracle.navs_traditional(m, e, o, e2l))
+    np.testing.assert_array_equal(g["vol_edge"], oracle.volumes_edge(m, e, nd))
+    np.testing.assert_array_equal(g["vol_element"], oracle.volumes_element(m))
+    assert per_vector_rel(g["navs_scatter"], nd, m.dim) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_properties(engine, name):
+    """BASELINE sizes: size-independent identities + determinism."""
+    m = meshgen.baseline_config(name)
+    engine.set_mesh(m)
+    ne = engine.build_edges()
+    if name == "C5":
+        assert ne == 118031104 and m.num_nodes() == 16974593
+    engine.navs(DF, GATHER)
+    engine.volumes(EDGE)
+    r, ri = engine.check_closure()
+    assert r <= 1e-13 and ri <= 1e-13
+    rel, sv, se = engine.check_total_volume()
+    assert rel <= 1e-12
+    if name != "C4":
+        assert abs(sv - 1.0) <= 1e-12  # unit cube, PAPER §4.3
+    n1, v1 = engine.get_navs(), engine.get_volumes()
+    engine.navs(DF, GATHER)
+    engine.volumes(EDGE)
+    np.testing.assert_array_equal(engine.get_navs(), n1)  # SPEC.md:206 determinism
+    np.testing.assert_array_equal(engine.get_volumes(), v1)
+    engine.navs(DF, SCATTER)
+    assert per_vector_rel(engine.get_navs(), n1, m.dim) <= 1e-12
+    engine.navs(TR, GATHER)
+    nt = engine.get_navs()
+    scale = engine.max_face_area()
+    assert np.abs(nt - n1).max() <= 1e-13 * scale
+
+
+def test_corrupt_hook_detected(engine):
+    m = meshgen.tet_cube(16, amp=0.2, seed=42)
+    engine.set_mesh(m)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    assert engine.check_closure()[0] <= 1e-13
+    engine.corrupt_nav(123, 1e-3)
+    assert engine.check_closure()[0] >= 1e-4
+
+
+def test_errors(engine):
+    m = meshgen.tet_cube(2)
+    engine.set_mesh(m)
+    with pytest.raises(Exception):
+        engine.navs(DF, GATHER)  # before build_edges
+    bad = Mesh(3, m.coords, m.elements, np.array([0, 26, 13], np.int32))  # not a mesh edge
+    engine.set_mesh(bad)
+    engine.build_edges()
+    with pytest.raises(EdgeAbsent):
+        engine.navs(DF, GATHER)
+
+
+def test_edge_of_and_helpers(engine, oracle):
+    m = meshgen.baseline_config("C2", 4)
+    engine.set_mesh(m)
+    engine.build_edges()
+    el = engine.edges()
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, m.num_nodes(), 5000).astype(np.int32)
+    b = rng.integers(0, m.num_nodes(), 5000).astype(np.int32)
+    a[:2500] = el.edges[:2500, 1]  # reversed present pairs
+    b[:2500] = el.edges[:2500, 0]
+    got = engine.edge_of(a, b)
+    want = np.array([el.edge_of(int(x), int(y)) for x, y in zip(a, b)])
+    np.testing.assert_array_equal(got, want)
+    assert engine.max_face_area() == oracle.max_face_area(m)
+    assert engine.max_element_volume() == oracle.max_element_volume(m)
+    assert abs(engine.total_volume() - 1.0) <= 1e-14
+    mask = engine.boundary_node_mask()
+    want_mask = np.zeros(m.num_nodes(), bool)
+    want_mask[m.boundary] = True
+    np.testing.assert_array_equal(mask, want_mask)
