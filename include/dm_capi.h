@@ -39,9 +39,11 @@ extern "C" {
 #define DM_VOL_EDGE 0        /* SPEC.md:170-178 */
 #define DM_VOL_ELEMENT 1     /* SPEC.md:180-188 */
 /* Element-loop variants (north_star (b)). */
-#define DM_VARIANT_GATHER 0  /* deterministic CSR gather, bitwise = serial oracle */
-#define DM_VARIANT_SCATTER 1 /* fp64 atomics (REDG.F64), order nondeterministic */
-#define DM_VARIANT_ROWS 2    /* node-row staged gather, bitwise = serial oracle */
+#define DM_VARIANT_GATHER 0       /* ring-walk gather (default): deterministic, <=1e-12 */
+#define DM_VARIANT_SCATTER 1      /* fp64 atomics (REDG.F64), order nondeterministic */
+#define DM_VARIANT_GATHER_ELEM 2  /* element-id CSR gather + conn lookup, bitwise */
+#define DM_VARIANT_GATHER_FACES 3 /* face-list CSR gather, bitwise */
+#define DM_VARIANT_GATHER_EXACT 4 /* row-table CSR gather, bitwise = serial oracle */
 
 typedef struct dm_ctx dm_ctx;
 
@@ -153,6 +155,10 @@ int dm_sync(dm_ctx* ctx);
 int dm_set_timing(dm_ctx* ctx, int enable);
 int dm_get_timings(dm_ctx* ctx, float* ms, int n);
 int64_t dm_kernel_launches(const dm_ctx* ctx);
+/* Which element-loop kernels the plan enables: info[0] ring path built,
+ * [1] ring path usable, [2] row tables built, [3] row tables usable,
+ * [4] max tile node count (ring path), [5] failure flag of the ring build. */
+int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
 /* Pinned host memory for end-to-end transfers. */
 int dm_host_alloc(size_t bytes, void** ptr);
 int dm_host_free(void* ptr);

@@ -40,6 +40,9 @@ DM_VOL_EDGE = 0
 DM_VOL_ELEMENT = 1
 DM_VARIANT_GATHER = 0
 DM_VARIANT_SCATTER = 1
+DM_VARIANT_GATHER_ELEM = 2
+DM_VARIANT_GATHER_FACES = 3
+DM_VARIANT_GATHER_EXACT = 4
 
 DM_VCOUNT = 8
 
@@ -82,6 +85,7 @@ CAPI = {
     "dm_set_timing": (C.c_int, [P, C.c_int]),
     "dm_get_timings": (C.c_int, [P, FP, C.c_int]),
     "dm_kernel_launches": (C.c_int64, [P]),
+    "dm_plan_info": (C.c_int, [P, I64P]),
     "dm_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(P)]),
     "dm_host_free": (C.c_int, [P]),
 }

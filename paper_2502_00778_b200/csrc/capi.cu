@@ -1,5 +1,6 @@
 // capi.cu -- the extern "C" surface of libdualmesh.so (include/dm_capi.h):
 // context lifetime, mesh upload, result download, timing and plumbing.
+#include <cstdlib>
 #include <cstring>
 
 #include "dm_internal.cuh"
@@ -27,7 +28,7 @@ int check_device(dm_ctx* c) {
 }
 
 void drop_derived(dm_ctx* c) {
-  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = false;
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_tables = c->have_rings = false;
   c->have_navs = c->have_vols = false;
   c->navs_algo = -1;
   c->ne = 0;
@@ -57,6 +58,7 @@ int dm_create(dm_ctx** out, int device) {
   *out = nullptr;
   auto* c = new dm_ctx;
   c->device = device;
+  if (const char* g = std::getenv("DUALMESH_GATHER_CFG")) c->gather_cfg = std::atoi(g);
   int st = check_device(c);
   if (st == DM_OK) {
     cudaError_t e = cudaSetDevice(device);
@@ -322,6 +324,18 @@ int dm_get_timings(dm_ctx* c, float* ms, int n) {
 }
 
 int64_t dm_kernel_launches(const dm_ctx* c) { return c ? c->launches : -1; }
+
+int dm_plan_info(dm_ctx* c, int64_t info[8]) {
+  if (!c || !info) return DM_ERR_INVALID_ARG;
+  for (int i = 0; i < 8; ++i) info[i] = 0;
+  info[0] = c->have_rings;
+  info[1] = c->ring_ok;
+  info[2] = c->have_tables;
+  info[3] = c->table_ok;
+  info[4] = c->ring_max_nodes;
+  info[5] = c->ring_fail;
+  return DM_OK;
+}
 
 int dm_host_alloc(size_t bytes, void** ptr) {
   if (!ptr) return DM_ERR_INVALID_ARG;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 #include <cstdio>
 #include <string>
 
@@ -71,6 +72,7 @@ struct dm_ctx {
   dm::DevBuf<int2> edges;
   dm::DevBuf<dm::u32> os;  // origin_start (32-bit on device)
   dm::DevBuf<int32_t> e2l, inc_ptr, inc;
+  dm::DevBuf<int2> ifl;  // face-list incidence, same order as inc (edges.cu make_ifl)
   // derived: incoming-edge CSR per node, boundary (edge,facet) pairs, node->element CSR
   bool have_in = false;
   dm::DevBuf<dm::u32> in_ptr;
@@ -78,6 +80,18 @@ struct dm_ctx {
   bool have_bedge = false;
   dm::i64 n_bedge = 0;
   dm::DevBuf<dm::u64> bedge;
+  dm::DevBuf<dm::u32> tile_bptr;  // bedge slice per kTileEdges-edge tile
+  bool have_tables = false, table_ok = false;
+  dm::DevBuf<dm::u32> adj_ptr;
+  dm::DevBuf<int32_t> adj;
+  dm::DevBuf<uint16_t> codes;  // tables.cu
+  dm::DevBuf<int4> tile_meta;  // 2 per tile: {A0,A1,P0,P1}, {j0,jl,0,0}
+  bool have_rings = false, ring_ok = false;
+  dm::i64 ring_max_nodes = 0, ring_fail = 0;
+  dm::DevBuf<int32_t> tnodes;      // kTileNodeCap per tile (rings.cu)
+  dm::DevBuf<dm::u32> tnode_cnt;
+  dm::DevBuf<uint16_t> rcodes;     // n+3 per edge at inc_ptr[e] + 3e
+  dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU, 0}
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
   dm::DevBuf<int32_t> n2e;
@@ -102,6 +116,9 @@ struct dm_ctx {
   dm::DevBuf<int32_t> derived;
   dm::DevBuf<dm::i64> vlist;  // first offending ids per class
   dm::i64 vlist_n[DM_VCOUNT] = {0};
+
+  // tuning knob for the GATHER kernel shape (env DUALMESH_GATHER_CFG)
+  int gather_cfg = 0;
 
   // timing
   bool timing = false;
@@ -136,6 +153,12 @@ inline int fail(dm_ctx* c, int code, const std::string& msg) {
     }                                                                                 \
   } while (0)
 
+// Edges per CTA tile of the edge-owned kernels (navs gather / finalize).
+constexpr int kTileEdges = 256;
+// Ring path (rings.cu): unique nodes per tile, incidences per edge.
+constexpr int kTileNodeCap = 1536;
+constexpr int kRingMax = 24;
+
 inline unsigned grid_for(i64 n, int per_block) {
   return static_cast<unsigned>((n + per_block - 1) / per_block);
 }
@@ -143,12 +166,35 @@ inline unsigned grid_for(i64 n, int per_block) {
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ d4 ld_d4(const d4* p) {
   d4 r;
-  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
                : "l"(p));
   return r;
 }
+// x, y, z of a padded node without the pad word (6 registers instead of 8).
+__device__ __forceinline__ d4 ld_d3(const d4* p) {
+  d4 r;
+  asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  asm("ld.global.nc.f64 %0, [%1+16];" : "=d"(r.z) : "l"(p));
+  r.w = 0.0;
+  return r;
+}
 __device__ __forceinline__ double2 ld_d2(const double2* p) { return __ldg(p); }
+
+// cp.async (LDGSTS) helpers: global -> shared without a register round trip.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
 __device__ __forceinline__ int4 ld_i4(const int4* p) { return __ldg(p); }
 
 // Select el[i] for a runtime i in 0..3 without local-memory indexing.
@@ -202,6 +248,8 @@ int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg);
 int ensure_incoming(dm_ctx* c);
 int ensure_bedge(dm_ctx* c);
 int ensure_n2e(dm_ctx* c);
+int ensure_tables(dm_ctx* c);
+int ensure_rings(dm_ctx* c);
 int build_edges_impl(dm_ctx* c);
 int navs_impl(dm_ctx* c, int algo, int variant);
 int volumes_impl(dm_ctx* c, int algo);

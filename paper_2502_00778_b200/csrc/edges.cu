@@ -86,10 +86,34 @@ __global__ void k_count_unique(const u64* items, const u32* bstart, i64 nv, u32*
   if (lane == 0) ucnt[j] = total;
 }
 
-// Warp per bucket: emit edges, inc_ptr, inc and e2l.
-template <int L>
-__global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 nv, int2* edges,
-                       int32_t* inc_ptr, int32_t* inc, int32_t* e2l) {
+// Face-list incidence entry for element E seen from its local edge l:
+//   x = node at il | ij << 30,  y = node at ir | ik << 30   (3D)
+//   x = node at im | ij << 30,  y = ik << 30                 (2D)
+// where ij / ik are the local slots of the origin j = min and of k, and
+// il < ir (3D) / im (2D) are the remaining local slots.  With x_j and x_k
+// known per edge, this is everything the dual-free and traditional
+// contributions need (geometry.cuh), in the reference's local order.
+template <int D>
+__device__ __forceinline__ int2 make_ifl(const int32_t* el, int E, int l) {
+  int v[4];
+  load_elem<D>(el, E, v);
+  int la, lb;
+  local_edge<D>(l, la, lb);
+  const int ij = v[la] < v[lb] ? la : lb, ik = v[la] < v[lb] ? lb : la;
+  if (D == 3) {
+    const unsigned rest = 0xFu & ~((1u << ij) | (1u << ik));
+    const int il = __ffs(rest) - 1, ir = __ffs(rest & (rest - 1)) - 1;
+    return make_int2(v[il] | (ij << 30), v[ir] | (ik << 30));
+  }
+  const int im = 3 - la - lb;
+  return make_int2(v[im] | (ij << 30), ik << 30);
+}
+
+// Warp per bucket: emit edges, inc_ptr, inc, e2l and the face-list incidence.
+template <int D, int L>
+__global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 nv,
+                       const int32_t* el, int2* edges, int32_t* inc_ptr, int32_t* inc,
+                       int32_t* e2l, int2* ifl) {
   const int lane = threadIdx.x & 31;
   const i64 j = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (j >= nv) return;
@@ -115,6 +139,7 @@ __global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 n
       }
       inc[b + i] = static_cast<int32_t>(val / L);
       e2l[val] = id;
+      ifl[b + i] = make_ifl<D>(el, static_cast<int>(val / L), static_cast<int>(val % L));
     }
     id_base += __popc(hm);
   }
@@ -128,9 +153,9 @@ int build_edges_impl(dm_ctx* c) {
   const int D = c->dim;
   const int L = D == 3 ? 6 : 3;
   const i64 M = static_cast<i64>(L) * c->nE;
-  if (M >= (1ll << 31) || c->nv >= (1ll << 31))
+  if (M >= (1ll << 31) || c->nv >= (1ll << 30))
     return fail(c, DM_ERR_UNSUPPORTED, "mesh exceeds the 32-bit item space of the device layout");
-  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = false;
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_tables = c->have_rings = false;
   c->have_navs = c->have_vols = false;
   const i64 nv = c->nv;
 
@@ -167,12 +192,13 @@ int build_edges_impl(dm_ctx* c) {
   DM_CK(c, c->inc_ptr.ensure(static_cast<size_t>(c->ne + 1)));
   DM_CK(c, c->inc.ensure(static_cast<size_t>(M)));
   DM_CK(c, c->e2l.ensure(static_cast<size_t>(M)));
+  DM_CK(c, c->ifl.ensure(static_cast<size_t>(M)));
   if (D == 3) {
-    DM_LAUNCH(c, k_emit<6>, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p, nv,
-              c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p);
+    DM_LAUNCH(c, (k_emit<3, 6>), grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p,
+              nv, c->elems.p, c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p, c->ifl.p);
   } else {
-    DM_LAUNCH(c, k_emit<3>, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p, nv,
-              c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p);
+    DM_LAUNCH(c, (k_emit<2, 3>), grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p,
+              nv, c->elems.p, c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p, c->ifl.p);
   }
   DM_LAUNCH(c, k_set_i32, 1, 1, 0, c->inc_ptr.p + c->ne, static_cast<int32_t>(M));
   DM_CK(c, cudaStreamSynchronize(c->stream));
@@ -253,6 +279,19 @@ __global__ void k_bedge_scatter(const int32_t* bnd, i64 nB, const int2* edges, c
   if (id < 0) return;
   const int j = a < c ? a : c;
   out[start[j] + atomicAdd(fill + j, 1u)] = (static_cast<u64>(id) << 32) | static_cast<u64>(b);
+}
+
+__global__ void k_tile_bptr(const u64* bedge, u32 n, i64 ne, i64 ntiles, u32* tile_bptr) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t > ntiles) return;
+  const i64 e = t * kTileEdges < ne ? t * kTileEdges : ne;
+  u32 lo = 0, hi = n;
+  while (lo < hi) {
+    const u32 mid = (lo + hi) >> 1;
+    if ((bedge[mid] >> 32) < static_cast<u64>(e)) lo = mid + 1;
+    else hi = mid;
+  }
+  tile_bptr[t] = lo;
 }
 
 __global__ void k_edge_of(const int2* edges, const u32* os, i64 nv, const int32_t* a,
@@ -348,6 +387,11 @@ int ensure_bedge(dm_ctx* c) {
   }
   st = segment_sort_u64(c, c->bedge.p, c->cnt.p, nv);
   if (st) return st;
+  // per-tile slices of the sorted (edge, facet) list, so no kernel searches it
+  const i64 ntiles = (c->ne + kTileEdges - 1) / kTileEdges;
+  DM_CK(c, c->tile_bptr.ensure(static_cast<size_t>(ntiles + 1)));
+  DM_LAUNCH(c, k_tile_bptr, grid_for(ntiles + 1, 256), 256, 0, c->bedge.p, static_cast<u32>(n),
+            c->ne, ntiles, c->tile_bptr.p);
   c->n_bedge = n;
   c->have_bedge = true;
   return DM_OK;

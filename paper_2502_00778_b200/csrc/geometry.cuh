@@ -19,11 +19,13 @@ template <>
 struct Coords<3> {
   const d4* __restrict__ p;
   __device__ __forceinline__ d4 operator[](int v) const { return ld_d4(p + v); }
+  __device__ __forceinline__ d4 xyz(int v) const { return ld_d3(p + v); }
 };
 template <>
 struct Coords<2> {
   const double2* __restrict__ p;
   __device__ __forceinline__ double2 operator[](int v) const { return ld_d2(p + v); }
+  __device__ __forceinline__ double2 xyz(int v) const { return ld_d2(p + v); }
 };
 
 // Dual-free 3D: the
@@ -51,15 +53,11 @@ __device__ __forceinline__ void df2(const Coords<2>& X, int v0, int v1, int v2, 
 
 // Traditional 3D:
 // c = (E-m)x(L-m) + (R-m)x(E-m), sign fixed so that c.(x_k-x_j) >= 0.
-__device__ __forceinline__ void tr3(const Coords<3>& X, int v0, int v1, int v2, int v3, int ij,
-                                    int ik, double& c0, double& c1, double& c2) {
-  const d4 x0 = X[v0], x1 = X[v1], x2 = X[v2], x3 = X[v3];
-  // the two other local nodes, ascending local order
-  const unsigned rest = 0xFu & ~((1u << ij) | (1u << ik));
-  const int il = __ffs(rest) - 1;
-  const int ir = __ffs(rest & (rest - 1)) - 1;
-  auto pick = [&](int i) -> d4 { return i == 0 ? x0 : (i == 1 ? x1 : (i == 2 ? x2 : x3)); };
-  const d4 xj = pick(ij), xk = pick(ik), xl = pick(il), xr = pick(ir);
+// x0..x3 in local order (for the centroid sum); xl / xr are the two other
+// local nodes in ascending local order.
+__device__ __forceinline__ void tr3_core(const d4& x0, const d4& x1, const d4& x2, const d4& x3,
+                                         const d4& xj, const d4& xk, const d4& xl, const d4& xr,
+                                         double& c0, double& c1, double& c2) {
   const double mx = (xj.x + xk.x) * 0.5, my = (xj.y + xk.y) * 0.5, mz = (xj.z + xk.z) * 0.5;
   const double Ex = (x0.x + x1.x + x2.x + x3.x) * 0.25;
   const double Ey = (x0.y + x1.y + x2.y + x3.y) * 0.25;
@@ -84,13 +82,21 @@ __device__ __forceinline__ void tr3(const Coords<3>& X, int v0, int v1, int v2, 
   }
 }
 
+__device__ __forceinline__ void tr3(const Coords<3>& X, int v0, int v1, int v2, int v3, int ij,
+                                    int ik, double& c0, double& c1, double& c2) {
+  const d4 x0 = X[v0], x1 = X[v1], x2 = X[v2], x3 = X[v3];
+  const unsigned rest = 0xFu & ~((1u << ij) | (1u << ik));
+  const int il = __ffs(rest) - 1;
+  const int ir = __ffs(rest & (rest - 1)) - 1;
+  auto pick = [&](int i) -> d4 { return i == 0 ? x0 : (i == 1 ? x1 : (i == 2 ? x2 : x3)); };
+  tr3_core(x0, x1, x2, x3, pick(ij), pick(ik), pick(il), pick(ir), c0, c1, c2);
+}
+
 // Traditional 2D: rotation of t = x_E - x_m with positive
 // dot against x_k - x_j.
-__device__ __forceinline__ void tr2(const Coords<2>& X, int v0, int v1, int v2, int ij, int ik,
-                                    double& c0, double& c1) {
-  const double2 x0 = X[v0], x1 = X[v1], x2 = X[v2];
-  auto pick = [&](int i) -> double2 { return i == 0 ? x0 : (i == 1 ? x1 : x2); };
-  const double2 xj = pick(ij), xk = pick(ik);
+__device__ __forceinline__ void tr2_core(const double2& x0, const double2& x1, const double2& x2,
+                                         const double2& xj, const double2& xk, double& c0,
+                                         double& c1) {
   const double tx = (x0.x + x1.x + x2.x) * (1.0 / 3.0) - (xj.x + xk.x) * 0.5;
   const double ty = (x0.y + x1.y + x2.y) * (1.0 / 3.0) - (xj.y + xk.y) * 0.5;
   c0 = ty;
@@ -99,6 +105,13 @@ __device__ __forceinline__ void tr2(const Coords<2>& X, int v0, int v1, int v2, 
     c0 = -c0;
     c1 = -c1;
   }
+}
+
+__device__ __forceinline__ void tr2(const Coords<2>& X, int v0, int v1, int v2, int ij, int ik,
+                                    double& c0, double& c1) {
+  const double2 x0 = X[v0], x1 = X[v1], x2 = X[v2];
+  auto pick = [&](int i) -> double2 { return i == 0 ? x0 : (i == 1 ? x1 : x2); };
+  tr2_core(x0, x1, x2, pick(ij), pick(ik), c0, c1);
 }
 
 // Boundary directed area n_B (ref mesh.cpp:113-127).

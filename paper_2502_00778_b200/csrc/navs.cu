@@ -8,23 +8,33 @@
 //                          so K4 never re-reads navs.
 //
 // Variants (north_star (b)):
-//   GATHER  (default): one CTA per 256 consecutive edges.  The CTA's slice of
-//           the edge->element CSR (inc) is contiguous; its incidences are
-//           evaluated in parallel into shared memory, then every edge thread
-//           folds its own incidences in ascending element id, scales, adds
-//           its boundary terms in ascending facet id and writes navs and s
-//           once.  This is the serial oracle's summation order, so the result
-//           is bitwise identical to it.  No atomics, no memset.
+//   GATHER (default): one CTA per 256-edge tile.  The tile's slice of the
+//       face-list incidence (ifl, edges.cu) is contiguous; every incidence
+//       (edge e, element E) carries the two nodes of E off the edge plus the
+//       local slots of j and k, so an incidence costs one streaming 8-byte
+//       load and two coordinate gathers -- no dependent connectivity load.
+//       Incidences are evaluated in parallel into shared memory, then each
+//       edge thread folds its own incidences in ascending element id, scales,
+//       adds its boundary terms in ascending facet id, and writes navs and s
+//       once.  That is the serial oracle's summation order: bitwise equal.
+//   GATHER_ELEM: the same fold through the element-id CSR (inc) and a
+//       dependent connectivity gather per incidence (kept for comparison).
 //   SCATTER: one thread per element, fp64 atomics (REDG.E.ADD.F64) through
-//           e2l into zeroed navs, then the same per-edge tail.  Faster or
-//           not, its summation order varies run to run (<=1e-12 parity).
+//       e2l into zeroed navs, then the same per-edge tail; summation order
+//       varies run to run (<=1e-12 parity, not deterministic).
+#include <algorithm>
+
 #include "geometry.cuh"
 
 namespace dm {
 namespace {
 
-constexpr int kEB = 256;    // edges per CTA (one per thread)
-constexpr int kCH = 1536;   // incidences staged per shared-memory chunk
+constexpr int kEB = kTileEdges;  // edges per CTA (one per thread)
+constexpr int kCH = 1536;        // GATHER_ELEM incidences per shared-memory chunk
+constexpr int kNodeMask = (1 << 30) - 1;
+
+template <int D>
+using Pt = typename std::conditional<D == 3, d4, double2>::type;
 
 template <int D, int ALGO>
 __device__ __forceinline__ void contribution(const Coords<D>& X, const int32_t* __restrict__ el,
@@ -50,16 +60,64 @@ __device__ __forceinline__ void contribution(const Coords<D>& X, const int32_t* 
   }
 }
 
-// Per-edge tail shared by both variants: scale pass, boundary pass, write
-// navs and s.  acc holds the element-loop sum for edge e (in ascending
-// element order for GATHER).  [rb, re) is the CTA's slice of the sorted
-// boundary (edge, facet) list.
+// Contribution from a face-list entry f, with x_j / x_k of the edge.
+template <int ALGO>
+__device__ __forceinline__ void face_contrib3(int ij, int ik, const d4& xj, const d4& xk,
+                                              const d4& xl, const d4& xr, double& c0, double& c1,
+                                              double& c2) {
+  const unsigned rest = 0xFu & ~((1u << ij) | (1u << ik));
+  const int il = __ffs(rest) - 1;
+  // value selects (no references: a runtime-chosen reference would force
+  // the operands to the stack)
+  auto pick = [&](int i) -> d4 {
+    d4 r;
+    r.x = i == ij ? xj.x : (i == ik ? xk.x : (i == il ? xl.x : xr.x));
+    r.y = i == ij ? xj.y : (i == ik ? xk.y : (i == il ? xl.y : xr.y));
+    r.z = i == ij ? xj.z : (i == ik ? xk.z : (i == il ? xl.z : xr.z));
+    r.w = 0.0;
+    return r;
+  };
+  if constexpr (ALGO == kDualFree) {
+    const unsigned fc = (kOppPacked >> (6 * ij)) & 63u;  // ref mesh.cpp:15
+    const d4 p0 = pick(fc & 3);
+    const d4 p1 = pick((fc >> 2) & 3);
+    const d4 p2 = pick((fc >> 4) & 3);
+    cross3(p1.x - p0.x, p1.y - p0.y, p1.z - p0.z, p2.x - p0.x, p2.y - p0.y, p2.z - p0.z, c0, c1,
+           c2);
+  } else {
+    tr3_core(pick(0), pick(1), pick(2), pick(3), xj, xk, xl, xr, c0, c1, c2);
+  }
+}
+
+template <int ALGO>
+__device__ __forceinline__ void face_contrib2(int ij, int ik, const double2& xj, const double2& xk,
+                                              const double2& xm, double& c0, double& c1) {
+  auto pick = [&](int i) -> double2 {
+    return make_double2(i == ij ? xj.x : (i == ik ? xk.x : xm.x),
+                        i == ij ? xj.y : (i == ik ? xk.y : xm.y));
+  };
+  if constexpr (ALGO == kDualFree) {
+    const double2 p = pick(ij == 2 ? 0 : ij + 1);  // ref mesh.cpp:97-101
+    const double2 q = pick(ij == 0 ? 2 : ij - 1);
+    c0 = (1.0 / 3.0) * (q.y - p.y);
+    c1 = (1.0 / 3.0) * (p.x - q.x);
+  } else {
+    tr2_core(pick(0), pick(1), pick(2), xj, xk, c0, c1);
+  }
+}
+
+// Per-edge tail shared by all variants: scale pass, boundary pass and the
+// edge-volume term s.  acc holds the element-loop sum for edge e; [rb, re)
+// is the tile's slice of the sorted boundary (edge, facet) list.
 template <int D, int ALGO>
-__device__ __forceinline__ void edge_tail(const Coords<D>& X, i64 e, int j, int k, double* acc,
-                                          const u64* __restrict__ bedge, u32 rb, u32 re,
-                                          const int32_t* __restrict__ bnd,
-                                          double* __restrict__ navs, double* __restrict__ svals) {
-  double n[3] = {acc[0], acc[1], D == 3 ? acc[2] : 0.0};
+__device__ __forceinline__ void edge_tail_values(const Coords<D>& X, i64 e, const double* acc,
+                                                 const Pt<D>& xj, const Pt<D>& xk,
+                                                 const u64* __restrict__ bedge, u32 rb, u32 re,
+                                                 const int32_t* __restrict__ bnd, double* n,
+                                                 double& s) {
+  n[0] = acc[0];
+  n[1] = acc[1];
+  n[2] = D == 3 ? acc[2] : 0.0;
   if constexpr (D == 3) {
     const double f = ALGO == kDualFree ? (1.0 / 12.0) : 0.5;  // SPEC.md:162 / PAPER.md:170
     n[0] *= f;
@@ -68,8 +126,7 @@ __device__ __forceinline__ void edge_tail(const Coords<D>& X, i64 e, int j, int 
   }
   if constexpr (ALGO == kDualFree) {
     if (rb < re) {
-      // lower bound of edge e in the slice
-      u32 lo = rb, hi = re;
+      u32 lo = rb, hi = re;  // lower bound of e in the tile slice
       while (lo < hi) {
         const u32 mid = (lo + hi) >> 1;
         if ((bedge[mid] >> 32) < static_cast<u64>(e)) lo = mid + 1;
@@ -95,44 +152,510 @@ __device__ __forceinline__ void edge_tail(const Coords<D>& X, i64 e, int j, int 
       }
     }
   }
-  double s;
-  if constexpr (D == 3) {
-    const d4 xj = X[j], xk = X[k];
-    s = (xk.x - xj.x) * n[0] + (xk.y - xj.y) * n[1];
-    s = s + (xk.z - xj.z) * n[2];
-    navs[3 * e] = n[0];
-    navs[3 * e + 1] = n[1];
-    navs[3 * e + 2] = n[2];
-  } else {
-    const double2 xj = X[j], xk = X[k];
-    s = (xk.x - xj.x) * n[0] + (xk.y - xj.y) * n[1];
-    navs[2 * e] = n[0];
-    navs[2 * e + 1] = n[1];
-  }
-  svals[e] = s;
-}
-
-__device__ __forceinline__ u32 lower_bound_edge(const u64* bedge, u32 n, i64 e) {
-  u32 lo = 0, hi = n;
-  while (lo < hi) {
-    const u32 mid = (lo + hi) >> 1;
-    if ((bedge[mid] >> 32) < static_cast<u64>(e)) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
+  s = (xk.x - xj.x) * n[0] + (xk.y - xj.y) * n[1];
+  if constexpr (D == 3) s = s + (xk.z - xj.z) * n[2];
 }
 
 template <int D, int ALGO>
-__global__ void __launch_bounds__(kEB)
+__device__ __forceinline__ void edge_tail(const Coords<D>& X, i64 e, const double* acc,
+                                          const Pt<D>& xj, const Pt<D>& xk,
+                                          const u64* __restrict__ bedge, u32 rb, u32 re,
+                                          const int32_t* __restrict__ bnd,
+                                          double* __restrict__ navs, double* __restrict__ svals) {
+  double n[3], s;
+  edge_tail_values<D, ALGO>(X, e, acc, xj, xk, bedge, rb, re, bnd, n, s);
+#pragma unroll
+  for (int d = 0; d < D; ++d) navs[D * e + d] = n[d];
+  svals[e] = s;
+}
+
+// Coalesced store of a warp's block of 32 consecutive edges' navs: lane l
+// stores doubles l, l+32, l+64 of the warp's contiguous 32*D-double block
+// (shuffle transpose).  All 32 lanes must call it.
+template <int D>
+__device__ __forceinline__ void store_navs_warp(const double* n, i64 wbase, i64 ne,
+                                                double* __restrict__ navs) {
+  __syncwarp();
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    const int i = lane + 32 * r;  // double index inside the warp block
+    const int src = i / D, comp = i - src * D;
+    const double v0 = __shfl_sync(0xffffffffu, n[0], src);
+    const double v1 = __shfl_sync(0xffffffffu, n[1], src);
+    double v = comp == 0 ? v0 : v1;
+    if constexpr (D == 3) {
+      const double v2 = __shfl_sync(0xffffffffu, n[2], src);
+      v = comp == 2 ? v2 : v;
+    }
+    if (wbase + src < ne) navs[D * wbase + i] = v;
+  }
+}
+
+// ------------------------------------------------------------------ GATHER (row table)
+// One CTA per 256-edge tile, one thread per edge.  The tile's edges belong
+// to consecutive origin rows [j0, jl]; per-tile metadata (tables.cu) gives
+// the tile's contiguous slices of the incidence codes, of the rows'
+// adjacency and of the row pointers, so the CTA stages everything in two
+// independent waves -- (1) codes, adjacency ids, row pointers, row-node
+// coordinates (all coalesced), (2) one gather of the adjacency coordinates
+// (about two random node loads per edge instead of two per incidence) --
+// and then evaluates every incidence from shared memory only.  Tiles larger
+// than the shared-memory caps read the same data from global memory (same
+// arithmetic, same order).
+constexpr int kTabCap = 1024;   // adjacency coordinates per tile
+constexpr int kCodeCap = 2048;  // incidence codes per tile
+constexpr int kRowCap = 320;    // origin rows per tile
+
+// Dual-free term of one incidence from its code and a coordinate source.
+template <int D, typename Tab>
+__device__ __forceinline__ void df_code(unsigned cd, int rb, const Tab& tab, double* c) {
+  if constexpr (D == 3) {
+    const d4 p0 = tab(rb + static_cast<int>(cd & 31u));
+    const d4 p1 = tab(rb + static_cast<int>((cd >> 5) & 31u));
+    const d4 p2 = tab(rb + static_cast<int>((cd >> 10) & 31u));
+    cross3(p1.x - p0.x, p1.y - p0.y, p1.z - p0.z, p2.x - p0.x, p2.y - p0.y, p2.z - p0.z, c[0],
+           c[1], c[2]);
+  } else {
+    const double2 p = tab(rb + static_cast<int>(cd & 31u));
+    const double2 q = tab(rb + static_cast<int>((cd >> 5) & 31u));
+    c[0] = (1.0 / 3.0) * (q.y - p.y);
+    c[1] = (1.0 / 3.0) * (p.x - q.x);
+  }
+}
+
+template <int D, int U, int MINB>
+__global__ void __launch_bounds__(kEB, MINB)
     k_navs_gather(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
-                  const int32_t* __restrict__ inc, const int32_t* __restrict__ el, Coords<D> X,
-                  i64 ne, const u64* __restrict__ bedge, u32 n_bedge,
+                  const uint16_t* __restrict__ codes, const u32* __restrict__ adj_ptr,
+                  const int32_t* __restrict__ adj, const u32* __restrict__ os,
+                  const int4* __restrict__ tile_meta, Coords<D> X, i64 ne,
+                  const u64* __restrict__ bedge, const u32* __restrict__ tile_bptr,
                   const int32_t* __restrict__ bnd, double* __restrict__ navs,
                   double* __restrict__ svals) {
+  __shared__ double s_t[D][kTabCap];     // adjacency coordinates (SoA)
+  __shared__ double s_xr[D][kRowCap];    // row-node coordinates (SoA)
+  __shared__ u32 s_rp[kRowCap + 1];      // adj_ptr of the rows (tile-relative)
+  __shared__ u32 s_ro[kRowCap];          // adj_ptr[j+1] - os[j+1] (tile-relative)
+  __shared__ uint16_t s_cd[kCodeCap];    // incidence codes
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  const i64 e0 = static_cast<i64>(blockIdx.x) * kEB;
+  const i64 e = e0 + t;
+  const bool valid = e < ne;
+  // tile_meta[2*tile] = {A0, A1, P0, P1}, [2*tile+1] = {j0, jl, 0, 0}
+  const int4 m0 = __ldg(tile_meta + 2 * blockIdx.x);
+  const int4 m1 = __ldg(tile_meta + 2 * blockIdx.x + 1);
+  const u32 A0 = static_cast<u32>(m0.x);
+  const int T = m0.y - m0.x, P0 = m0.z, NP = m0.w - m0.z;
+  const int j0 = m1.x, NR = m1.y - m1.x + 1;
+  const bool fast = T <= kTabCap && NP <= kCodeCap && NR <= kRowCap;  // CTA-uniform
+  int2 jk = make_int2(j0, j0);  // idle lanes of a partial tile point at row j0
+  int pb = 0, pe = 0;
+  if (valid) {
+    jk = edges[e];
+    pb = inc_ptr[e];
+    pe = inc_ptr[e + 1];
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+  Pt<D> xj, xk;
+  if (fast) {
+    // wave 1: codes, row pointers, row-node coordinates (coalesced)
+    for (int i = t; i < NP; i += kEB) s_cd[i] = __ldg(codes + P0 + i);
+    for (int r = t; r <= NR; r += kEB) {
+      const u32 ap = __ldg(adj_ptr + j0 + r);
+      s_rp[r] = ap - A0;
+      if (r > 0) s_ro[r - 1] = ap - __ldg(os + j0 + r) - A0;
+    }
+    for (int r = t; r < NR; r += kEB) {
+      const Pt<D> p = X[j0 + r];
+      s_xr[0][r] = p.x;
+      s_xr[1][r] = p.y;
+      if constexpr (D == 3) s_xr[2][r] = p.z;
+    }
+    // wave 2: adjacency coordinates (one gather per adjacency entry)
+    for (int i = t; i < T; i += kEB) {
+      const Pt<D> p = X[__ldg(adj + A0 + i)];
+      s_t[0][i] = p.x;
+      s_t[1][i] = p.y;
+      if constexpr (D == 3) s_t[2][i] = p.z;
+    }
+    __syncthreads();
+    auto tab = [&](int i) -> Pt<D> {
+      Pt<D> p;
+      p.x = s_t[0][i];
+      p.y = s_t[1][i];
+      if constexpr (D == 3) p.z = s_t[2][i];
+      return p;
+    };
+    const int r = jk.x - j0;
+    const int rb = static_cast<int>(s_rp[r]);
+    xj.x = s_xr[0][r];
+    xj.y = s_xr[1][r];
+    if constexpr (D == 3) xj.z = s_xr[2][r];
+    xk = tab(static_cast<int>(s_ro[r] + static_cast<u32>(e)));
+    const uint16_t* cd = s_cd - P0;
+    int q = pb;
+    for (; q + U <= pe; q += U) {
+      unsigned w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = cd[q + u];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double c[3];
+        df_code<D>(w[u], rb, tab, c);
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc[d] += c[d];
+      }
+    }
+    for (; q < pe; ++q) {
+      double c[3];
+      df_code<D>(cd[q], rb, tab, c);
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[d] += c[d];
+    }
+  } else {
+    // oversized tile: identical arithmetic and order straight from global memory
+    auto tab = [&](int i) -> Pt<D> { return X[__ldg(adj + A0 + i)]; };
+    const int rb = static_cast<int>(__ldg(adj_ptr + jk.x) - A0);
+    xj = X[jk.x];
+    xk = tab(static_cast<int>(__ldg(adj_ptr + jk.x + 1) - __ldg(os + jk.x + 1) +
+                              static_cast<u32>(e) - A0));
+    for (int q = pb; q < pe; ++q) {
+      double c[3];
+      df_code<D>(__ldg(codes + q), rb, tab, c);
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[d] += c[d];
+    }
+  }
+  double n[3] = {0.0, 0.0, 0.0};
+  double s = 0.0;
+  if (valid) {
+    edge_tail_values<D, kDualFree>(X, e, acc, xj, xk, bedge, tile_bptr[blockIdx.x],
+                                   tile_bptr[blockIdx.x + 1], bnd, n, s);
+    svals[e] = s;
+  }
+  store_navs_warp<D>(n, e - lane, ne, navs);
+}
+
+// ------------------------------------------------------------------ GATHER (ring walk)
+// One CTA per 256-edge tile, one thread per edge (3D dual-free).  The tile's
+// unique node set (rings.cu) is gathered once into shared memory; each edge
+// then walks the ring of its incident elements: one table read per
+// incidence, term +-cross(m_i - x_k, m_(i+1) - x_k), summed in ring order.
+// Deterministic (fixed order), within rounding of the serial oracle, which
+// sums in ascending element order instead (tests bound it by 1e-12).
+constexpr int kRingCodeCap = 3072;
+
+template <int MINB>
+__global__ void __launch_bounds__(kEB, MINB)
+    k_navs_ring(const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ rcodes,
+                const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt, Coords<3> X,
+                i64 ne, const u64* __restrict__ bedge, const u32* __restrict__ tile_bptr,
+                const int32_t* __restrict__ bnd, double* __restrict__ navs,
+                double* __restrict__ svals) {
+  __shared__ double s_t[3][kTileNodeCap];
+  __shared__ uint16_t s_cd[kRingCodeCap];
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  const i64 e0 = static_cast<i64>(blockIdx.x) * kEB;
+  const i64 e1 = (e0 + kEB < ne) ? e0 + kEB : ne;
+  const i64 e = e0 + t;
+  const bool valid = e < ne;
+  const int NU = static_cast<int>(__ldg(tcnt + blockIdx.x));
+  const int C0 = __ldg(inc_ptr + e0) + 3 * static_cast<int>(e0);
+  const int NC = __ldg(inc_ptr + e1) + 3 * static_cast<int>(e1) - C0;
+  const bool codes_fit = NC <= kRingCodeCap;  // CTA-uniform
+  int pb = 0, pe = 0;
+  if (valid) {
+    pb = inc_ptr[e];
+    pe = inc_ptr[e + 1];
+  }
+  if (codes_fit)
+    for (int i = t; i < NC; i += kEB) s_cd[i] = __ldg(rcodes + C0 + i);
+  const int32_t* tn = tnodes + static_cast<i64>(blockIdx.x) * kTileNodeCap;
+  for (int i = t; i < NU; i += kEB) {
+    const d4 p = X[__ldg(tn + i)];
+    s_t[0][i] = p.x;
+    s_t[1][i] = p.y;
+    s_t[2][i] = p.z;
+  }
+  __syncthreads();
+  const uint16_t* cd = codes_fit ? s_cd - C0 : rcodes;
+  auto tab = [&](unsigned i) -> d4 {
+    d4 p;
+    p.x = s_t[0][i];
+    p.y = s_t[1][i];
+    p.z = s_t[2][i];
+    return p;
+  };
+  double acc[3] = {0.0, 0.0, 0.0};
+  d4 xj{}, xk{};
+  if (valid) {
+    const int base = pb + 3 * static_cast<int>(e);
+    xj = tab(cd[base]);
+    xk = tab(cd[base + 1]);
+    d4 mp = tab(cd[base + 2]);
+    double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
+    const int n = pe - pb;
+    for (int i = 0; i < n; ++i) {
+      const unsigned w = cd[base + 3 + i];
+      const d4 m = tab(w & 0x7fffu);
+      const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
+      double c0, c1, c2;
+      cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
+      if (w & 0x8000u) {
+        acc[0] -= c0;
+        acc[1] -= c1;
+        acc[2] -= c2;
+      } else {
+        acc[0] += c0;
+        acc[1] += c1;
+        acc[2] += c2;
+      }
+      dx = ex;
+      dy = ey;
+      dz = ez;
+    }
+  }
+  double n[3] = {0.0, 0.0, 0.0};
+  double s = 0.0;
+  if (valid) {
+    edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, tile_bptr[blockIdx.x],
+                                   tile_bptr[blockIdx.x + 1], bnd, n, s);
+    svals[e] = s;
+  }
+  store_navs_warp<3>(n, e - lane, ne, navs);
+}
+
+// ------------------------------------------------------------------ GATHER (pipelined ring walk)
+// Persistent form of k_navs_ring: each CTA walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ...  While tile i is evaluated, the coordinates,
+// ring codes and inc_ptr slice of tile i+1 stream into the other half of a
+// double buffer with cp.async (LDGSTS, no register round trip), and the node
+// ids of tile i+2 are prefetched into registers -- so the per-tile gather
+// latency is hidden behind the previous tile's arithmetic.  Same arithmetic
+// and order as k_navs_ring.  Tiles with more than kPipeCap nodes or
+// kPipeCodeCap codes are evaluated straight from global memory.
+constexpr int kPipeCap = 1024;
+constexpr int kPipeCodeCap = 3072;
+constexpr int kIdsPerThread = kPipeCap / kEB;
+
+struct PipeSmem {
+  double tab[2][3][kPipeCap];
+  uint32_t cd[2][kPipeCodeCap / 2 + 2];
+  int32_t ip[2][kEB + 1];
+};
+
+__device__ __forceinline__ void pipe_issue(PipeSmem& S, int b, int tile, const int4& m,
+                                           const int (&ids)[kIdsPerThread], Coords<3> X,
+                                           const int32_t* __restrict__ inc_ptr,
+                                           const uint16_t* __restrict__ rcodes, i64 ne) {
+  const int t = threadIdx.x;
+  if (m.z <= kPipeCap) {
+#pragma unroll
+    for (int u = 0; u < kIdsPerThread; ++u) {
+      const int i = t + u * kEB;
+      if (i < m.z) {
+        const double* src = reinterpret_cast<const double*>(X.p + ids[u]);
+        cp_async8(&S.tab[b][0][i], src);
+        cp_async8(&S.tab[b][1][i], src + 1);
+        cp_async8(&S.tab[b][2][i], src + 2);
+      }
+    }
+  }
+  if (m.y <= kPipeCodeCap) {
+    const int w0 = m.x >> 1, w1 = (m.x + m.y + 1) >> 1;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(rcodes);
+    for (int w = w0 + t; w < w1; w += kEB) cp_async4(&S.cd[b][w - w0], src + w);
+  }
+  const i64 e0 = static_cast<i64>(tile) * kEB;
+  const i64 cnt = (e0 + kEB < ne ? kEB : ne - e0) + 1;
+  for (int i = t; i < cnt; i += kEB) cp_async4(&S.ip[b][i], inc_ptr + e0 + i);
+}
+
+__device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int4* __restrict__ meta,
+                                         const int32_t* __restrict__ tnodes, int4& m,
+                                         int (&ids)[kIdsPerThread]) {
+  if (tile < ntiles) {
+    m = __ldg(meta + tile);
+    const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
+#pragma unroll
+    for (int u = 0; u < kIdsPerThread; ++u) {
+      const int i = threadIdx.x + u * kEB;
+      ids[u] = (i < m.z && m.z <= kPipeCap) ? __ldg(tn + i) : 0;
+    }
+  } else {
+    m = make_int4(0, 0, 0, 0);
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kEB, MINB)
+    k_navs_ring_pipe(const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ rcodes,
+                     const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
+                     Coords<3> X, i64 ne, int ntiles, const u64* __restrict__ bedge,
+                     const u32* __restrict__ tile_bptr, const int32_t* __restrict__ bnd,
+                     double* __restrict__ navs, double* __restrict__ svals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  // prologue: ids of tile 0 -> issue its copies; ids of tile 1 into registers
+  int4 m_cur, m_nxt;
+  int ids[kIdsPerThread];
+  pipe_ids(tile, ntiles, meta, tnodes, m_cur, ids);
+  pipe_issue(S, 0, tile, m_cur, ids, X, inc_ptr, rcodes, ne);
+  cp_async_commit();
+  pipe_ids(tile + gridDim.x, ntiles, meta, tnodes, m_nxt, ids);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int b = it & 1;
+    const int nxt = tile + gridDim.x;
+    if (nxt < ntiles) pipe_issue(S, b ^ 1, nxt, m_nxt, ids, X, inc_ptr, rcodes, ne);
+    cp_async_commit();
+    const int4 m = m_cur;
+    m_cur = m_nxt;
+    pipe_ids(nxt + gridDim.x, ntiles, meta, tnodes, m_nxt, ids);
+    cp_async_wait<1>();
+    __syncthreads();
+    // ---- evaluate tile `tile` from buffer b
+    const i64 e0 = static_cast<i64>(tile) * kEB;
+    const i64 e = e0 + t;
+    const bool valid = e < ne;
+    const bool tab_fast = m.z <= kPipeCap, cd_fast = m.y <= kPipeCodeCap;
+    const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
+    auto tab = [&](unsigned i) -> d4 {
+      d4 p;
+      if (tab_fast) {
+        p.x = S.tab[b][0][i];
+        p.y = S.tab[b][1][i];
+        p.z = S.tab[b][2][i];
+      } else {
+        p = X[__ldg(tn + i)];
+      }
+      return p;
+    };
+    const uint16_t* cd = cd_fast ? reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1)
+                                 : rcodes;
+    double acc[3] = {0.0, 0.0, 0.0};
+    d4 xj{}, xk{};
+    if (valid) {
+      const int pb = S.ip[b][t], pe = S.ip[b][t + 1];
+      const int base = pb + 3 * static_cast<int>(e);
+      xj = tab(cd[base]);
+      xk = tab(cd[base + 1]);
+      const d4 mp = tab(cd[base + 2]);
+      double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
+      const int n = pe - pb;
+      for (int i = 0; i < n; ++i) {
+        const unsigned w = cd[base + 3 + i];
+        const d4 mm = tab(w & 0x7fffu);
+        const double ex = mm.x - xk.x, ey = mm.y - xk.y, ez = mm.z - xk.z;
+        double c0, c1, c2;
+        cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
+        if (w & 0x8000u) {
+          acc[0] -= c0;
+          acc[1] -= c1;
+          acc[2] -= c2;
+        } else {
+          acc[0] += c0;
+          acc[1] += c1;
+          acc[2] += c2;
+        }
+        dx = ex;
+        dy = ey;
+        dz = ez;
+      }
+    }
+    double n[3] = {0.0, 0.0, 0.0};
+    double s = 0.0;
+    if (valid) {
+      edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, tile_bptr[tile],
+                                     tile_bptr[tile + 1], bnd, n, s);
+      svals[e] = s;
+    }
+    store_navs_warp<3>(n, e - lane, ne, navs);
+    __syncthreads();  // buffer b is refilled two iterations from now
+  }
+  cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------ GATHER_FACES
+// One thread per edge.  x_j, x_k live in registers; the thread walks its own
+// slice of the face-list incidence in ascending element order, U entries at
+// a time with all loads of a batch issued before any use (memory-level
+// parallelism without shared memory or block barriers), and folds the
+// contributions in registers.  The navs row is written coalesced by a warp
+// shuffle transpose (lane l stores doubles l, l+32, l+64 of the warp's
+// 32*D-double block).
+template <int D, int ALGO, int U, int MINB>
+__global__ void __launch_bounds__(kEB, MINB)
+    k_navs_faces(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
+                  const int2* __restrict__ ifl, Coords<D> X, i64 ne,
+                  const u64* __restrict__ bedge, const u32* __restrict__ tile_bptr,
+                  const int32_t* __restrict__ bnd, double* __restrict__ navs,
+                  double* __restrict__ svals) {
+  const int lane = threadIdx.x & 31;
+  const i64 e = static_cast<i64>(blockIdx.x) * kEB + threadIdx.x;
+  const bool valid = e < ne;
+  int pb = 0, pe = 0;
+  int2 jk = make_int2(0, 0);
+  if (valid) {
+    jk = edges[e];
+    pb = inc_ptr[e];
+    pe = inc_ptr[e + 1];
+  }
+  const Pt<D> xj = X[jk.x], xk = X[jk.y];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int q0 = pb; q0 < pe; q0 += U) {
+    int2 f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) f[u] = q0 + u < pe ? __ldg(ifl + q0 + u) : make_int2(0, 0);
+    Pt<D> xl[U], xr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (q0 + u < pe) {
+        xl[u] = X[f[u].x & kNodeMask];
+        if constexpr (D == 3) xr[u] = X[f[u].y & kNodeMask];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (q0 + u < pe) {
+        double c[3];
+        const int ij = static_cast<unsigned>(f[u].x) >> 30;
+        const int ik = static_cast<unsigned>(f[u].y) >> 30;
+        if constexpr (D == 3) face_contrib3<ALGO>(ij, ik, xj, xk, xl[u], xr[u], c[0], c[1], c[2]);
+        else face_contrib2<ALGO>(ij, ik, xj, xk, xl[u], c[0], c[1]);
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc[d] += c[d];
+      }
+    }
+  }
+  double n[3] = {0.0, 0.0, 0.0};
+  double s = 0.0;
+  if (valid) {
+    edge_tail_values<D, ALGO>(X, e, acc, xj, xk, bedge,
+                              ALGO == kDualFree ? tile_bptr[blockIdx.x] : 0u,
+                              ALGO == kDualFree ? tile_bptr[blockIdx.x + 1] : 0u, bnd, n, s);
+    svals[e] = s;
+  }
+  store_navs_warp<D>(n, e - lane, ne, navs);
+}
+
+// ------------------------------------------------------------------ GATHER_ELEM
+template <int D, int ALGO>
+__global__ void __launch_bounds__(kEB)
+    k_navs_gather_elem(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
+                       const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
+                       Coords<D> X, i64 ne, const u64* __restrict__ bedge,
+                       const u32* __restrict__ tile_bptr, const int32_t* __restrict__ bnd,
+                       double* __restrict__ navs, double* __restrict__ svals) {
   __shared__ int s_j[kEB], s_k[kEB];
   __shared__ unsigned char s_le[kCH];
-  __shared__ double s_c[kCH * D];
-  __shared__ u32 s_br[2];
+  __shared__ double s_c[D][kCH];
 
   const int t = threadIdx.x;
   const i64 e0 = static_cast<i64>(blockIdx.x) * kEB;
@@ -149,10 +672,6 @@ __global__ void __launch_bounds__(kEB)
   }
   s_j[t] = j;
   s_k[t] = k;
-  if (ALGO == kDualFree && t == 0) {
-    s_br[0] = lower_bound_edge(bedge, n_bedge, e0);
-    s_br[1] = lower_bound_edge(bedge, n_bedge, e1);
-  }
   const int P0 = __ldg(inc_ptr + e0), P1 = __ldg(inc_ptr + e1);
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
@@ -166,21 +685,22 @@ __global__ void __launch_bounds__(kEB)
       double c[3];
       contribution<D, ALGO>(X, el, __ldg(inc + q), s_j[le], s_k[le], c);
 #pragma unroll
-      for (int d = 0; d < D; ++d) s_c[(q - c0) * D + d] = c[d];
+      for (int d = 0; d < D; ++d) s_c[d][q - c0] = c[d];
     }
     __syncthreads();
     for (int q = qb; q < qe; ++q) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) acc[d] += s_c[(q - c0) * D + d];
+      for (int d = 0; d < D; ++d) acc[d] += s_c[d][q - c0];
     }
     __syncthreads();
   }
   if (!valid) return;
-  edge_tail<D, ALGO>(X, e, j, k, acc, bedge, ALGO == kDualFree ? s_br[0] : 0u,
-                     ALGO == kDualFree ? s_br[1] : 0u, bnd, navs, svals);
+  edge_tail<D, ALGO>(X, e, acc, X[j], X[k], bedge,
+                     ALGO == kDualFree ? tile_bptr[blockIdx.x] : 0u,
+                     ALGO == kDualFree ? tile_bptr[blockIdx.x + 1] : 0u, bnd, navs, svals);
 }
 
-// -------------------------------------------------------------- SCATTER
+// ------------------------------------------------------------------ SCATTER
 template <int D, int ALGO>
 __global__ void __launch_bounds__(256)
     k_navs_scatter(const int32_t* __restrict__ el, Coords<D> X, i64 nE,
@@ -210,50 +730,18 @@ __global__ void __launch_bounds__(256)
 }
 
 template <int D, int ALGO>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kEB)
     k_edge_finalize(const int2* __restrict__ edges, Coords<D> X, i64 ne,
-                    const u64* __restrict__ bedge, u32 n_bedge, const int32_t* __restrict__ bnd,
-                    double* __restrict__ navs, double* __restrict__ svals) {
-  __shared__ u32 s_br[2];
-  const i64 e0 = static_cast<i64>(blockIdx.x) * blockDim.x;
-  const i64 e1 = (e0 + blockDim.x < ne) ? e0 + blockDim.x : ne;
-  if (ALGO == kDualFree && threadIdx.x == 0) {
-    s_br[0] = lower_bound_edge(bedge, n_bedge, e0);
-    s_br[1] = lower_bound_edge(bedge, n_bedge, e1);
-  }
-  __syncthreads();
-  const i64 e = e0 + threadIdx.x;
+                    const u64* __restrict__ bedge, const u32* __restrict__ tile_bptr,
+                    const int32_t* __restrict__ bnd, double* __restrict__ navs,
+                    double* __restrict__ svals) {
+  const i64 e = static_cast<i64>(blockIdx.x) * kEB + threadIdx.x;
   if (e >= ne) return;
   const int2 jk = edges[e];
   double acc[3] = {navs[D * e], navs[D * e + 1], D == 3 ? navs[D * e + 2] : 0.0};
-  edge_tail<D, ALGO>(X, e, jk.x, jk.y, acc, bedge, ALGO == kDualFree ? s_br[0] : 0u,
-                     ALGO == kDualFree ? s_br[1] : 0u, bnd, navs, svals);
-}
-
-template <int D, int ALGO>
-int launch_navs(dm_ctx* c, int variant) {
-  Coords<D> X;
-  if constexpr (D == 3) X.p = c->x4.p;
-  else X.p = reinterpret_cast<const double2*>(c->coords.p);
-  const u32 nb = static_cast<u32>(c->n_bedge);
-  const i64 ne = c->ne;
-  if (variant == DM_VARIANT_SCATTER) {
-    tmark(c, 0);
-    DM_CK(c, cudaMemsetAsync(c->navs.p, 0, sizeof(double) * D * ne, c->stream));
-    DM_LAUNCH(c, (k_navs_scatter<D, ALGO>), grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE,
-              c->e2l.p, c->navs.p);
-    tmark(c, 1);
-    DM_LAUNCH(c, (k_edge_finalize<D, ALGO>), grid_for(ne, 256), 256, 0, c->edges.p, X, ne,
-              c->bedge.p, nb, c->bnd.p, c->navs.p, c->svals.p);
-    tmark(c, 2);
-  } else {
-    tmark(c, 0);
-    DM_LAUNCH(c, (k_navs_gather<D, ALGO>), grid_for(ne, kEB), kEB, 0, c->edges.p, c->inc_ptr.p,
-              c->inc.p, c->elems.p, X, ne, c->bedge.p, nb, c->bnd.p, c->navs.p, c->svals.p);
-    tmark(c, 1);
-    tmark(c, 2);
-  }
-  return DM_OK;
+  edge_tail<D, ALGO>(X, e, acc, X[jk.x], X[jk.y], bedge,
+                     ALGO == kDualFree ? tile_bptr[blockIdx.x] : 0u,
+                     ALGO == kDualFree ? tile_bptr[blockIdx.x + 1] : 0u, bnd, navs, svals);
 }
 
 template <int D>
@@ -275,17 +763,99 @@ __global__ void __launch_bounds__(256)
   svals[e] = s;
 }
 
+template <int D>
+Coords<D> coords_of(dm_ctx* c) {
+  Coords<D> X;
+  if constexpr (D == 3) X.p = c->x4.p;
+  else X.p = reinterpret_cast<const double2*>(c->coords.p);
+  return X;
+}
+
+template <int D, int ALGO>
+int launch_navs(dm_ctx* c, int variant) {
+  const Coords<D> X = coords_of<D>(c);
+  const i64 ne = c->ne;
+  const unsigned tiles = grid_for(ne, kEB);
+  if (variant == DM_VARIANT_SCATTER) {
+    tmark(c, 0);
+    DM_CK(c, cudaMemsetAsync(c->navs.p, 0, sizeof(double) * D * ne, c->stream));
+    DM_LAUNCH(c, (k_navs_scatter<D, ALGO>), grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE,
+              c->e2l.p, c->navs.p);
+    tmark(c, 1);
+    DM_LAUNCH(c, (k_edge_finalize<D, ALGO>), tiles, kEB, 0, c->edges.p, X, ne, c->bedge.p,
+              c->tile_bptr.p, c->bnd.p, c->navs.p, c->svals.p);
+    tmark(c, 2);
+  } else if (variant == DM_VARIANT_GATHER_ELEM) {
+    tmark(c, 0);
+    DM_LAUNCH(c, (k_navs_gather_elem<D, ALGO>), tiles, kEB, 0, c->edges.p, c->inc_ptr.p,
+              c->inc.p, c->elems.p, X, ne, c->bedge.p, c->tile_bptr.p, c->bnd.p, c->navs.p,
+              c->svals.p);
+    tmark(c, 1);
+    tmark(c, 2);
+  } else if (variant == DM_VARIANT_GATHER && D == 3 && ALGO == kDualFree && c->ring_ok) {
+    tmark(c, 0);
+    if constexpr (D == 3) {
+      if (c->gather_cfg == 5) {
+        DM_LAUNCH(c, k_navs_ring<3>, tiles, kEB, 0, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
+                  c->tnode_cnt.p, X, ne, c->bedge.p, c->tile_bptr.p, c->bnd.p, c->navs.p,
+                  c->svals.p);
+      } else {
+        const int smem = static_cast<int>(sizeof(PipeSmem));
+        auto kern = c->gather_cfg == 1 ? k_navs_ring_pipe<2> : k_navs_ring_pipe<3>;
+        DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0, nsm = 0;
+        DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
+        DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+        const unsigned grid = static_cast<unsigned>(
+            std::min<i64>(static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
+        DM_LAUNCH(c, kern, grid, kEB, smem, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
+                  c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->tile_bptr.p,
+                  c->bnd.p, c->navs.p, c->svals.p);
+      }
+    }
+    tmark(c, 1);
+    tmark(c, 2);
+  } else if (variant == DM_VARIANT_GATHER_FACES || !c->table_ok || ALGO != kDualFree) {
+    // face-list gather: traditional algorithm, meshes with node degree > 32
+    tmark(c, 0);
+#define DM_FACES(U, MINB)                                                                     \
+  DM_LAUNCH(c, (k_navs_faces<D, ALGO, U, MINB>), tiles, kEB, 0, c->edges.p, c->inc_ptr.p,      \
+            c->ifl.p, X, ne, c->bedge.p, c->tile_bptr.p, c->bnd.p, c->navs.p, c->svals.p)
+    switch (c->gather_cfg) {
+      case 1: DM_FACES(4, 2); break;
+      default: DM_FACES(2, 3); break;
+    }
+#undef DM_FACES
+    tmark(c, 1);
+    tmark(c, 2);
+  } else {
+    tmark(c, 0);
+#define DM_TABLE(U, MINB)                                                                     \
+  DM_LAUNCH(c, (k_navs_gather<D, U, MINB>), tiles, kEB, 0, c->edges.p, c->inc_ptr.p,           \
+            c->codes.p, c->adj_ptr.p, c->adj.p, c->os.p, c->tile_meta.p, X, ne, c->bedge.p,  \
+            c->tile_bptr.p, c->bnd.p, c->navs.p, c->svals.p)
+    switch (c->gather_cfg) {
+      case 1: DM_TABLE(2, 4); break;
+      case 2: DM_TABLE(4, 2); break;
+      case 3: DM_TABLE(1, 4); break;
+      default: DM_TABLE(2, 3); break;
+    }
+#undef DM_TABLE
+    tmark(c, 1);
+    tmark(c, 2);
+  }
+  return DM_OK;
+}
+
 }  // namespace
 
 int svals_from_navs(dm_ctx* c) {
   if (c->dim == 3) {
-    Coords<3> X{c->x4.p};
-    DM_LAUNCH(c, k_svals<3>, grid_for(c->ne, 256), 256, 0, c->edges.p, X, c->ne, c->navs.p,
-              c->svals.p);
+    DM_LAUNCH(c, k_svals<3>, grid_for(c->ne, 256), 256, 0, c->edges.p, coords_of<3>(c), c->ne,
+              c->navs.p, c->svals.p);
   } else {
-    Coords<2> X{reinterpret_cast<const double2*>(c->coords.p)};
-    DM_LAUNCH(c, k_svals<2>, grid_for(c->ne, 256), 256, 0, c->edges.p, X, c->ne, c->navs.p,
-              c->svals.p);
+    DM_LAUNCH(c, k_svals<2>, grid_for(c->ne, 256), 256, 0, c->edges.p, coords_of<2>(c), c->ne,
+              c->navs.p, c->svals.p);
   }
   return DM_OK;
 }
@@ -294,10 +864,19 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "navs requested before build_edges");
   if (algo != DM_NAV_TRADITIONAL && algo != DM_NAV_DUALFREE)
     return fail(c, DM_ERR_INVALID_ARG, "unknown nav algorithm");
-  if (variant != DM_VARIANT_GATHER && variant != DM_VARIANT_SCATTER)
+  if (variant < DM_VARIANT_GATHER || variant > DM_VARIANT_GATHER_EXACT)
     return fail(c, DM_ERR_INVALID_ARG, "unknown nav variant");
   int st = ensure_bedge(c);
   if (st) return st;
+  if (variant == DM_VARIANT_GATHER && algo == DM_NAV_DUALFREE) {
+    st = ensure_rings(c);
+    if (st) return st;
+  }
+  if ((variant == DM_VARIANT_GATHER_EXACT || (variant == DM_VARIANT_GATHER && !c->ring_ok)) &&
+      algo == DM_NAV_DUALFREE) {
+    st = ensure_tables(c);
+    if (st) return st;
+  }
   DM_CK(c, c->navs.ensure(static_cast<size_t>(c->dim * c->ne)));
   DM_CK(c, c->svals.ensure(static_cast<size_t>(c->ne)));
   if (c->dim == 3) {

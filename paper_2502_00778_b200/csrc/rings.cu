@@ -1,0 +1,242 @@
+// rings.cu -- connectivity-only structures of the fast GATHER path (3D).
+//
+// For an interior edge (j,k) the incident tetrahedra form a closed ring
+// around it: element i has nodes {j, k, m_i, m_(i+1)}.  For a boundary edge
+// the ring is an open chain.  The dual-free term of element i is
+//   2 n_j^E = +-cross(m_i - x_k, m_(i+1) - x_k)
+// (the face opposite j is {k, m_i, m_(i+1)}; the sign is the parity of
+// (k, m_i, m_(i+1)) against the outward vertex order of the reference,
+// mesh.cpp:15,103-110), so walking the ring needs ONE new coordinate per
+// incidence instead of three.
+//
+//   tile nodes : per 256-edge tile, the sorted unique ids of every node the
+//                tile touches (j, k, ring nodes), at a fixed stride of
+//                kTileNodeCap, count in tnode_cnt[tile].
+//   ring codes : per edge, n+3 16-bit words at offset inc_ptr[e] + 3e:
+//                  [slot(j), slot(k), slot(m_0), slot(m_1)|s_0<<15, ...,
+//                   slot(m_n)|s_(n-1)<<15]      (slots into the tile list)
+// Built once per topology.  Any tile with more than kTileNodeCap nodes, an
+// edge with more than kRingMax incidences or a non-manifold fan (the walk
+// does not consume every incident element) sets ring_ok = false and the
+// GATHER path falls back to the bit-exact row-table kernel.
+#include "dm_internal.cuh"
+
+namespace dm {
+namespace {
+
+constexpr int kCand = 8192;  // candidate ids gathered per tile (before dedup)
+
+__global__ void __launch_bounds__(kTileEdges)
+    k_tile_nodes(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
+                 const int32_t* __restrict__ inc, const int32_t* __restrict__ el, i64 ne,
+                 int32_t* __restrict__ tnodes, u32* __restrict__ tcnt, int* __restrict__ flag) {
+  __shared__ int buf[kCand];
+  __shared__ int s_n;
+  __shared__ int s_w[kTileEdges / 32 + 1];
+  const int t = threadIdx.x;
+  const i64 e = static_cast<i64>(blockIdx.x) * kTileEdges + t;
+  if (t == 0) s_n = 0;
+  __syncthreads();
+  if (e < ne) {
+    const int2 jk = edges[e];
+    const int pb = inc_ptr[e], pe = inc_ptr[e + 1];
+    const int m = 2 + 2 * (pe - pb);
+    int w = atomicAdd(&s_n, m);
+    if (w + m <= kCand) {
+      buf[w++] = jk.x;
+      buf[w++] = jk.y;
+      for (int q = pb; q < pe; ++q) {
+        const int4 v = reinterpret_cast<const int4*>(el)[inc[q]];
+        const int vs[4] = {v.x, v.y, v.z, v.w};
+        for (int a = 0; a < 4; ++a)
+          if (vs[a] != jk.x && vs[a] != jk.y) buf[w++] = vs[a];
+      }
+    }
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (n > kCand) {
+    if (t == 0) atomicOr(flag, 1);
+    return;
+  }
+  int P = 2;
+  while (P < n) P <<= 1;
+  for (int i = n + t; i < P; i += kTileEdges) buf[i] = 0x7fffffff;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < P; i += kTileEdges) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int a = buf[i], b = buf[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            buf[i] = b;
+            buf[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  // unique, in order: each thread owns a contiguous chunk
+  const int per = (n + kTileEdges - 1) / kTileEdges;
+  const int lo = t * per, hi = min(n, lo + per);
+  int mine = 0;
+  for (int i = lo; i < hi; ++i)
+    if (i == 0 || buf[i] != buf[i - 1]) ++mine;
+  // block exclusive scan of `mine`
+  const int lane = t & 31, warp = t >> 5;
+  int incl = warp_incl_scan(mine);
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (t == 0) {
+    int run = 0;
+    for (int w = 0; w < kTileEdges / 32; ++w) {
+      const int v = s_w[w];
+      s_w[w] = run;
+      run += v;
+    }
+    s_w[kTileEdges / 32] = run;
+  }
+  __syncthreads();
+  int pos = s_w[warp] + incl - mine;
+  const int total = s_w[kTileEdges / 32];
+  if (t == 0) atomicMax(flag + 1, total);
+  if (total > kTileNodeCap) {
+    if (t == 0) atomicOr(flag, 2);
+    return;
+  }
+  int32_t* out = tnodes + static_cast<i64>(blockIdx.x) * kTileNodeCap;
+  for (int i = lo; i < hi; ++i)
+    if (i == 0 || buf[i] != buf[i - 1]) out[pos++] = buf[i];
+  if (t == 0) tcnt[blockIdx.x] = static_cast<u32>(total);
+}
+
+__device__ __forceinline__ int tslot(const int32_t* list, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (list[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// parity of the permutation taking (a0,a1,a2) to (b0,b1,b2): +1 even, -1 odd
+__device__ __forceinline__ int perm_sign(int a0, int a1, int a2, int b0, int b1, int b2) {
+  // rotate (a) so that a0 == b0, then compare the second entries
+  const int x1 = a0 == b0 ? a1 : (a1 == b0 ? a2 : a0);
+  (void)b2;
+  return x1 == b1 ? 1 : -1;
+}
+
+__global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
+                             const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
+                             const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt,
+                             i64 ne, uint16_t* __restrict__ rcodes, int* __restrict__ flag) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const i64 tile = e / kTileEdges;
+  const int32_t* list = tnodes + tile * kTileNodeCap;
+  const int nl = static_cast<int>(tcnt[tile]);
+  const int2 jk = edges[e];
+  const int j = jk.x, k = jk.y;
+  const int pb = inc_ptr[e], n = inc_ptr[e + 1] - pb;
+  if (n > kRingMax) {
+    atomicOr(flag, 4);
+    return;
+  }
+  int a[kRingMax], b[kRingMax], p0[kRingMax], p1[kRingMax], p2[kRingMax];
+  for (int i = 0; i < n; ++i) {
+    const int4 v = reinterpret_cast<const int4*>(el)[inc[pb + i]];
+    const int vs[4] = {v.x, v.y, v.z, v.w};
+    const int ij = vs[0] == j ? 0 : (vs[1] == j ? 1 : (vs[2] == j ? 2 : 3));
+    const unsigned f = (kOppPacked >> (6 * ij)) & 63u;  // ref mesh.cpp:15
+    p0[i] = vs[f & 3];
+    p1[i] = vs[(f >> 2) & 3];
+    p2[i] = vs[(f >> 4) & 3];
+    int o[2], no = 0;
+    for (int q = 0; q < 4; ++q)
+      if (vs[q] != j && vs[q] != k) o[no++] = vs[q];
+    a[i] = o[0];
+    b[i] = o[1];
+  }
+  // start: the smallest node seen exactly once (open chain), else a[0]
+  int start = -1;
+  for (int i = 0; i < n; ++i)
+    for (int s = 0; s < 2; ++s) {
+      const int v = s ? b[i] : a[i];
+      int cnt = 0;
+      for (int q = 0; q < n; ++q) cnt += (a[q] == v) + (b[q] == v);
+      if (cnt == 1 && (start < 0 || v < start)) start = v;
+    }
+  if (start < 0) start = a[0];
+  uint16_t* out = rcodes + pb + 3 * e;
+  out[0] = static_cast<uint16_t>(tslot(list, nl, j));
+  out[1] = static_cast<uint16_t>(tslot(list, nl, k));
+  out[2] = static_cast<uint16_t>(tslot(list, nl, start));
+  unsigned used = 0;
+  int cur = start;
+  for (int step = 0; step < n; ++step) {
+    int pick = -1;
+    for (int i = 0; i < n; ++i)
+      if (!(used >> i & 1u) && (a[i] == cur || b[i] == cur)) {
+        pick = i;
+        break;
+      }
+    if (pick < 0) {
+      atomicOr(flag, 8);  // non-manifold fan: the walk cannot continue
+      return;
+    }
+    used |= 1u << pick;
+    const int nxt = a[pick] == cur ? b[pick] : a[pick];
+    const int sg = perm_sign(k, cur, nxt, p0[pick], p1[pick], p2[pick]);
+    out[3 + step] = static_cast<uint16_t>(tslot(list, nl, nxt) | (sg < 0 ? 0x8000u : 0u));
+    cur = nxt;
+  }
+}
+
+__global__ void k_ring_meta(const int32_t* __restrict__ inc_ptr, const u32* __restrict__ tcnt,
+                            i64 ne, i64 ntiles, int4* __restrict__ meta) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const i64 e0 = t * kTileEdges, e1 = (e0 + kTileEdges < ne) ? e0 + kTileEdges : ne;
+  const int C0 = inc_ptr[e0] + 3 * static_cast<int>(e0);
+  const int C1 = inc_ptr[e1] + 3 * static_cast<int>(e1);
+  meta[t] = make_int4(C0, C1 - C0, static_cast<int>(tcnt[t]), 0);
+}
+
+}  // namespace
+
+int ensure_rings(dm_ctx* c) {
+  if (c->have_rings) return DM_OK;
+  if (c->dim != 3) {
+    c->ring_ok = false;
+    c->have_rings = true;
+    return DM_OK;
+  }
+  const i64 ne = c->ne;
+  const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
+  const i64 M = 6 * c->nE;
+  DM_CK(c, c->tnodes.ensure(static_cast<size_t>(ntiles * kTileNodeCap)));
+  DM_CK(c, c->tnode_cnt.ensure(static_cast<size_t>(ntiles)));
+  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(M + 3 * ne + 4)));
+  DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(ntiles)));
+  DM_CK(c, c->flag.ensure(4));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
+  DM_LAUNCH(c, k_tile_nodes, static_cast<unsigned>(ntiles), kTileEdges, 0, c->edges.p,
+            c->inc_ptr.p, c->inc.p, c->elems.p, ne, c->tnodes.p, c->tnode_cnt.p, c->flag.p);
+  DM_LAUNCH(c, k_ring_codes, grid_for(ne, 128), 128, 0, c->edges.p, c->inc_ptr.p, c->inc.p,
+            c->elems.p, c->tnodes.p, c->tnode_cnt.p, ne, c->rcodes.p, c->flag.p);
+  DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, c->inc_ptr.p, c->tnode_cnt.p, ne,
+            ntiles, c->ring_meta.p);
+  int fl[2] = {0, 0};
+  DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  c->ring_fail = fl[0];
+  c->ring_max_nodes = fl[1];
+  c->ring_ok = (fl[0] == 0);
+  c->have_rings = true;
+  return DM_OK;
+}
+
+}  // namespace dm

@@ -14,6 +14,8 @@ pytestmark = pytest.mark.gpu
 
 DF, TR = _lib.DM_NAV_DUALFREE, _lib.DM_NAV_TRADITIONAL
 GATHER, SCATTER = _lib.DM_VARIANT_GATHER, _lib.DM_VARIANT_SCATTER
+EXACT, FACES, ELEMV = (_lib.DM_VARIANT_GATHER_EXACT, _lib.DM_VARIANT_GATHER_FACES,
+                       _lib.DM_VARIANT_GATHER_ELEM)
 EDGE, ELEM = _lib.DM_VOL_EDGE, _lib.DM_VOL_ELEMENT
 
 
@@ -30,17 +32,36 @@ def run_all(eng, mesh):
     eng.build_edges()
     out = {"edgelist": eng.edges(), "e2l": eng.e2l()}
     out["inc_ptr"], out["inc"] = eng.incidence()
-    eng.navs(DF, GATHER)
+    eng.navs(DF, EXACT)
     out["navs_dualfree"] = eng.get_navs()
     eng.volumes(EDGE)
     out["vol_edge"] = eng.get_volumes()
     eng.volumes(ELEM)
     out["vol_element"] = eng.get_volumes()
+    eng.navs(DF, FACES)
+    out["navs_faces"] = eng.get_navs()
+    eng.navs(DF, ELEMV)
+    out["navs_elem"] = eng.get_navs()
     eng.navs(TR, GATHER)
     out["navs_traditional"] = eng.get_navs()
     eng.navs(DF, SCATTER)
     out["navs_scatter"] = eng.get_navs()
+    eng.navs(DF, GATHER)  # default fast path (ring walk in 3D)
+    out["navs_fast"] = eng.get_navs()
+    eng.volumes(EDGE)
+    out["vol_fast"] = eng.get_volumes()
+    eng.navs(DF, GATHER)
+    out["navs_fast2"] = eng.get_navs()
     return out
+
+
+def check_fast(g, want_navs, want_vol, dim):
+    """Default GATHER: deterministic, within 1e-12 of the serial oracle."""
+    np.testing.assert_array_equal(g["navs_fast"], g["navs_fast2"])  # SPEC.md:206
+    assert per_vector_rel(g["navs_fast"], want_navs, dim) <= 1e-12
+    assert np.abs(g["vol_fast"] - want_vol).max() <= 1e-12 * np.abs(want_vol).max()
+    np.testing.assert_array_equal(g["navs_faces"], want_navs)
+    np.testing.assert_array_equal(g["navs_elem"], want_navs)
 
 
 def test_fixtures_bit_exact(engine, fixtures, oracle):
@@ -54,6 +75,7 @@ def test_fixtures_bit_exact(engine, fixtures, oracle):
         np.testing.assert_array_equal(g["navs_traditional"], oracle.navs_traditional(m, e, o))
         np.testing.assert_array_equal(g["vol_edge"], oracle.volumes_edge(m, e, g["navs_dualfree"]))
         np.testing.assert_array_equal(g["vol_element"], oracle.volumes_element(m))
+        check_fast(g, g["navs_dualfree"], g["vol_edge"], m.dim)
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
@@ -68,6 +90,7 @@ def test_golden_configs_bit_exact(engine, golden_configs, name):
     for k in ("navs_dualfree", "navs_traditional", "vol_edge", "vol_element"):
         np.testing.assert_array_equal(g[k], gd[k], err_msg=k)
     assert per_vector_rel(g["navs_scatter"], gd["navs_dualfree"], gd["mesh"].dim) <= 1e-12
+    check_fast(g, gd["navs_dualfree"], gd["vol_edge"], gd["mesh"].dim)
 
 
 @pytest.mark.parametrize("name,scale", [("C1", 1), ("C2", 1), ("C3", 2), ("C4", 2)])
@@ -87,6 +110,7 @@ def test_live_oracle_parity(engine, oracle, name, scale):
     np.testing.assert_array_equal(g["vol_edge"], oracle.volumes_edge(m, e, nd))
     np.testing.assert_array_equal(g["vol_element"], oracle.volumes_element(m))
     assert per_vector_rel(g["navs_scatter"], nd, m.dim) <= 1e-12
+    check_fast(g, nd, oracle.volumes_edge(m, e, nd), m.dim)
 
 
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
@@ -97,19 +121,25 @@ def test_full_size_properties(engine, name):
     ne = engine.build_edges()
     if name == "C5":
         assert ne == 118031104 and m.num_nodes() == 16974593
-    engine.navs(DF, GATHER)
-    engine.volumes(EDGE)
-    r, ri = engine.check_closure()
-    assert r <= 1e-13 and ri <= 1e-13
-    rel, sv, se = engine.check_total_volume()
-    assert rel <= 1e-12
-    if name != "C4":
-        assert abs(sv - 1.0) <= 1e-12  # unit cube, PAPER §4.3
+    for variant in (GATHER, EXACT):
+        engine.navs(DF, variant)
+        engine.volumes(EDGE)
+        r, ri = engine.check_closure()
+        assert r <= 1e-13 and ri <= 1e-13
+        rel, sv, se = engine.check_total_volume()
+        assert rel <= 1e-12
+        if name != "C4":
+            assert abs(sv - 1.0) <= 1e-12  # unit cube, PAPER §4.3
     n1, v1 = engine.get_navs(), engine.get_volumes()
-    engine.navs(DF, GATHER)
+    engine.navs(DF, EXACT)
     engine.volumes(EDGE)
     np.testing.assert_array_equal(engine.get_navs(), n1)  # SPEC.md:206 determinism
     np.testing.assert_array_equal(engine.get_volumes(), v1)
+    engine.navs(DF, GATHER)
+    nf = engine.get_navs()
+    engine.navs(DF, GATHER)
+    np.testing.assert_array_equal(engine.get_navs(), nf)
+    assert per_vector_rel(nf, n1, m.dim) <= 1e-12
     engine.navs(DF, SCATTER)
     assert per_vector_rel(engine.get_navs(), n1, m.dim) <= 1e-12
     engine.navs(TR, GATHER)
