@@ -91,7 +91,7 @@ struct dm_ctx {
   dm::DevBuf<int32_t> tnodes;      // kTileNodeCap per tile (rings.cu)
   dm::DevBuf<dm::u32> tnode_cnt;
   dm::DevBuf<uint16_t> rcodes;     // n+3 per edge at inc_ptr[e] + 3e
-  dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU, 0}
+  dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU | nbnd << 16, bptr}
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
   dm::DevBuf<int32_t> n2e;
@@ -185,6 +185,10 @@ __device__ __forceinline__ double2 ld_d2(const double2* p) { return __ldg(p); }
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -393,29 +393,27 @@ __global__ void __launch_bounds__(kEB, MINB)
   d4 xj{}, xk{};
   if (valid) {
     const int base = pb + 3 * static_cast<int>(e);
-    xj = tab(cd[base]);
+    xj = tab(cd[base] & 0x7fffu);
     xk = tab(cd[base + 1]);
     d4 mp = tab(cd[base + 2]);
     double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
     const int n = pe - pb;
     for (int i = 0; i < n; ++i) {
-      const unsigned w = cd[base + 3 + i];
-      const d4 m = tab(w & 0x7fffu);
+      const d4 m = tab(cd[base + 3 + i]);
       const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
       double c0, c1, c2;
       cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
-      if (w & 0x8000u) {
-        acc[0] -= c0;
-        acc[1] -= c1;
-        acc[2] -= c2;
-      } else {
-        acc[0] += c0;
-        acc[1] += c1;
-        acc[2] += c2;
-      }
+      acc[0] += c0;
+      acc[1] += c1;
+      acc[2] += c2;
       dx = ex;
       dy = ey;
       dz = ez;
+    }
+    if (cd[base] & 0x8000u) {
+      acc[0] = -acc[0];
+      acc[1] = -acc[1];
+      acc[2] = -acc[2];
     }
   }
   double n[3] = {0.0, 0.0, 0.0};
@@ -429,38 +427,43 @@ __global__ void __launch_bounds__(kEB, MINB)
 }
 
 // ------------------------------------------------------------------ GATHER (pipelined ring walk)
-// Persistent form of k_navs_ring: each CTA walks tiles blockIdx.x,
-// blockIdx.x + gridDim.x, ...  While tile i is evaluated, the coordinates,
-// ring codes and inc_ptr slice of tile i+1 stream into the other half of a
-// double buffer with cp.async (LDGSTS, no register round trip), and the node
-// ids of tile i+2 are prefetched into registers -- so the per-tile gather
-// latency is hidden behind the previous tile's arithmetic.  Same arithmetic
-// and order as k_navs_ring.  Tiles with more than kPipeCap nodes or
-// kPipeCodeCap codes are evaluated straight from global memory.
-constexpr int kPipeCap = 1024;
+// Persistent form of the ring walk: each CTA walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ...  While tile i is evaluated, the coordinates
+// (2 x 16-byte cp.async per node into a 32-byte AoS table), ring codes and
+// inc_ptr slice of tile i+1 stream into the other half of a double buffer
+// with cp.async (LDGSTS, no register round trip), and the node ids and
+// metadata of tile i+2 are prefetched into registers -- so the per-tile
+// gather latency hides behind the previous tile's arithmetic.  The terms of
+// an edge are summed unsigned and the edge's common orientation applied
+// once.  Tiles with more than kPipeCap nodes or kPipeCodeCap codes are
+// evaluated straight from global memory (same arithmetic, same order).
 constexpr int kPipeCodeCap = 3072;
-constexpr int kIdsPerThread = kPipeCap / kEB;
 
+template <int CAP>
 struct PipeSmem {
-  double tab[2][3][kPipeCap];
+  d4 tab[2][CAP];
   uint32_t cd[2][kPipeCodeCap / 2 + 2];
   int32_t ip[2][kEB + 1];
 };
 
-__device__ __forceinline__ void pipe_issue(PipeSmem& S, int b, int tile, const int4& m,
-                                           const int (&ids)[kIdsPerThread], Coords<3> X,
+__device__ __forceinline__ int meta_nu(const int4& m) { return m.z & 0xffff; }
+
+template <int CAP>
+__device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, const int4& m,
+                                           const int (&ids)[CAP / kEB], Coords<3> X,
                                            const int32_t* __restrict__ inc_ptr,
                                            const uint16_t* __restrict__ rcodes, i64 ne) {
   const int t = threadIdx.x;
-  if (m.z <= kPipeCap) {
+  const int nu = meta_nu(m);
+  if (nu <= CAP) {
 #pragma unroll
-    for (int u = 0; u < kIdsPerThread; ++u) {
+    for (int u = 0; u < CAP / kEB; ++u) {
       const int i = t + u * kEB;
-      if (i < m.z) {
-        const double* src = reinterpret_cast<const double*>(X.p + ids[u]);
-        cp_async8(&S.tab[b][0][i], src);
-        cp_async8(&S.tab[b][1][i], src + 1);
-        cp_async8(&S.tab[b][2][i], src + 2);
+      if (i < nu) {
+        const d4* src = X.p + ids[u];
+        cp_async16(&S.tab[b][i], src);
+        cp_async16(reinterpret_cast<double*>(&S.tab[b][i]) + 2,
+                   reinterpret_cast<const double*>(src) + 2);
       }
     }
   }
@@ -474,109 +477,116 @@ __device__ __forceinline__ void pipe_issue(PipeSmem& S, int b, int tile, const i
   for (int i = t; i < cnt; i += kEB) cp_async4(&S.ip[b][i], inc_ptr + e0 + i);
 }
 
-__device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int4* __restrict__ meta,
-                                         const int32_t* __restrict__ tnodes, int4& m,
-                                         int (&ids)[kIdsPerThread]) {
+// ids of `tile` into registers (always the full kPipeCap window: the tile
+// list has a fixed stride, so no dependency on the tile's metadata).
+template <int NI>
+__device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __restrict__ tnodes,
+                                         int (&ids)[NI]) {
   if (tile < ntiles) {
-    m = __ldg(meta + tile);
     const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
 #pragma unroll
-    for (int u = 0; u < kIdsPerThread; ++u) {
-      const int i = threadIdx.x + u * kEB;
-      ids[u] = (i < m.z && m.z <= kPipeCap) ? __ldg(tn + i) : 0;
-    }
-  } else {
-    m = make_int4(0, 0, 0, 0);
+    for (int u = 0; u < NI; ++u) ids[u] = __ldg(tn + threadIdx.x + u * kEB);
   }
 }
 
-template <int MINB>
+template <bool kFast>
+__device__ __forceinline__ void ring_edge(const d4* __restrict__ tab, const int32_t* __restrict__ tn,
+                                          Coords<3> X, const uint16_t* __restrict__ cd, int base,
+                                          int n, double* acc, d4& xj, d4& xk) {
+  auto T = [&](unsigned i) -> d4 {
+    if constexpr (kFast) {
+      const double2 xy = *reinterpret_cast<const double2*>(&tab[i]);
+      d4 p;
+      p.x = xy.x;
+      p.y = xy.y;
+      p.z = tab[i].z;
+      return p;
+    } else {
+      return X[__ldg(tn + i)];
+    }
+  };
+  const unsigned w0 = cd[base];
+  xj = T(w0 & 0x7fffu);
+  xk = T(cd[base + 1]);
+  const d4 mp = T(cd[base + 2]);
+  double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const d4 m = T(cd[base + 3 + i]);
+    const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
+    double c0, c1, c2;
+    cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
+    a0 += c0;
+    a1 += c1;
+    a2 += c2;
+    dx = ex;
+    dy = ey;
+    dz = ez;
+  }
+  const bool neg = (w0 & 0x8000u) != 0;
+  acc[0] = neg ? -a0 : a0;
+  acc[1] = neg ? -a1 : a1;
+  acc[2] = neg ? -a2 : a2;
+}
+
+template <int CAP, int MINB>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      Coords<3> X, i64 ne, int ntiles, const u64* __restrict__ bedge,
-                     const u32* __restrict__ tile_bptr, const int32_t* __restrict__ bnd,
-                     double* __restrict__ navs, double* __restrict__ svals) {
+                     const int32_t* __restrict__ bnd, double* __restrict__ navs,
+                     double* __restrict__ svals) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
+  PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(smem_raw);
   const int t = threadIdx.x;
   const int lane = t & 31;
   int tile = blockIdx.x;
   if (tile >= ntiles) return;
-  // prologue: ids of tile 0 -> issue its copies; ids of tile 1 into registers
-  int4 m_cur, m_nxt;
-  int ids[kIdsPerThread];
-  pipe_ids(tile, ntiles, meta, tnodes, m_cur, ids);
+  const int G = gridDim.x;
+  // prologue: tile 0 -> buffer 0; ids / metadata of tile 1 into registers
+  int ids[CAP / kEB];
+  int4 m_cur = __ldg(meta + tile);
+  pipe_ids(tile, ntiles, tnodes, ids);
   pipe_issue(S, 0, tile, m_cur, ids, X, inc_ptr, rcodes, ne);
   cp_async_commit();
-  pipe_ids(tile + gridDim.x, ntiles, meta, tnodes, m_nxt, ids);
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+  int4 m_nxt = tile + G < ntiles ? __ldg(meta + tile + G) : make_int4(0, 0, 0, 0);
+  pipe_ids(tile + G, ntiles, tnodes, ids);
+  for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int b = it & 1;
-    const int nxt = tile + gridDim.x;
+    const int nxt = tile + G;
     if (nxt < ntiles) pipe_issue(S, b ^ 1, nxt, m_nxt, ids, X, inc_ptr, rcodes, ne);
     cp_async_commit();
     const int4 m = m_cur;
     m_cur = m_nxt;
-    pipe_ids(nxt + gridDim.x, ntiles, meta, tnodes, m_nxt, ids);
+    m_nxt = nxt + G < ntiles ? __ldg(meta + nxt + G) : make_int4(0, 0, 0, 0);
+    pipe_ids(nxt + G, ntiles, tnodes, ids);
     cp_async_wait<1>();
     __syncthreads();
     // ---- evaluate tile `tile` from buffer b
-    const i64 e0 = static_cast<i64>(tile) * kEB;
-    const i64 e = e0 + t;
+    const i64 e = static_cast<i64>(tile) * kEB + t;
     const bool valid = e < ne;
-    const bool tab_fast = m.z <= kPipeCap, cd_fast = m.y <= kPipeCodeCap;
-    const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
-    auto tab = [&](unsigned i) -> d4 {
-      d4 p;
-      if (tab_fast) {
-        p.x = S.tab[b][0][i];
-        p.y = S.tab[b][1][i];
-        p.z = S.tab[b][2][i];
-      } else {
-        p = X[__ldg(tn + i)];
-      }
-      return p;
-    };
-    const uint16_t* cd = cd_fast ? reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1)
-                                 : rcodes;
     double acc[3] = {0.0, 0.0, 0.0};
     d4 xj{}, xk{};
     if (valid) {
-      const int pb = S.ip[b][t], pe = S.ip[b][t + 1];
+      const int pb = S.ip[b][t], n = S.ip[b][t + 1] - pb;
       const int base = pb + 3 * static_cast<int>(e);
-      xj = tab(cd[base]);
-      xk = tab(cd[base + 1]);
-      const d4 mp = tab(cd[base + 2]);
-      double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
-      const int n = pe - pb;
-      for (int i = 0; i < n; ++i) {
-        const unsigned w = cd[base + 3 + i];
-        const d4 mm = tab(w & 0x7fffu);
-        const double ex = mm.x - xk.x, ey = mm.y - xk.y, ez = mm.z - xk.z;
-        double c0, c1, c2;
-        cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
-        if (w & 0x8000u) {
-          acc[0] -= c0;
-          acc[1] -= c1;
-          acc[2] -= c2;
-        } else {
-          acc[0] += c0;
-          acc[1] += c1;
-          acc[2] += c2;
-        }
-        dx = ex;
-        dy = ey;
-        dz = ez;
-      }
+      const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
+      if (meta_nu(m) <= CAP && m.y <= kPipeCodeCap)
+        ring_edge<true>(S.tab[b], tn, X,
+                        reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
+                        acc, xj, xk);
+      else
+        ring_edge<false>(S.tab[b], tn, X, rcodes, base, n, acc, xj, xk);
     }
-    double n[3] = {0.0, 0.0, 0.0};
+    double nv[3] = {0.0, 0.0, 0.0};
     double s = 0.0;
     if (valid) {
-      edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, tile_bptr[tile],
-                                     tile_bptr[tile + 1], bnd, n, s);
+      const u32 rb = static_cast<u32>(m.w);
+      edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, rb,
+                                     rb + (static_cast<u32>(m.z) >> 16), bnd, nv, s);
       svals[e] = s;
     }
-    store_navs_warp<3>(n, e - lane, ne, navs);
+    store_navs_warp<3>(nv, e - lane, ne, navs);
     __syncthreads();  // buffer b is refilled two iterations from now
   }
   cp_async_wait<0>();
@@ -800,17 +810,25 @@ int launch_navs(dm_ctx* c, int variant) {
                   c->tnode_cnt.p, X, ne, c->bedge.p, c->tile_bptr.p, c->bnd.p, c->navs.p,
                   c->svals.p);
       } else {
-        const int smem = static_cast<int>(sizeof(PipeSmem));
-        auto kern = c->gather_cfg == 1 ? k_navs_ring_pipe<2> : k_navs_ring_pipe<3>;
-        DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int per_sm = 0, nsm = 0;
-        DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
-        DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-        const unsigned grid = static_cast<unsigned>(
-            std::min<i64>(static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
-        DM_LAUNCH(c, kern, grid, kEB, smem, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
-                  c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->tile_bptr.p,
-                  c->bnd.p, c->navs.p, c->svals.p);
+        auto launch = [&](auto kern, int smem) -> int {
+          DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          int per_sm = 0, nsm = 0;
+          DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
+          DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+          const unsigned grid = static_cast<unsigned>(std::min<i64>(
+              static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
+          DM_LAUNCH(c, kern, grid, kEB, smem, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
+                    c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->bnd.p,
+                    c->navs.p, c->svals.p);
+          return DM_OK;
+        };
+        int st = DM_OK;
+        switch (c->gather_cfg) {
+          case 1: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
+          case 2: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
+          default: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
+        }
+        if (st) return st;
       }
     }
     tmark(c, 1);

@@ -13,8 +13,12 @@
 //                tile touches (j, k, ring nodes), at a fixed stride of
 //                kTileNodeCap, count in tnode_cnt[tile].
 //   ring codes : per edge, n+3 16-bit words at offset inc_ptr[e] + 3e:
-//                  [slot(j), slot(k), slot(m_0), slot(m_1)|s_0<<15, ...,
-//                   slot(m_n)|s_(n-1)<<15]      (slots into the tile list)
+//                  [slot(j) | s<<15, slot(k), slot(m_0), slot(m_1), ...,
+//                   slot(m_n)]                  (slots into the tile list)
+//                where s is the common orientation of all terms of the edge:
+//                around a consistently oriented ring every term has the same
+//                parity, so the sign is applied once to the sum
+//                (sum(-c_i) == -sum(c_i) exactly in IEEE arithmetic).
 // Built once per topology.  Any tile with more than kTileNodeCap nodes, an
 // edge with more than kRingMax incidences or a non-manifold fan (the walk
 // does not consume every incident element) sets ring_ok = false and the
@@ -171,7 +175,7 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
     }
   if (start < 0) start = a[0];
   uint16_t* out = rcodes + pb + 3 * e;
-  out[0] = static_cast<uint16_t>(tslot(list, nl, j));
+  int sg0 = 0;
   out[1] = static_cast<uint16_t>(tslot(list, nl, k));
   out[2] = static_cast<uint16_t>(tslot(list, nl, start));
   unsigned used = 0;
@@ -190,25 +194,36 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
     used |= 1u << pick;
     const int nxt = a[pick] == cur ? b[pick] : a[pick];
     const int sg = perm_sign(k, cur, nxt, p0[pick], p1[pick], p2[pick]);
-    out[3 + step] = static_cast<uint16_t>(tslot(list, nl, nxt) | (sg < 0 ? 0x8000u : 0u));
+    if (step == 0) sg0 = sg;
+    else if (sg != sg0) {
+      atomicOr(flag, 16);  // inconsistently oriented fan
+      return;
+    }
+    out[3 + step] = static_cast<uint16_t>(tslot(list, nl, nxt));
     cur = nxt;
   }
+  out[0] = static_cast<uint16_t>(tslot(list, nl, j) | (sg0 < 0 ? 0x8000u : 0u));
 }
 
 __global__ void k_ring_meta(const int32_t* __restrict__ inc_ptr, const u32* __restrict__ tcnt,
-                            i64 ne, i64 ntiles, int4* __restrict__ meta) {
+                            const u32* __restrict__ tile_bptr, i64 ne, i64 ntiles,
+                            int4* __restrict__ meta) {
   const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
   const i64 e0 = t * kTileEdges, e1 = (e0 + kTileEdges < ne) ? e0 + kTileEdges : ne;
   const int C0 = inc_ptr[e0] + 3 * static_cast<int>(e0);
   const int C1 = inc_ptr[e1] + 3 * static_cast<int>(e1);
-  meta[t] = make_int4(C0, C1 - C0, static_cast<int>(tcnt[t]), 0);
+  const int nb = static_cast<int>(tile_bptr[t + 1] - tile_bptr[t]);  // <= 3 * 256
+  meta[t] = make_int4(C0, C1 - C0, static_cast<int>(tcnt[t]) | nb << 16,
+                      static_cast<int>(tile_bptr[t]));
 }
 
 }  // namespace
 
 int ensure_rings(dm_ctx* c) {
   if (c->have_rings) return DM_OK;
+  int st0 = ensure_bedge(c);  // tile_bptr feeds the ring metadata
+  if (st0) return st0;
   if (c->dim != 3) {
     c->ring_ok = false;
     c->have_rings = true;
@@ -227,8 +242,8 @@ int ensure_rings(dm_ctx* c) {
             c->inc_ptr.p, c->inc.p, c->elems.p, ne, c->tnodes.p, c->tnode_cnt.p, c->flag.p);
   DM_LAUNCH(c, k_ring_codes, grid_for(ne, 128), 128, 0, c->edges.p, c->inc_ptr.p, c->inc.p,
             c->elems.p, c->tnodes.p, c->tnode_cnt.p, ne, c->rcodes.p, c->flag.p);
-  DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, c->inc_ptr.p, c->tnode_cnt.p, ne,
-            ntiles, c->ring_meta.p);
+  DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, c->inc_ptr.p, c->tnode_cnt.p,
+            c->tile_bptr.p, ne, ntiles, c->ring_meta.p);
   int fl[2] = {0, 0};
   DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
