@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(kEB, MINB)
 // once.  Tiles with more than kPipeCap nodes or kPipeCodeCap codes are
 // evaluated straight from global memory (same arithmetic, same order).
 constexpr int kPipeCodeCap = 3072;
+extern __shared__ __align__(128) unsigned char dm_smem[];
 
 template <int CAP>
 struct PipeSmem {
@@ -489,7 +490,7 @@ __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __
   }
 }
 
-template <bool kFast>
+template <bool kFast, int RU = 1>
 __device__ __forceinline__ void ring_edge(const d4* __restrict__ tab, const int32_t* __restrict__ tn,
                                           Coords<3> X, const uint16_t* __restrict__ cd, int base,
                                           int n, double* acc, d4& xj, d4& xk) {
@@ -511,17 +512,29 @@ __device__ __forceinline__ void ring_edge(const d4* __restrict__ tab, const int3
   const d4 mp = T(cd[base + 2]);
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const d4 m = T(cd[base + 3 + i]);
-    const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
-    double c0, c1, c2;
-    cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
-    a0 += c0;
-    a1 += c1;
-    a2 += c2;
-    dx = ex;
-    dy = ey;
-    dz = ez;
+  // RU ring steps per batch: all codes, then all table reads, then the
+  // sequential fold -- independent loads overlap instead of chaining.
+  for (int i0 = 0; i0 < n; i0 += RU) {
+    unsigned w[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) w[u] = i0 + u < n ? cd[base + 3 + i0 + u] : 0u;
+    d4 m[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) m[u] = T(w[u]);
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      if (i0 + u < n) {
+        const double ex = m[u].x - xk.x, ey = m[u].y - xk.y, ez = m[u].z - xk.z;
+        double c0, c1, c2;
+        cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
+        a0 += c0;
+        a1 += c1;
+        a2 += c2;
+        dx = ex;
+        dy = ey;
+        dz = ez;
+      }
+    }
   }
   const bool neg = (w0 & 0x8000u) != 0;
   acc[0] = neg ? -a0 : a0;
@@ -529,15 +542,14 @@ __device__ __forceinline__ void ring_edge(const d4* __restrict__ tab, const int3
   acc[2] = neg ? -a2 : a2;
 }
 
-template <int CAP, int MINB>
+template <int CAP, int MINB, int RU = 1>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      Coords<3> X, i64 ne, int ntiles, const u64* __restrict__ bedge,
                      const int32_t* __restrict__ bnd, double* __restrict__ navs,
                      double* __restrict__ svals) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(smem_raw);
+  PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(dm_smem);
   const int t = threadIdx.x;
   const int lane = t & 31;
   int tile = blockIdx.x;
@@ -572,7 +584,7 @@ __global__ void __launch_bounds__(kEB, MINB)
       const int base = pb + 3 * static_cast<int>(e);
       const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
       if (meta_nu(m) <= CAP && m.y <= kPipeCodeCap)
-        ring_edge<true>(S.tab[b], tn, X,
+        ring_edge<true, RU>(S.tab[b], tn, X,
                         reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
                         acc, xj, xk);
       else
@@ -588,6 +600,123 @@ __global__ void __launch_bounds__(kEB, MINB)
     }
     store_navs_warp<3>(nv, e - lane, ne, navs);
     __syncthreads();  // buffer b is refilled two iterations from now
+  }
+  cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------ GATHER (ring walk, TMA)
+// The default 3D dual-free kernel.  Same pipeline as k_navs_ring_pipe, but
+// the coordinate table of the next tile is fetched by the TMA engine with
+// tile::gather4 (4 node records of 32 bytes per instruction, completion on
+// a per-buffer mbarrier) instead of per-lane cp.async: the gather costs no
+// LSU / L1 wavefronts and no shared-memory write conflicts.
+template <int CAP>
+struct TmaSmem {
+  d4 tab[2][CAP];  // 128-byte aligned: each gather4 lands 4 records = 128 B
+  uint32_t cd[2][kPipeCodeCap / 2 + 2];
+  int32_t ip[2][kEB + 1];
+  unsigned long long mbar[2];
+};
+
+template <int CAP>
+__device__ __forceinline__ void tma_issue(TmaSmem<CAP>& S, int b, int tile, const int4& m,
+                                          const int (&ids)[CAP / kEB], const CUtensorMap* map,
+                                          const int32_t* __restrict__ inc_ptr,
+                                          const uint16_t* __restrict__ rcodes, i64 ne) {
+  const int t = threadIdx.x;
+  const int nu = meta_nu(m);
+  if (nu <= CAP) {
+    const int groups = (nu + 3) >> 2;
+    if (t == 0) mbar_expect_tx(&S.mbar[b], static_cast<unsigned>(groups) * 128u);
+#pragma unroll
+    for (int u = 0; u < CAP / kEB; ++u) {
+      // lanes 4g..4g+3 hold nodes 4g..4g+3 of this stripe; lane 4g issues
+      const int i = t + u * kEB;
+      const int id = i < nu ? ids[u] : 0;
+      const int r1 = __shfl_down_sync(0xffffffffu, id, 1);
+      const int r2 = __shfl_down_sync(0xffffffffu, id, 2);
+      const int r3 = __shfl_down_sync(0xffffffffu, id, 3);
+      if ((t & 3) == 0 && i < nu) tma_gather4(&S.tab[b][i], map, &S.mbar[b], id, r1, r2, r3);
+    }
+  }
+  if (m.y <= kPipeCodeCap) {
+    const int w0 = m.x >> 1, w1 = (m.x + m.y + 1) >> 1;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(rcodes);
+    for (int w = w0 + t; w < w1; w += kEB) cp_async4(&S.cd[b][w - w0], src + w);
+  }
+  const i64 e0 = static_cast<i64>(tile) * kEB;
+  const i64 cnt = (e0 + kEB < ne ? kEB : ne - e0) + 1;
+  for (int i = t; i < cnt; i += kEB) cp_async4(&S.ip[b][i], inc_ptr + e0 + i);
+}
+
+template <int CAP, int MINB>
+__global__ void __launch_bounds__(kEB, MINB)
+    k_navs_ring_tma(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ inc_ptr,
+                    const uint16_t* __restrict__ rcodes, const int32_t* __restrict__ tnodes,
+                    const int4* __restrict__ meta, Coords<3> X, i64 ne, int ntiles,
+                    const u64* __restrict__ bedge, const int32_t* __restrict__ bnd,
+                    double* __restrict__ navs, double* __restrict__ svals) {
+  TmaSmem<CAP>& S = *reinterpret_cast<TmaSmem<CAP>*>(dm_smem);
+  const int t = threadIdx.x;
+  const int lane = t & 31;
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  const int G = gridDim.x;
+  if (t == 0) {
+    mbar_init(&S.mbar[0], 1);
+    mbar_init(&S.mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phases = 0u;  // bit b = parity of buffer b's mbarrier
+  int ids[CAP / kEB];
+  int4 m_cur = __ldg(meta + tile);
+  pipe_ids(tile, ntiles, tnodes, ids);
+  tma_issue(S, 0, tile, m_cur, ids, &xmap, inc_ptr, rcodes, ne);
+  cp_async_commit();
+  int4 m_nxt = tile + G < ntiles ? __ldg(meta + tile + G) : make_int4(0, 0, 0, 0);
+  pipe_ids(tile + G, ntiles, tnodes, ids);
+  for (int it = 0; tile < ntiles; ++it, tile += G) {
+    const int b = it & 1;
+    const int nxt = tile + G;
+    if (nxt < ntiles) tma_issue(S, b ^ 1, nxt, m_nxt, ids, &xmap, inc_ptr, rcodes, ne);
+    cp_async_commit();
+    const int4 m = m_cur;
+    m_cur = m_nxt;
+    m_nxt = nxt + G < ntiles ? __ldg(meta + nxt + G) : make_int4(0, 0, 0, 0);
+    pipe_ids(nxt + G, ntiles, tnodes, ids);
+    cp_async_wait<1>();
+    const bool tab_fast = meta_nu(m) <= CAP;
+    if (tab_fast) {
+      mbar_wait(&S.mbar[b], (phases >> b) & 1u);
+      phases ^= 1u << b;
+    }
+    __syncthreads();
+    const i64 e = static_cast<i64>(tile) * kEB + t;
+    const bool valid = e < ne;
+    double acc[3] = {0.0, 0.0, 0.0};
+    d4 xj{}, xk{};
+    if (valid) {
+      const int pb = S.ip[b][t], n = S.ip[b][t + 1] - pb;
+      const int base = pb + 3 * static_cast<int>(e);
+      const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
+      if (tab_fast && m.y <= kPipeCodeCap)
+        ring_edge<true>(S.tab[b], tn, X,
+                        reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
+                        acc, xj, xk);
+      else
+        ring_edge<false>(S.tab[b], tn, X, rcodes, base, n, acc, xj, xk);
+    }
+    double nv[3] = {0.0, 0.0, 0.0};
+    double s = 0.0;
+    if (valid) {
+      const u32 rb = static_cast<u32>(m.w);
+      edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, rb,
+                                     rb + (static_cast<u32>(m.z) >> 16), bnd, nv, s);
+      svals[e] = s;
+    }
+    store_navs_warp<3>(nv, e - lane, ne, navs);
+    __syncthreads();  // buffer b is refilled next iteration
   }
   cp_async_wait<0>();
 }
@@ -822,10 +951,27 @@ int launch_navs(dm_ctx* c, int variant) {
                     c->navs.p, c->svals.p);
           return DM_OK;
         };
+        auto launch_tma = [&](auto kern, int smem) -> int {
+          DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          int per_sm = 0, nsm = 0;
+          DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
+          DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+          const unsigned grid = static_cast<unsigned>(std::min<i64>(
+              static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
+          DM_LAUNCH(c, kern, grid, kEB, smem, c->x4_map, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
+                    c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->bnd.p,
+                    c->navs.p, c->svals.p);
+          return DM_OK;
+        };
         int st = DM_OK;
-        switch (c->gather_cfg) {
-          case 1: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
-          case 2: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
+        // default: cp.async pipeline (TMA gather4 variants measured slower: cfg 0-2)
+        const int cfg = c->gather_cfg == 0 || !c->x4_map_ok ? 6 : c->gather_cfg;
+        switch (cfg) {
+          case 1: st = launch_tma(k_navs_ring_tma<1024, 2>, sizeof(TmaSmem<1024>)); break;
+          case 2: st = launch_tma(k_navs_ring_tma<512, 4>, sizeof(TmaSmem<512>)); break;
+          case 6: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
+          case 7: st = launch(k_navs_ring_pipe<768, 3, 2>, sizeof(PipeSmem<768>)); break;
+          case 3: st = launch_tma(k_navs_ring_tma<768, 3>, sizeof(TmaSmem<768>)); break;
           default: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
         }
         if (st) return st;
