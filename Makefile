@@ -20,7 +20,7 @@ CU_SRCS := $(CSRC)/capi.cu $(CSRC)/primitives.cu $(CSRC)/edges.cu $(CSRC)/navs.c
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) include/dm_capi.h
 
-all: $(LIBDIR)/libdualmesh.so $(LIBDIR)/libdm_meshgen.so oracle
+all: $(LIBDIR)/libdualmesh.so $(LIBDIR)/libdm_meshgen.so oracle tests/cpp/_build/libapi_probe.so
 
 build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build
@@ -37,6 +37,11 @@ $(LIBDIR)/libdualmesh.so: $(CU_OBJS) build/host_api.o
 $(LIBDIR)/libdm_meshgen.so: $(CSRC)/meshgen.cpp include/dm_meshgen.h
 	@mkdir -p $(LIBDIR)
 	$(CXX) $(CXXFLAGS) -O3 -shared -o $@ $<
+
+# test infrastructure: extern "C" probe over the C++ drop-in API
+tests/cpp/_build/libapi_probe.so: tests/cpp/api_probe.cpp $(LIBDIR)/libdualmesh.so include/dualmesh/mesh.hpp
+	@mkdir -p tests/cpp/_build
+	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -ldualmesh -Wl,-rpath,'$$ORIGIN/../../../$(LIBDIR)'
 
 oracle:
 	$(MAKE) -C oracle

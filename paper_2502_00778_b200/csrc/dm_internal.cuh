@@ -119,6 +119,7 @@ struct dm_ctx {
   dm::DevBuf<int32_t> derived;
   dm::DevBuf<dm::i64> vlist;  // first offending ids per class
   dm::i64 vlist_n[DM_VCOUNT] = {0};
+  dm::i64 vlist_cap = 0;
 
   // tuning knob for the GATHER kernel shape (env DUALMESH_GATHER_CFG)
   int gather_cfg = 0;
@@ -285,6 +286,8 @@ int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n);
 // 4096 keys (larger ones set *flag = 1).  Keys are u32 or u64.
 int segment_sort_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg);
 int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg);
+// (key, value) pairs sorted lexicographically within each segment.
+int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg);
 
 // Derived structures, built lazily.
 int ensure_incoming(dm_ctx* c);

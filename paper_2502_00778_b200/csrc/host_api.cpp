@@ -188,9 +188,9 @@ ValidationOutcome validate_mesh(const Mesh& mesh) {
   out.volume_signs.assign(signs.begin(), signs.end());
   for (int64_t e : ids(DM_V_NONPOSITIVE))
     out.violations.push_back("nonpositive volume, element " + std::to_string(e + 1));
-  for (int64_t e : ids(DM_V_FACE_OVERSHARED))
+  for (int64_t f : ids(DM_V_FACE_OVERSHARED))  // f = element * (dim+1) + local face
     out.violations.push_back("face shared by more than two elements, element " +
-                             std::to_string(e + 1));
+                             std::to_string(f / (mesh.dim + 1) + 1));
   // Boundary classes are reported in facet order, interleaved as in the
   // reference loop: merge the per-class lists (payload: b << 32 | aux).
   std::vector<std::pair<int64_t, std::string>> bmsgs;

@@ -177,7 +177,109 @@ int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg) {
   return DM_OK;
 }
 
+// ---- key/value variant: sorts (key, value) pairs lexicographically
+template <bool kWarp>
+__device__ void bitonic_kv(u64* k, u32* v, int P, int tid, int nthr) {
+  for (int kk = 2; kk <= P; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += nthr) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const u64 a = k[i], b = k[ixj];
+          const u32 va = v[i], vb = v[ixj];
+          const bool gt = a > b || (a == b && va > vb);
+          if (gt == ((i & kk) == 0)) {
+            k[i] = b;
+            k[ixj] = a;
+            v[i] = vb;
+            v[ixj] = va;
+          }
+        }
+      }
+      if (kWarp) __syncwarp();
+      else __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_segsort_kv_warp(u64* keys, u32* vals, const u32* seg, i64 nseg, u32* big, int* nbig) {
+  __shared__ u64 sk[8][kWarpSeg];
+  __shared__ u32 sv[8][kWarpSeg];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 s = static_cast<i64>(blockIdx.x) * 8 + warp;
+  if (s >= nseg) return;
+  const u32 b = seg[s];
+  const int n = static_cast<int>(seg[s + 1] - b);
+  if (n <= 1) return;
+  if (n > kWarpSeg) {
+    if (lane == 0) big[atomicAdd(nbig, 1)] = static_cast<u32>(s);
+    return;
+  }
+  int P = 2;
+  while (P < n) P <<= 1;
+  for (int i = lane; i < P; i += 32) {
+    sk[warp][i] = i < n ? keys[b + i] : ~0ull;
+    sv[warp][i] = i < n ? vals[b + i] : ~0u;
+  }
+  __syncwarp();
+  bitonic_kv<true>(sk[warp], sv[warp], P, lane, 32);
+  for (int i = lane; i < n; i += 32) {
+    keys[b + i] = sk[warp][i];
+    vals[b + i] = sv[warp][i];
+  }
+}
+
+__global__ void __launch_bounds__(512)
+    k_segsort_kv_block(u64* keys, u32* vals, const u32* seg, const u32* big, const int* nbig,
+                       int* flag) {
+  extern __shared__ unsigned char smem_raw[];
+  u64* sk = reinterpret_cast<u64*>(smem_raw);
+  u32* sv = reinterpret_cast<u32*>(sk + kBlockSeg);
+  const int count = *nbig;
+  for (int q = blockIdx.x; q < count; q += gridDim.x) {
+    const u32 s = big[q];
+    const u32 b = seg[s];
+    const int n = static_cast<int>(seg[s + 1] - b);
+    if (n > kBlockSeg) {
+      if (threadIdx.x == 0) atomicExch(flag, 1);
+      continue;
+    }
+    int P = 2;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      sk[i] = i < n ? keys[b + i] : ~0ull;
+      sv[i] = i < n ? vals[b + i] : ~0u;
+    }
+    __syncthreads();
+    bitonic_kv<false>(sk, sv, P, threadIdx.x, blockDim.x);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      keys[b + i] = sk[i];
+      vals[b + i] = sv[i];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg) {
+  if (nseg <= 0) return DM_OK;
+  DevBuf<u32> big;
+  DM_CK(c, big.ensure(static_cast<size_t>(nseg)));
+  DM_CK(c, c->flag.ensure(4));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
+  int* nbig = c->flag.p + 1;
+  DM_LAUNCH(c, k_segsort_kv_warp, grid_for(nseg, 8), 256, 0, keys, vals, seg, nseg, big.p, nbig);
+  const size_t smem = kBlockSeg * (sizeof(u64) + sizeof(u32));
+  DM_CK(c, cudaFuncSetAttribute(k_segsort_kv_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  DM_LAUNCH(c, k_segsort_kv_block, 296, 512, smem, keys, vals, seg, big.p, nbig, c->flag.p);
+  int f = 0;
+  int st = read_flag(c, &f);
+  if (st) return st;
+  if (f) return fail(c, DM_ERR_UNSUPPORTED, "segment longer than 4096 keys (node valence too high)");
+  return DM_OK;
+}
 
 int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n) {
   // temp: sum over levels of (nb+1)

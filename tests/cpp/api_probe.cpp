@@ -1,0 +1,110 @@
+// api_probe.cpp -- TEST INFRASTRUCTURE: extern "C" wrappers that call the
+// C++ drop-in API (include/dualmesh/*.hpp, implemented by libdualmesh.so) so
+// the Python tests can compare it with the reference's own mesh.cpp
+// (oracle/_ref).  Built by the top-level Makefile into build/libapi_probe.so.
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "dualmesh/mesh.hpp"
+#include "dualmesh/metrics.hpp"
+
+namespace {
+dualmesh::Mesh make(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                    const int32_t* b, int64_t nb) {
+  dualmesh::Mesh m;
+  m.dim = dim;
+  m.coords.assign(x, x + dim * nv);
+  m.elements.assign(el, el + (dim + 1) * ne);
+  if (nb) m.boundary.assign(b, b + dim * nb);
+  return m;
+}
+}  // namespace
+
+extern "C" {
+
+// Returns the number of violations (or -1 on exception, message in buf).
+int64_t probe_validate(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                       const int32_t* b, int64_t nb, char* buf, int64_t cap, int8_t* signs) {
+  try {
+    auto out = dualmesh::validate_mesh(make(dim, x, nv, el, ne, b, nb));
+    std::string j;
+    for (const auto& v : out.violations) j += v + "\n";
+    std::strncpy(buf, j.c_str(), static_cast<size_t>(cap - 1));
+    buf[cap - 1] = '\0';
+    if (signs)
+      for (size_t e = 0; e < out.volume_signs.size(); ++e) signs[e] = out.volume_signs[e];
+    return static_cast<int64_t>(out.violations.size());
+  } catch (const std::exception& ex) {
+    std::strncpy(buf, ex.what(), static_cast<size_t>(cap - 1));
+    buf[cap - 1] = '\0';
+    return -1;
+  }
+}
+
+int64_t probe_derive(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                     int32_t* out, int64_t cap) {
+  auto f = dualmesh::derive_boundary_faces(make(dim, x, nv, el, ne, nullptr, 0));
+  for (size_t i = 0; i < f.size() && static_cast<int64_t>(i) < cap; ++i) out[i] = f[i];
+  return static_cast<int64_t>(f.size());
+}
+
+int64_t probe_build_edges(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                          int32_t* edges, uint64_t* os, int64_t cap) {
+  auto l = dualmesh::build_edges(make(dim, x, nv, el, ne, nullptr, 0));
+  for (size_t i = 0; i < l.size() && static_cast<int64_t>(i) < cap; ++i) {
+    edges[2 * i] = l.edges[i][0];
+    edges[2 * i + 1] = l.edges[i][1];
+  }
+  for (size_t v = 0; v < l.origin_start.size(); ++v) os[v] = l.origin_start[v];
+  return static_cast<int64_t>(l.size());
+}
+
+// compute_metrics + the checks; returns 0, or -1 / -2 on invalid_argument / runtime_error.
+int probe_compute_metrics(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                          const int32_t* b, int64_t nb, int nav_algo, int vol_algo, double* navs,
+                          double* vols, double* closure, double* total_rel) {
+  try {
+    auto m = make(dim, x, nv, el, ne, b, nb);
+    auto r = dualmesh::compute_metrics(m, static_cast<dualmesh::NavAlgo>(nav_algo),
+                                       static_cast<dualmesh::VolAlgo>(vol_algo));
+    std::memcpy(navs, r.navs.navs.data(), r.navs.navs.size() * sizeof(double));
+    std::memcpy(vols, r.volumes.volumes.data(), r.volumes.volumes.size() * sizeof(double));
+    *closure = dualmesh::check_closure(m, r.edges, r.navs);
+    *total_rel = dualmesh::check_total_volume(m, r.volumes);
+    // the stand-alone SPEC ops must agree with the facade
+    auto n2 = dualmesh::lumped_navs_dualfree(m, r.edges);
+    auto v2 = dualmesh::dual_volumes_edge_based(m, r.edges, n2);
+    if (nav_algo == 1 && vol_algo == 0 &&
+        (n2.navs != r.navs.navs || v2.volumes != r.volumes.volumes))
+      return -3;
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  } catch (const std::exception&) {
+    return -2;
+  }
+}
+
+// mesh/edge mismatch must raise std::invalid_argument.
+int probe_mismatch(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne) {
+  auto m = make(dim, x, nv, el, ne, nullptr, 0);
+  auto l = dualmesh::build_edges(m);
+  l.edges.pop_back();
+  try {
+    dualmesh::lumped_navs_dualfree(m, l);
+  } catch (const std::invalid_argument&) {
+    return 1;
+  } catch (...) {
+    return 2;
+  }
+  return 0;
+}
+
+double probe_element_volume(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                            int64_t e) {
+  return dualmesh::element_volume(make(dim, x, nv, el, ne, nullptr, 0), static_cast<size_t>(e));
+}
+
+}  // extern "C"
