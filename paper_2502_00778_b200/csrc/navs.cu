@@ -442,7 +442,11 @@ extern __shared__ __align__(128) unsigned char dm_smem[];
 
 template <int CAP>
 struct PipeSmem {
-  d4 tab[2][CAP];
+  // node table split into a 16-byte (x,y) array and an 8-byte z array: a
+  // random 16-byte LDS spreads over 8 bank groups instead of the 4 a 32-byte
+  // record allows, and z over 16 (fewer conflict wavefronts per read)
+  double2 xy[2][CAP];
+  double z[2][CAP];
   uint32_t cd[2][kPipeCodeCap / 2 + 2];
   int32_t ip[2][kEB + 1];
 };
@@ -461,10 +465,9 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
     for (int u = 0; u < CAP / kEB; ++u) {
       const int i = t + u * kEB;
       if (i < nu) {
-        const d4* src = X.p + ids[u];
-        cp_async16(&S.tab[b][i], src);
-        cp_async16(reinterpret_cast<double*>(&S.tab[b][i]) + 2,
-                   reinterpret_cast<const double*>(src) + 2);
+        const double* src = reinterpret_cast<const double*>(X.p + ids[u]);
+        cp_async16(&S.xy[b][i], src);
+        cp_async8(&S.z[b][i], src + 2);
       }
     }
   }
@@ -490,22 +493,10 @@ __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __
   }
 }
 
-template <bool kFast, int RU = 1>
-__device__ __forceinline__ void ring_edge(const d4* __restrict__ tab, const int32_t* __restrict__ tn,
-                                          Coords<3> X, const uint16_t* __restrict__ cd, int base,
-                                          int n, double* acc, d4& xj, d4& xk) {
-  auto T = [&](unsigned i) -> d4 {
-    if constexpr (kFast) {
-      const double2 xy = *reinterpret_cast<const double2*>(&tab[i]);
-      d4 p;
-      p.x = xy.x;
-      p.y = xy.y;
-      p.z = tab[i].z;
-      return p;
-    } else {
-      return X[__ldg(tn + i)];
-    }
-  };
+// Walks one edge's ring; T(slot) returns the node record of a tile slot.
+template <int RU = 1, typename TabFn>
+__device__ __forceinline__ void ring_walk(const TabFn& T, const uint16_t* __restrict__ cd,
+                                          int base, int n, double* acc, d4& xj, d4& xk) {
   const unsigned w0 = cd[base];
   xj = T(w0 & 0x7fffu);
   xk = T(cd[base + 1]);
@@ -583,12 +574,23 @@ __global__ void __launch_bounds__(kEB, MINB)
       const int pb = S.ip[b][t], n = S.ip[b][t + 1] - pb;
       const int base = pb + 3 * static_cast<int>(e);
       const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
-      if (meta_nu(m) <= CAP && m.y <= kPipeCodeCap)
-        ring_edge<true, RU>(S.tab[b], tn, X,
-                        reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
-                        acc, xj, xk);
-      else
-        ring_edge<false>(S.tab[b], tn, X, rcodes, base, n, acc, xj, xk);
+      if (meta_nu(m) <= CAP && m.y <= kPipeCodeCap) {
+        const double2* xy = S.xy[b];
+        const double* zz = S.z[b];
+        auto T = [&](unsigned i) -> d4 {
+          const double2 v = xy[i];
+          d4 p;
+          p.x = v.x;
+          p.y = v.y;
+          p.z = zz[i];
+          return p;
+        };
+        ring_walk<RU>(T, reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
+                      acc, xj, xk);
+      } else {
+        auto T = [&](unsigned i) -> d4 { return X[__ldg(tn + i)]; };
+        ring_walk(T, rcodes, base, n, acc, xj, xk);
+      }
     }
     double nv[3] = {0.0, 0.0, 0.0};
     double s = 0.0;
@@ -700,12 +702,22 @@ __global__ void __launch_bounds__(kEB, MINB)
       const int pb = S.ip[b][t], n = S.ip[b][t + 1] - pb;
       const int base = pb + 3 * static_cast<int>(e);
       const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
-      if (tab_fast && m.y <= kPipeCodeCap)
-        ring_edge<true>(S.tab[b], tn, X,
-                        reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
-                        acc, xj, xk);
-      else
-        ring_edge<false>(S.tab[b], tn, X, rcodes, base, n, acc, xj, xk);
+      if (tab_fast && m.y <= kPipeCodeCap) {
+        const d4* tb = S.tab[b];
+        auto T = [&](unsigned i) -> d4 {
+          const double2 v = *reinterpret_cast<const double2*>(&tb[i]);
+          d4 p;
+          p.x = v.x;
+          p.y = v.y;
+          p.z = tb[i].z;
+          return p;
+        };
+        ring_walk(T, reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n, acc,
+                  xj, xk);
+      } else {
+        auto T = [&](unsigned i) -> d4 { return X[__ldg(tn + i)]; };
+        ring_walk(T, rcodes, base, n, acc, xj, xk);
+      }
     }
     double nv[3] = {0.0, 0.0, 0.0};
     double s = 0.0;
@@ -971,6 +983,9 @@ int launch_navs(dm_ctx* c, int variant) {
           case 2: st = launch_tma(k_navs_ring_tma<512, 4>, sizeof(TmaSmem<512>)); break;
           case 6: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
           case 7: st = launch(k_navs_ring_pipe<768, 3, 2>, sizeof(PipeSmem<768>)); break;
+          case 8: st = launch(k_navs_ring_pipe<640, 4>, sizeof(PipeSmem<640>)); break;
+          case 9: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
+          case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
           case 3: st = launch_tma(k_navs_ring_tma<768, 3>, sizeof(TmaSmem<768>)); break;
           default: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
         }
