@@ -338,94 +338,6 @@ __global__ void __launch_bounds__(kEB, MINB)
   store_navs_warp<D>(n, e - lane, ne, navs);
 }
 
-// ------------------------------------------------------------------ GATHER (ring walk)
-// One CTA per 256-edge tile, one thread per edge (3D dual-free).  The tile's
-// unique node set (rings.cu) is gathered once into shared memory; each edge
-// then walks the ring of its incident elements: one table read per
-// incidence, term +-cross(m_i - x_k, m_(i+1) - x_k), summed in ring order.
-// Deterministic (fixed order), within rounding of the serial oracle, which
-// sums in ascending element order instead (tests bound it by 1e-12).
-constexpr int kRingCodeCap = 3072;
-
-template <int MINB>
-__global__ void __launch_bounds__(kEB, MINB)
-    k_navs_ring(const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ rcodes,
-                const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt, Coords<3> X,
-                i64 ne, const u64* __restrict__ bedge, const u32* __restrict__ tile_bptr,
-                const int32_t* __restrict__ bnd, double* __restrict__ navs,
-                double* __restrict__ svals) {
-  __shared__ double s_t[3][kTileNodeCap];
-  __shared__ uint16_t s_cd[kRingCodeCap];
-  const int t = threadIdx.x;
-  const int lane = t & 31;
-  const i64 e0 = static_cast<i64>(blockIdx.x) * kEB;
-  const i64 e1 = (e0 + kEB < ne) ? e0 + kEB : ne;
-  const i64 e = e0 + t;
-  const bool valid = e < ne;
-  const int NU = static_cast<int>(__ldg(tcnt + blockIdx.x));
-  const int C0 = __ldg(inc_ptr + e0) + 3 * static_cast<int>(e0);
-  const int NC = __ldg(inc_ptr + e1) + 3 * static_cast<int>(e1) - C0;
-  const bool codes_fit = NC <= kRingCodeCap;  // CTA-uniform
-  int pb = 0, pe = 0;
-  if (valid) {
-    pb = inc_ptr[e];
-    pe = inc_ptr[e + 1];
-  }
-  if (codes_fit)
-    for (int i = t; i < NC; i += kEB) s_cd[i] = __ldg(rcodes + C0 + i);
-  const int32_t* tn = tnodes + static_cast<i64>(blockIdx.x) * kTileNodeCap;
-  for (int i = t; i < NU; i += kEB) {
-    const d4 p = X[__ldg(tn + i)];
-    s_t[0][i] = p.x;
-    s_t[1][i] = p.y;
-    s_t[2][i] = p.z;
-  }
-  __syncthreads();
-  const uint16_t* cd = codes_fit ? s_cd - C0 : rcodes;
-  auto tab = [&](unsigned i) -> d4 {
-    d4 p;
-    p.x = s_t[0][i];
-    p.y = s_t[1][i];
-    p.z = s_t[2][i];
-    return p;
-  };
-  double acc[3] = {0.0, 0.0, 0.0};
-  d4 xj{}, xk{};
-  if (valid) {
-    const int base = pb + 3 * static_cast<int>(e);
-    xj = tab(cd[base] & 0x7fffu);
-    xk = tab(cd[base + 1]);
-    d4 mp = tab(cd[base + 2]);
-    double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
-    const int n = pe - pb;
-    for (int i = 0; i < n; ++i) {
-      const d4 m = tab(cd[base + 3 + i]);
-      const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
-      double c0, c1, c2;
-      cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
-      acc[0] += c0;
-      acc[1] += c1;
-      acc[2] += c2;
-      dx = ex;
-      dy = ey;
-      dz = ez;
-    }
-    if (cd[base] & 0x8000u) {
-      acc[0] = -acc[0];
-      acc[1] = -acc[1];
-      acc[2] = -acc[2];
-    }
-  }
-  double n[3] = {0.0, 0.0, 0.0};
-  double s = 0.0;
-  if (valid) {
-    edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, tile_bptr[blockIdx.x],
-                                   tile_bptr[blockIdx.x + 1], bnd, n, s);
-    svals[e] = s;
-  }
-  store_navs_warp<3>(n, e - lane, ne, navs);
-}
-
 // ------------------------------------------------------------------ GATHER (pipelined ring walk)
 // Persistent form of the ring walk: each CTA walks tiles blockIdx.x,
 // blockIdx.x + gridDim.x, ...  While tile i is evaluated, the coordinates
@@ -437,7 +349,7 @@ __global__ void __launch_bounds__(kEB, MINB)
 // an edge are summed unsigned and the edge's common orientation applied
 // once.  Tiles with more than kPipeCap nodes or kPipeCodeCap codes are
 // evaluated straight from global memory (same arithmetic, same order).
-constexpr int kPipeCodeCap = 3072;
+constexpr int kPipeCodeCap = 4096;
 extern __shared__ __align__(128) unsigned char dm_smem[];
 
 template <int CAP>
@@ -447,9 +359,12 @@ struct PipeSmem {
   // record allows, and z over 16 (fewer conflict wavefronts per read)
   double2 xy[2][CAP];
   double z[2][CAP];
-  uint32_t cd[2][kPipeCodeCap / 2 + 2];
+  uint32_t cd[2][kPipeCodeCap / 2 + 4];  // rows stay 16-byte aligned for cp.async.16
+  int4 wo[2];                            // u16 warp-block code offsets of the tile
   int32_t ip[2][kEB + 1];
 };
+static_assert(sizeof(double) * 2 * 512 % 16 == 0 && (kPipeCodeCap / 2 + 4) % 4 == 0,
+              "PipeSmem members must stay 16-byte aligned");
 
 __device__ __forceinline__ int meta_nu(const int4& m) { return m.z & 0xffff; }
 
@@ -457,7 +372,8 @@ template <int CAP>
 __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, const int4& m,
                                            const int (&ids)[CAP / kEB], Coords<3> X,
                                            const int32_t* __restrict__ inc_ptr,
-                                           const uint16_t* __restrict__ rcodes, i64 ne) {
+                                           const uint16_t* __restrict__ rcodes,
+                                           const int4* __restrict__ meta, i64 ne) {
   const int t = threadIdx.x;
   const int nu = meta_nu(m);
   if (nu <= CAP) {
@@ -472,10 +388,11 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
     }
   }
   if (m.y <= kPipeCodeCap) {
-    const int w0 = m.x >> 1, w1 = (m.x + m.y + 1) >> 1;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(rcodes);
-    for (int w = w0 + t; w < w1; w += kEB) cp_async4(&S.cd[b][w - w0], src + w);
+    // code blocks are warp-aligned (multiples of 32 codes): 16-byte pieces
+    const uint4* src = reinterpret_cast<const uint4*>(rcodes + m.x);
+    for (int w = t; w < m.y / 8; w += kEB) cp_async16(&S.cd[b][4 * w], src + w);
   }
+  if (t == 0) cp_async16(&S.wo[b], meta + 2 * tile + 1);
   const i64 e0 = static_cast<i64>(tile) * kEB;
   const i64 cnt = (e0 + kEB < ne ? kEB : ne - e0) + 1;
   for (int i = t; i < cnt; i += kEB) cp_async4(&S.ip[b][i], inc_ptr + e0 + i);
@@ -493,22 +410,21 @@ __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __
   }
 }
 
-// Walks one edge's ring; T(slot) returns the node record of a tile slot.
+// Walks one edge's ring; T(slot) returns the node record of a tile slot;
+// cd points at this lane's step-0 code, step s at cd[s * 32].
 template <int RU = 1, typename TabFn>
-__device__ __forceinline__ void ring_walk(const TabFn& T, const uint16_t* __restrict__ cd,
-                                          int base, int n, double* acc, d4& xj, d4& xk) {
-  const unsigned w0 = cd[base];
+__device__ __forceinline__ void ring_walk(const TabFn& T, const uint16_t* __restrict__ cd, int n,
+                                          double* acc, d4& xj, d4& xk) {
+  const unsigned w0 = cd[0];
   xj = T(w0 & 0x7fffu);
-  xk = T(cd[base + 1]);
-  const d4 mp = T(cd[base + 2]);
+  xk = T(cd[32]);
+  const d4 mp = T(cd[64]);
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  // RU ring steps per batch: all codes, then all table reads, then the
-  // sequential fold -- independent loads overlap instead of chaining.
   for (int i0 = 0; i0 < n; i0 += RU) {
     unsigned w[RU];
 #pragma unroll
-    for (int u = 0; u < RU; ++u) w[u] = i0 + u < n ? cd[base + 3 + i0 + u] : 0u;
+    for (int u = 0; u < RU; ++u) w[u] = i0 + u < n ? cd[(3 + i0 + u) * 32] : 0u;
     d4 m[RU];
 #pragma unroll
     for (int u = 0; u < RU; ++u) m[u] = T(w[u]);
@@ -548,20 +464,20 @@ __global__ void __launch_bounds__(kEB, MINB)
   const int G = gridDim.x;
   // prologue: tile 0 -> buffer 0; ids / metadata of tile 1 into registers
   int ids[CAP / kEB];
-  int4 m_cur = __ldg(meta + tile);
+  int4 m_cur = __ldg(meta + 2 * tile);
   pipe_ids(tile, ntiles, tnodes, ids);
-  pipe_issue(S, 0, tile, m_cur, ids, X, inc_ptr, rcodes, ne);
+  pipe_issue(S, 0, tile, m_cur, ids, X, inc_ptr, rcodes, meta, ne);
   cp_async_commit();
-  int4 m_nxt = tile + G < ntiles ? __ldg(meta + tile + G) : make_int4(0, 0, 0, 0);
+  int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
   pipe_ids(tile + G, ntiles, tnodes, ids);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int b = it & 1;
     const int nxt = tile + G;
-    if (nxt < ntiles) pipe_issue(S, b ^ 1, nxt, m_nxt, ids, X, inc_ptr, rcodes, ne);
+    if (nxt < ntiles) pipe_issue(S, b ^ 1, nxt, m_nxt, ids, X, inc_ptr, rcodes, meta, ne);
     cp_async_commit();
     const int4 m = m_cur;
     m_cur = m_nxt;
-    m_nxt = nxt + G < ntiles ? __ldg(meta + nxt + G) : make_int4(0, 0, 0, 0);
+    m_nxt = nxt + G < ntiles ? __ldg(meta + 2 * (nxt + G)) : make_int4(0, 0, 0, 0);
     pipe_ids(nxt + G, ntiles, tnodes, ids);
     cp_async_wait<1>();
     __syncthreads();
@@ -571,8 +487,10 @@ __global__ void __launch_bounds__(kEB, MINB)
     double acc[3] = {0.0, 0.0, 0.0};
     d4 xj{}, xk{};
     if (valid) {
-      const int pb = S.ip[b][t], n = S.ip[b][t + 1] - pb;
-      const int base = pb + 3 * static_cast<int>(e);
+      const int n = S.ip[b][t + 1] - S.ip[b][t];
+      const int warp = t >> 5;
+      const unsigned wo = (reinterpret_cast<const unsigned*>(&S.wo[b])[warp >> 1] >>
+                           (16 * (warp & 1))) & 0xffffu;
       const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
       if (meta_nu(m) <= CAP && m.y <= kPipeCodeCap) {
         const double2* xy = S.xy[b];
@@ -585,11 +503,10 @@ __global__ void __launch_bounds__(kEB, MINB)
           p.z = zz[i];
           return p;
         };
-        ring_walk<RU>(T, reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n,
-                      acc, xj, xk);
+        ring_walk<RU>(T, reinterpret_cast<const uint16_t*>(S.cd[b]) + wo + lane, n, acc, xj, xk);
       } else {
         auto T = [&](unsigned i) -> d4 { return X[__ldg(tn + i)]; };
-        ring_walk(T, rcodes, base, n, acc, xj, xk);
+        ring_walk(T, rcodes + m.x + wo + lane, n, acc, xj, xk);
       }
     }
     double nv[3] = {0.0, 0.0, 0.0};
@@ -602,133 +519,6 @@ __global__ void __launch_bounds__(kEB, MINB)
     }
     store_navs_warp<3>(nv, e - lane, ne, navs);
     __syncthreads();  // buffer b is refilled two iterations from now
-  }
-  cp_async_wait<0>();
-}
-
-// ------------------------------------------------------------------ GATHER (ring walk, TMA)
-// The default 3D dual-free kernel.  Same pipeline as k_navs_ring_pipe, but
-// the coordinate table of the next tile is fetched by the TMA engine with
-// tile::gather4 (4 node records of 32 bytes per instruction, completion on
-// a per-buffer mbarrier) instead of per-lane cp.async: the gather costs no
-// LSU / L1 wavefronts and no shared-memory write conflicts.
-template <int CAP>
-struct TmaSmem {
-  d4 tab[2][CAP];  // 128-byte aligned: each gather4 lands 4 records = 128 B
-  uint32_t cd[2][kPipeCodeCap / 2 + 2];
-  int32_t ip[2][kEB + 1];
-  unsigned long long mbar[2];
-};
-
-template <int CAP>
-__device__ __forceinline__ void tma_issue(TmaSmem<CAP>& S, int b, int tile, const int4& m,
-                                          const int (&ids)[CAP / kEB], const CUtensorMap* map,
-                                          const int32_t* __restrict__ inc_ptr,
-                                          const uint16_t* __restrict__ rcodes, i64 ne) {
-  const int t = threadIdx.x;
-  const int nu = meta_nu(m);
-  if (nu <= CAP) {
-    const int groups = (nu + 3) >> 2;
-    if (t == 0) mbar_expect_tx(&S.mbar[b], static_cast<unsigned>(groups) * 128u);
-#pragma unroll
-    for (int u = 0; u < CAP / kEB; ++u) {
-      // lanes 4g..4g+3 hold nodes 4g..4g+3 of this stripe; lane 4g issues
-      const int i = t + u * kEB;
-      const int id = i < nu ? ids[u] : 0;
-      const int r1 = __shfl_down_sync(0xffffffffu, id, 1);
-      const int r2 = __shfl_down_sync(0xffffffffu, id, 2);
-      const int r3 = __shfl_down_sync(0xffffffffu, id, 3);
-      if ((t & 3) == 0 && i < nu) tma_gather4(&S.tab[b][i], map, &S.mbar[b], id, r1, r2, r3);
-    }
-  }
-  if (m.y <= kPipeCodeCap) {
-    const int w0 = m.x >> 1, w1 = (m.x + m.y + 1) >> 1;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(rcodes);
-    for (int w = w0 + t; w < w1; w += kEB) cp_async4(&S.cd[b][w - w0], src + w);
-  }
-  const i64 e0 = static_cast<i64>(tile) * kEB;
-  const i64 cnt = (e0 + kEB < ne ? kEB : ne - e0) + 1;
-  for (int i = t; i < cnt; i += kEB) cp_async4(&S.ip[b][i], inc_ptr + e0 + i);
-}
-
-template <int CAP, int MINB>
-__global__ void __launch_bounds__(kEB, MINB)
-    k_navs_ring_tma(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ inc_ptr,
-                    const uint16_t* __restrict__ rcodes, const int32_t* __restrict__ tnodes,
-                    const int4* __restrict__ meta, Coords<3> X, i64 ne, int ntiles,
-                    const u64* __restrict__ bedge, const int32_t* __restrict__ bnd,
-                    double* __restrict__ navs, double* __restrict__ svals) {
-  TmaSmem<CAP>& S = *reinterpret_cast<TmaSmem<CAP>*>(dm_smem);
-  const int t = threadIdx.x;
-  const int lane = t & 31;
-  int tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  const int G = gridDim.x;
-  if (t == 0) {
-    mbar_init(&S.mbar[0], 1);
-    mbar_init(&S.mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  unsigned phases = 0u;  // bit b = parity of buffer b's mbarrier
-  int ids[CAP / kEB];
-  int4 m_cur = __ldg(meta + tile);
-  pipe_ids(tile, ntiles, tnodes, ids);
-  tma_issue(S, 0, tile, m_cur, ids, &xmap, inc_ptr, rcodes, ne);
-  cp_async_commit();
-  int4 m_nxt = tile + G < ntiles ? __ldg(meta + tile + G) : make_int4(0, 0, 0, 0);
-  pipe_ids(tile + G, ntiles, tnodes, ids);
-  for (int it = 0; tile < ntiles; ++it, tile += G) {
-    const int b = it & 1;
-    const int nxt = tile + G;
-    if (nxt < ntiles) tma_issue(S, b ^ 1, nxt, m_nxt, ids, &xmap, inc_ptr, rcodes, ne);
-    cp_async_commit();
-    const int4 m = m_cur;
-    m_cur = m_nxt;
-    m_nxt = nxt + G < ntiles ? __ldg(meta + nxt + G) : make_int4(0, 0, 0, 0);
-    pipe_ids(nxt + G, ntiles, tnodes, ids);
-    cp_async_wait<1>();
-    const bool tab_fast = meta_nu(m) <= CAP;
-    if (tab_fast) {
-      mbar_wait(&S.mbar[b], (phases >> b) & 1u);
-      phases ^= 1u << b;
-    }
-    __syncthreads();
-    const i64 e = static_cast<i64>(tile) * kEB + t;
-    const bool valid = e < ne;
-    double acc[3] = {0.0, 0.0, 0.0};
-    d4 xj{}, xk{};
-    if (valid) {
-      const int pb = S.ip[b][t], n = S.ip[b][t + 1] - pb;
-      const int base = pb + 3 * static_cast<int>(e);
-      const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
-      if (tab_fast && m.y <= kPipeCodeCap) {
-        const d4* tb = S.tab[b];
-        auto T = [&](unsigned i) -> d4 {
-          const double2 v = *reinterpret_cast<const double2*>(&tb[i]);
-          d4 p;
-          p.x = v.x;
-          p.y = v.y;
-          p.z = tb[i].z;
-          return p;
-        };
-        ring_walk(T, reinterpret_cast<const uint16_t*>(S.cd[b]) - 2 * (m.x >> 1), base, n, acc,
-                  xj, xk);
-      } else {
-        auto T = [&](unsigned i) -> d4 { return X[__ldg(tn + i)]; };
-        ring_walk(T, rcodes, base, n, acc, xj, xk);
-      }
-    }
-    double nv[3] = {0.0, 0.0, 0.0};
-    double s = 0.0;
-    if (valid) {
-      const u32 rb = static_cast<u32>(m.w);
-      edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, rb,
-                                     rb + (static_cast<u32>(m.z) >> 16), bnd, nv, s);
-      svals[e] = s;
-    }
-    store_navs_warp<3>(nv, e - lane, ne, navs);
-    __syncthreads();  // buffer b is refilled next iteration
   }
   cp_async_wait<0>();
 }
@@ -946,51 +736,27 @@ int launch_navs(dm_ctx* c, int variant) {
   } else if (variant == DM_VARIANT_GATHER && D == 3 && ALGO == kDualFree && c->ring_ok) {
     tmark(c, 0);
     if constexpr (D == 3) {
-      if (c->gather_cfg == 5) {
-        DM_LAUNCH(c, k_navs_ring<3>, tiles, kEB, 0, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
-                  c->tnode_cnt.p, X, ne, c->bedge.p, c->tile_bptr.p, c->bnd.p, c->navs.p,
-                  c->svals.p);
-      } else {
-        auto launch = [&](auto kern, int smem) -> int {
-          DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-          int per_sm = 0, nsm = 0;
-          DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
-          DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-          const unsigned grid = static_cast<unsigned>(std::min<i64>(
-              static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
-          DM_LAUNCH(c, kern, grid, kEB, smem, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
-                    c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->bnd.p,
-                    c->navs.p, c->svals.p);
-          return DM_OK;
-        };
-        auto launch_tma = [&](auto kern, int smem) -> int {
-          DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-          int per_sm = 0, nsm = 0;
-          DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
-          DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
-          const unsigned grid = static_cast<unsigned>(std::min<i64>(
-              static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
-          DM_LAUNCH(c, kern, grid, kEB, smem, c->x4_map, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
-                    c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->bnd.p,
-                    c->navs.p, c->svals.p);
-          return DM_OK;
-        };
-        int st = DM_OK;
-        // default: cp.async pipeline (TMA gather4 variants measured slower: cfg 0-2)
-        const int cfg = c->gather_cfg == 0 || !c->x4_map_ok ? 6 : c->gather_cfg;
-        switch (cfg) {
-          case 1: st = launch_tma(k_navs_ring_tma<1024, 2>, sizeof(TmaSmem<1024>)); break;
-          case 2: st = launch_tma(k_navs_ring_tma<512, 4>, sizeof(TmaSmem<512>)); break;
-          case 6: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
-          case 7: st = launch(k_navs_ring_pipe<768, 3, 2>, sizeof(PipeSmem<768>)); break;
-          case 8: st = launch(k_navs_ring_pipe<640, 4>, sizeof(PipeSmem<640>)); break;
-          case 9: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
-          case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
-          case 3: st = launch_tma(k_navs_ring_tma<768, 3>, sizeof(TmaSmem<768>)); break;
-          default: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
-        }
-        if (st) return st;
+      auto launch = [&](auto kern, int smem) -> int {
+        DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0, nsm = 0;
+        DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEB, smem));
+        DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+        const unsigned grid = static_cast<unsigned>(std::min<i64>(
+            static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
+        DM_LAUNCH(c, kern, grid, kEB, smem, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
+                  c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->bnd.p,
+                  c->navs.p, c->svals.p);
+        return DM_OK;
+      };
+      int st = DM_OK;
+      switch (c->gather_cfg) {
+        case 7: st = launch(k_navs_ring_pipe<768, 3, 2>, sizeof(PipeSmem<768>)); break;
+        case 8: st = launch(k_navs_ring_pipe<640, 4>, sizeof(PipeSmem<640>)); break;
+        case 9: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
+        case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
+        default: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
       }
+      if (st) return st;
     }
     tmark(c, 1);
     tmark(c, 2);

@@ -12,9 +12,13 @@
 //   tile nodes : per 256-edge tile, the sorted unique ids of every node the
 //                tile touches (j, k, ring nodes), at a fixed stride of
 //                kTileNodeCap, count in tnode_cnt[tile].
-//   ring codes : per edge, n+3 16-bit words at offset inc_ptr[e] + 3e:
+//   ring codes : per edge, n+3 16-bit words
 //                  [slot(j) | s<<15, slot(k), slot(m_0), slot(m_1), ...,
 //                   slot(m_n)]                  (slots into the tile list)
+//                stored lane-transposed per warp of 32 consecutive edges: the
+//                warp block holds S_w = max(n+3) steps x 32 lanes, entry
+//                (step, lane) at wstart[w] + step*32 + lane, so the 32 lanes
+//                of a ring step read 64 contiguous bytes (one wavefront).
 //                where s is the common orientation of all terms of the edge:
 //                around a consistently oriented ring every term has the same
 //                parity, so the sign is applied once to the sum
@@ -136,7 +140,8 @@ __device__ __forceinline__ int perm_sign(int a0, int a1, int a2, int b0, int b1,
 __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
                              const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
                              const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt,
-                             i64 ne, uint16_t* __restrict__ rcodes, int* __restrict__ flag) {
+                             const u32* __restrict__ wstart, i64 ne,
+                             uint16_t* __restrict__ rcodes, int* __restrict__ flag) {
   const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= ne) return;
   const i64 tile = e / kTileEdges;
@@ -174,10 +179,10 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
       if (cnt == 1 && (start < 0 || v < start)) start = v;
     }
   if (start < 0) start = a[0];
-  uint16_t* out = rcodes + pb + 3 * e;
+  // step s of this edge lives at out[s * 32]
+  uint16_t* out = rcodes + wstart[e >> 5] + (e & 31);
   int sg0 = 0;
-  out[1] = static_cast<uint16_t>(tslot(list, nl, k));
-  out[2] = static_cast<uint16_t>(tslot(list, nl, start));
+  out[2 * 32] = static_cast<uint16_t>(tslot(list, nl, start));
   unsigned used = 0;
   int cur = start;
   for (int step = 0; step < n; ++step) {
@@ -199,23 +204,44 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
       atomicOr(flag, 16);  // inconsistently oriented fan
       return;
     }
-    out[3 + step] = static_cast<uint16_t>(tslot(list, nl, nxt));
+    out[(3 + step) * 32] = static_cast<uint16_t>(tslot(list, nl, nxt));
     cur = nxt;
   }
   out[0] = static_cast<uint16_t>(tslot(list, nl, j) | (sg0 < 0 ? 0x8000u : 0u));
+  out[32] = static_cast<uint16_t>(tslot(list, nl, k));
 }
 
-__global__ void k_ring_meta(const int32_t* __restrict__ inc_ptr, const u32* __restrict__ tcnt,
-                            const u32* __restrict__ tile_bptr, i64 ne, i64 ntiles,
+// Codes per warp block: S_w * 32 with S_w = max over the warp's edges of n+3.
+__global__ void k_ring_warpsize(const int32_t* __restrict__ inc_ptr, i64 ne, i64 nwarps,
+                                u32* __restrict__ wsize) {
+  const i64 w = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= nwarps) return;
+  int S = 3;
+  for (i64 e = w * 32; e < w * 32 + 32 && e < ne; ++e) S = max(S, inc_ptr[e + 1] - inc_ptr[e] + 3);
+  wsize[w] = static_cast<u32>(S * 32);
+}
+
+// meta[2t]   = {C0, NC, NU | nbnd << 16, bptr}
+// meta[2t+1] = eight u16 warp-block offsets relative to C0
+__global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restrict__ tcnt,
+                            const u32* __restrict__ tile_bptr, i64 nwarps, i64 ntiles,
                             int4* __restrict__ meta) {
   const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
-  const i64 e0 = t * kTileEdges, e1 = (e0 + kTileEdges < ne) ? e0 + kTileEdges : ne;
-  const int C0 = inc_ptr[e0] + 3 * static_cast<int>(e0);
-  const int C1 = inc_ptr[e1] + 3 * static_cast<int>(e1);
+  const i64 w0 = t * (kTileEdges / 32);
+  const i64 w1 = (w0 + kTileEdges / 32 < nwarps) ? w0 + kTileEdges / 32 : nwarps;
+  const u32 C0 = wstart[w0], C1 = wstart[w1];
   const int nb = static_cast<int>(tile_bptr[t + 1] - tile_bptr[t]);  // <= 3 * 256
-  meta[t] = make_int4(C0, C1 - C0, static_cast<int>(tcnt[t]) | nb << 16,
-                      static_cast<int>(tile_bptr[t]));
+  meta[2 * t] = make_int4(static_cast<int>(C0), static_cast<int>(C1 - C0),
+                          static_cast<int>(tcnt[t]) | nb << 16, static_cast<int>(tile_bptr[t]));
+  unsigned o[4] = {0u, 0u, 0u, 0u};
+  for (i64 w = w0; w < w1; ++w) {
+    const u32 off = min(wstart[w] - C0, 0xffffu);
+    const int q = static_cast<int>(w - w0);
+    o[q >> 1] |= off << (16 * (q & 1));
+  }
+  meta[2 * t + 1] = make_int4(static_cast<int>(o[0]), static_cast<int>(o[1]),
+                              static_cast<int>(o[2]), static_cast<int>(o[3]));
 }
 
 }  // namespace
@@ -231,19 +257,33 @@ int ensure_rings(dm_ctx* c) {
   }
   const i64 ne = c->ne;
   const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
-  const i64 M = 6 * c->nE;
+  const i64 nwarps = (ne + 31) / 32;
   DM_CK(c, c->tnodes.ensure(static_cast<size_t>(ntiles * kTileNodeCap)));
   DM_CK(c, c->tnode_cnt.ensure(static_cast<size_t>(ntiles)));
-  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(M + 3 * ne + 4)));
-  DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(ntiles)));
+  // tiles that overflow the caps keep count 0 (their codes are never used:
+  // the overflow sets ring_ok = false)
+  DM_CK(c, cudaMemsetAsync(c->tnode_cnt.p, 0, ntiles * sizeof(u32), c->stream));
+  DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(2 * ntiles)));
+  DevBuf<u32> wstart;
+  DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
+  DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->inc_ptr.p, ne, nwarps, wstart.p);
+  int st = scan_exclusive(c, wstart.p, wstart.p, nwarps);
+  if (st) return st;
+  u32 ncodes = 0;
+  DM_CK(c, cudaMemcpyAsync(&ncodes, wstart.p + nwarps, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(ncodes) + 8));
+  DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, (static_cast<size_t>(ncodes) + 8) * sizeof(uint16_t),
+                           c->stream));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
   DM_LAUNCH(c, k_tile_nodes, static_cast<unsigned>(ntiles), kTileEdges, 0, c->edges.p,
             c->inc_ptr.p, c->inc.p, c->elems.p, ne, c->tnodes.p, c->tnode_cnt.p, c->flag.p);
   DM_LAUNCH(c, k_ring_codes, grid_for(ne, 128), 128, 0, c->edges.p, c->inc_ptr.p, c->inc.p,
-            c->elems.p, c->tnodes.p, c->tnode_cnt.p, ne, c->rcodes.p, c->flag.p);
-  DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, c->inc_ptr.p, c->tnode_cnt.p,
-            c->tile_bptr.p, ne, ntiles, c->ring_meta.p);
+            c->elems.p, c->tnodes.p, c->tnode_cnt.p, wstart.p, ne, c->rcodes.p, c->flag.p);
+  DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
+            c->tile_bptr.p, nwarps, ntiles, c->ring_meta.p);
   int fl[2] = {0, 0};
   DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
