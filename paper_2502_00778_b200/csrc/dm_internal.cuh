@@ -65,8 +65,6 @@ struct dm_ctx {
   dm::i64 nv = 0, nE = 0, nB = 0;
   dm::DevBuf<double> coords;  // caller layout, dim doubles per node
   dm::DevBuf<dm::d4> x4;      // 3D padded copy
-  CUtensorMap x4_map;         // TMA view of x4: [nv rows x 4 doubles]
-  bool x4_map_ok = false;
   dm::DevBuf<int32_t> elems, bnd;
 
   // edge structures (K1)
@@ -93,8 +91,14 @@ struct dm_ctx {
   dm::i64 ring_max_nodes = 0, ring_fail = 0;
   dm::DevBuf<int32_t> tnodes;      // kTileNodeCap per tile (rings.cu)
   dm::DevBuf<dm::u32> tnode_cnt;
-  dm::DevBuf<uint16_t> rcodes;     // n+3 per edge at inc_ptr[e] + 3e
-  dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU | nbnd << 16, bptr}
+  dm::DevBuf<uint16_t> rcodes;     // lane-transposed warp blocks (rings.cu)
+  dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU | nbnd << 16, bptr}, offsets
+  dm::DevBuf<int32_t> eperm;       // tile position p -> edge id (Morton origin order)
+  dm::DevBuf<int32_t> morder;      // Morton rank -> node id
+  dm::DevBuf<double2> mxy;         // coordinates in Morton rank order: (x, y)
+  dm::DevBuf<double> mz;           //                                    z
+  dm::DevBuf<dm::u64> bedge_p;     // (p << 32 | facet), sorted
+  dm::DevBuf<dm::u32> tile_bptr_p; // bedge_p slice per tile
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
   dm::DevBuf<int32_t> n2e;
@@ -289,6 +293,8 @@ int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg);
 // (key, value) pairs sorted lexicographically within each segment.
 int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg);
 
+__global__ void k_tile_bptr(const u64* bedge, u32 n, i64 ne, i64 ntiles, u32* tile_bptr);
+
 // Derived structures, built lazily.
 int ensure_incoming(dm_ctx* c);
 int ensure_bedge(dm_ctx* c);
@@ -299,6 +305,7 @@ int build_edges_impl(dm_ctx* c);
 int navs_impl(dm_ctx* c, int algo, int variant);
 int volumes_impl(dm_ctx* c, int algo);
 int pad_coords(dm_ctx* c);
+int refresh_ring_coords(dm_ctx* c);
 int compute_element_volumes(dm_ctx* c);
 int svals_from_navs(dm_ctx* c);
 

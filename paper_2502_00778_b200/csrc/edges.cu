@@ -281,6 +281,16 @@ __global__ void k_bedge_scatter(const int32_t* bnd, i64 nB, const int2* edges, c
   out[start[j] + atomicAdd(fill + j, 1u)] = (static_cast<u64>(id) << 32) | static_cast<u64>(b);
 }
 
+__global__ void k_edge_of(const int2* edges, const u32* os, i64 nv, const int32_t* a,
+                          const int32_t* b, i64 n, int32_t* out) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = dev_edge_of(edges, os, nv, a[i], b[i]);
+}
+
+}  // namespace
+
+// tile_bptr[t] = first entry of the sorted (key << 32 | facet) list whose key
+// is >= t * kTileEdges (t = 0..ntiles).
 __global__ void k_tile_bptr(const u64* bedge, u32 n, i64 ne, i64 ntiles, u32* tile_bptr) {
   const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t > ntiles) return;
@@ -294,13 +304,6 @@ __global__ void k_tile_bptr(const u64* bedge, u32 n, i64 ne, i64 ntiles, u32* ti
   tile_bptr[t] = lo;
 }
 
-__global__ void k_edge_of(const int2* edges, const u32* os, i64 nv, const int32_t* a,
-                          const int32_t* b, i64 n, int32_t* out) {
-  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = dev_edge_of(edges, os, nv, a[i], b[i]);
-}
-
-}  // namespace
 
 int ensure_incoming(dm_ctx* c) {
   if (c->have_in) return DM_OK;

@@ -192,6 +192,20 @@ __device__ __forceinline__ void store_navs_warp(const double* n, i64 wbase, i64 
   }
 }
 
+// Per-lane store of one 3D navs row (24 bytes at 24e): one 16-byte and one
+// 8-byte store, ordered by the row's 16-byte alignment (e even: xy | z,
+// e odd: x | yz).
+__device__ __forceinline__ void store_nav_row(double* __restrict__ navs, i64 e, const double* n) {
+  double* r = navs + 3 * e;
+  if ((e & 1) == 0) {
+    *reinterpret_cast<double2*>(r) = make_double2(n[0], n[1]);
+    r[2] = n[2];
+  } else {
+    r[0] = n[0];
+    *reinterpret_cast<double2*>(r + 1) = make_double2(n[1], n[2]);
+  }
+}
+
 // ------------------------------------------------------------------ GATHER (row table)
 // One CTA per 256-edge tile, one thread per edge.  The tile's edges belong
 // to consecutive origin rows [j0, jl]; per-tile metadata (tables.cu) gives
@@ -339,15 +353,17 @@ __global__ void __launch_bounds__(kEB, MINB)
 }
 
 // ------------------------------------------------------------------ GATHER (pipelined ring walk)
-// Persistent form of the ring walk: each CTA walks tiles blockIdx.x,
-// blockIdx.x + gridDim.x, ...  While tile i is evaluated, the coordinates
-// (2 x 16-byte cp.async per node into a 32-byte AoS table), ring codes and
-// inc_ptr slice of tile i+1 stream into the other half of a double buffer
-// with cp.async (LDGSTS, no register round trip), and the node ids and
-// metadata of tile i+2 are prefetched into registers -- so the per-tile
-// gather latency hides behind the previous tile's arithmetic.  The terms of
-// an edge are summed unsigned and the edge's common orientation applied
-// once.  Tiles with more than kPipeCap nodes or kPipeCodeCap codes are
+// The default 3D dual-free kernel.  Persistent CTAs walk the 256-edge tiles
+// of the Morton edge order (rings.cu) blockIdx.x, blockIdx.x + gridDim.x,
+// ...; one thread per edge walks the ring of its incident elements through a
+// shared-memory table of the tile's nodes (one table read per incidence).
+// While tile i is evaluated, the node table (16-byte xy + 8-byte z cp.async
+// per node) and ring codes of tile i+1 stream into the other half of a
+// double buffer with cp.async (LDGSTS, no register round trip), and the node
+// ids, edge ids and metadata of tile i+2 are prefetched into registers -- so
+// the per-tile gather latency hides behind the previous tile's arithmetic.
+// The terms of an edge are summed unsigned and the edge's common orientation
+// applied once.  Tiles with more than CAP nodes or kPipeCodeCap codes are
 // evaluated straight from global memory (same arithmetic, same order).
 constexpr int kPipeCodeCap = 4096;
 extern __shared__ __align__(128) unsigned char dm_smem[];
@@ -361,7 +377,6 @@ struct PipeSmem {
   double z[2][CAP];
   uint32_t cd[2][kPipeCodeCap / 2 + 4];  // rows stay 16-byte aligned for cp.async.16
   int4 wo[2];                            // u16 warp-block code offsets of the tile
-  int32_t ip[2][kEB + 1];
 };
 static_assert(sizeof(double) * 2 * 512 % 16 == 0 && (kPipeCodeCap / 2 + 4) % 4 == 0,
               "PipeSmem members must stay 16-byte aligned");
@@ -370,10 +385,11 @@ __device__ __forceinline__ int meta_nu(const int4& m) { return m.z & 0xffff; }
 
 template <int CAP>
 __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, const int4& m,
-                                           const int (&ids)[CAP / kEB], Coords<3> X,
-                                           const int32_t* __restrict__ inc_ptr,
+                                           const int (&ids)[CAP / kEB],
+                                           const double2* __restrict__ mxy,
+                                           const double* __restrict__ mz,
                                            const uint16_t* __restrict__ rcodes,
-                                           const int4* __restrict__ meta, i64 ne) {
+                                           const int4* __restrict__ meta) {
   const int t = threadIdx.x;
   const int nu = meta_nu(m);
   if (nu <= CAP) {
@@ -381,9 +397,8 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
     for (int u = 0; u < CAP / kEB; ++u) {
       const int i = t + u * kEB;
       if (i < nu) {
-        const double* src = reinterpret_cast<const double*>(X.p + ids[u]);
-        cp_async16(&S.xy[b][i], src);
-        cp_async8(&S.z[b][i], src + 2);
+        cp_async16(&S.xy[b][i], mxy + ids[u]);
+        cp_async8(&S.z[b][i], mz + ids[u]);
       }
     }
   }
@@ -393,32 +408,38 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
     for (int w = t; w < m.y / 8; w += kEB) cp_async16(&S.cd[b][4 * w], src + w);
   }
   if (t == 0) cp_async16(&S.wo[b], meta + 2 * tile + 1);
-  const i64 e0 = static_cast<i64>(tile) * kEB;
-  const i64 cnt = (e0 + kEB < ne ? kEB : ne - e0) + 1;
-  for (int i = t; i < cnt; i += kEB) cp_async4(&S.ip[b][i], inc_ptr + e0 + i);
 }
 
-// ids of `tile` into registers (always the full kPipeCap window: the tile
-// list has a fixed stride, so no dependency on the tile's metadata).
+// node ids and this thread's edge id of `tile` into registers (always the
+// full CAP window: the tile list has a fixed stride, so no dependency on the
+// tile's metadata).
 template <int NI>
 __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __restrict__ tnodes,
-                                         int (&ids)[NI]) {
+                                         const int32_t* __restrict__ eperm, i64 ne,
+                                         int (&ids)[NI], int& eid) {
   if (tile < ntiles) {
     const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
 #pragma unroll
     for (int u = 0; u < NI; ++u) ids[u] = __ldg(tn + threadIdx.x + u * kEB);
+    const i64 p = static_cast<i64>(tile) * kEB + threadIdx.x;
+    eid = p < ne ? __ldg(eperm + p) : 0;
   }
 }
 
 // Walks one edge's ring; T(slot) returns the node record of a tile slot;
-// cd points at this lane's step-0 code, step s at cd[s * 32].
+// cd points at this lane's step-0 code, step s at cd[s * 32] (rings.cu
+// layout: word 0 = slot(j) | sign << 15, word 1 = slot(k) | n << 11,
+// word 2 = slot(m_0) | boundary << 15).  Returns the boundary bit.
 template <int RU = 1, typename TabFn>
-__device__ __forceinline__ void ring_walk(const TabFn& T, const uint16_t* __restrict__ cd, int n,
+__device__ __forceinline__ bool ring_walk(const TabFn& T, const uint16_t* __restrict__ cd,
                                           double* acc, d4& xj, d4& xk) {
   const unsigned w0 = cd[0];
-  xj = T(w0 & 0x7fffu);
-  xk = T(cd[32]);
-  const d4 mp = T(cd[64]);
+  const unsigned w1 = cd[32];
+  const unsigned w2 = cd[64];
+  const int n = static_cast<int>(w1 >> 11);
+  xj = T(w0 & 0x7ffu);
+  xk = T(w1 & 0x7ffu);
+  const d4 mp = T(w2 & 0x7ffu);
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int i0 = 0; i0 < n; i0 += RU) {
@@ -447,13 +468,15 @@ __device__ __forceinline__ void ring_walk(const TabFn& T, const uint16_t* __rest
   acc[0] = neg ? -a0 : a0;
   acc[1] = neg ? -a1 : a1;
   acc[2] = neg ? -a2 : a2;
+  return (w2 & 0x8000u) != 0;
 }
 
 template <int CAP, int MINB, int RU = 1>
 __global__ void __launch_bounds__(kEB, MINB)
-    k_navs_ring_pipe(const int32_t* __restrict__ inc_ptr, const uint16_t* __restrict__ rcodes,
+    k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint16_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
-                     Coords<3> X, i64 ne, int ntiles, const u64* __restrict__ bedge,
+                     const double2* __restrict__ mxy, const double* __restrict__ mz,
+                     Coords<3> X, i64 ne, int ntiles, const u64* __restrict__ bedge_p,
                      const int32_t* __restrict__ bnd, double* __restrict__ navs,
                      double* __restrict__ svals) {
   PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(dm_smem);
@@ -464,30 +487,34 @@ __global__ void __launch_bounds__(kEB, MINB)
   const int G = gridDim.x;
   // prologue: tile 0 -> buffer 0; ids / metadata of tile 1 into registers
   int ids[CAP / kEB];
+  int e_nxt = 0;
   int4 m_cur = __ldg(meta + 2 * tile);
-  pipe_ids(tile, ntiles, tnodes, ids);
-  pipe_issue(S, 0, tile, m_cur, ids, X, inc_ptr, rcodes, meta, ne);
+  pipe_ids(tile, ntiles, tnodes, eperm, ne, ids, e_nxt);
+  int e_cur = e_nxt;
+  pipe_issue(S, 0, tile, m_cur, ids, mxy, mz, rcodes, meta);
   cp_async_commit();
   int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
-  pipe_ids(tile + G, ntiles, tnodes, ids);
+  pipe_ids(tile + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int b = it & 1;
     const int nxt = tile + G;
-    if (nxt < ntiles) pipe_issue(S, b ^ 1, nxt, m_nxt, ids, X, inc_ptr, rcodes, meta, ne);
+    if (nxt < ntiles) pipe_issue(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
     cp_async_commit();
     const int4 m = m_cur;
+    const int e = e_cur;
     m_cur = m_nxt;
+    e_cur = e_nxt;
     m_nxt = nxt + G < ntiles ? __ldg(meta + 2 * (nxt + G)) : make_int4(0, 0, 0, 0);
-    pipe_ids(nxt + G, ntiles, tnodes, ids);
+    pipe_ids(nxt + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
     cp_async_wait<1>();
     __syncthreads();
     // ---- evaluate tile `tile` from buffer b
-    const i64 e = static_cast<i64>(tile) * kEB + t;
-    const bool valid = e < ne;
+    const i64 p = static_cast<i64>(tile) * kEB + t;
+    const bool valid = p < ne;
     double acc[3] = {0.0, 0.0, 0.0};
     d4 xj{}, xk{};
+    bool bflag = false;
     if (valid) {
-      const int n = S.ip[b][t + 1] - S.ip[b][t];
       const int warp = t >> 5;
       const unsigned wo = (reinterpret_cast<const unsigned*>(&S.wo[b])[warp >> 1] >>
                            (16 * (warp & 1))) & 0xffffu;
@@ -497,28 +524,38 @@ __global__ void __launch_bounds__(kEB, MINB)
         const double* zz = S.z[b];
         auto T = [&](unsigned i) -> d4 {
           const double2 v = xy[i];
-          d4 p;
-          p.x = v.x;
-          p.y = v.y;
-          p.z = zz[i];
-          return p;
+          d4 r;
+          r.x = v.x;
+          r.y = v.y;
+          r.z = zz[i];
+          return r;
         };
-        ring_walk<RU>(T, reinterpret_cast<const uint16_t*>(S.cd[b]) + wo + lane, n, acc, xj, xk);
+        bflag = ring_walk<RU>(T, reinterpret_cast<const uint16_t*>(S.cd[b]) + wo + lane, acc,
+                              xj, xk);
       } else {
-        auto T = [&](unsigned i) -> d4 { return X[__ldg(tn + i)]; };
-        ring_walk(T, rcodes + m.x + wo + lane, n, acc, xj, xk);
+        auto T = [&](unsigned i) -> d4 {
+          const int r = __ldg(tn + i);
+          const double2 v = __ldg(mxy + r);
+          d4 q;
+          q.x = v.x;
+          q.y = v.y;
+          q.z = __ldg(mz + r);
+          return q;
+        };
+        bflag = ring_walk(T, rcodes + m.x + wo + lane, acc, xj, xk);
       }
     }
     double nv[3] = {0.0, 0.0, 0.0};
     double s = 0.0;
     if (valid) {
+      // boundary terms: the tile's slice of the position-keyed facet list
       const u32 rb = static_cast<u32>(m.w);
-      edge_tail_values<3, kDualFree>(X, e, acc, xj, xk, bedge, rb,
-                                     rb + (static_cast<u32>(m.z) >> 16), bnd, nv, s);
+      const u32 re = bflag ? rb + (static_cast<u32>(m.z) >> 16) : rb;
+      edge_tail_values<3, kDualFree>(X, p, acc, xj, xk, bedge_p, rb, re, bnd, nv, s);
       svals[e] = s;
     }
-    store_navs_warp<3>(nv, e - lane, ne, navs);
-    __syncthreads();  // buffer b is refilled two iterations from now
+    if (valid) store_nav_row(navs, e, nv);
+    __syncthreads();  // buffer b is refilled next iteration
   }
   cp_async_wait<0>();
 }
@@ -743,18 +780,18 @@ int launch_navs(dm_ctx* c, int variant) {
         DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
         const unsigned grid = static_cast<unsigned>(std::min<i64>(
             static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
-        DM_LAUNCH(c, kern, grid, kEB, smem, c->inc_ptr.p, c->rcodes.p, c->tnodes.p,
-                  c->ring_meta.p, X, ne, static_cast<int>(tiles), c->bedge.p, c->bnd.p,
+        DM_LAUNCH(c, kern, grid, kEB, smem, c->eperm.p, c->rcodes.p, c->tnodes.p,
+                  c->ring_meta.p, c->mxy.p, c->mz.p, X, ne, static_cast<int>(tiles), c->bedge_p.p, c->bnd.p,
                   c->navs.p, c->svals.p);
         return DM_OK;
       };
       int st = DM_OK;
       switch (c->gather_cfg) {
-        case 7: st = launch(k_navs_ring_pipe<768, 3, 2>, sizeof(PipeSmem<768>)); break;
-        case 8: st = launch(k_navs_ring_pipe<640, 4>, sizeof(PipeSmem<640>)); break;
-        case 9: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
+        case 7: st = launch(k_navs_ring_pipe<512, 3, 2>, sizeof(PipeSmem<512>)); break;
+        case 8: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
+        case 9: st = launch(k_navs_ring_pipe<256, 3>, sizeof(PipeSmem<256>)); break;
         case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
-        default: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
+        default: st = launch(k_navs_ring_pipe<512, 3>, sizeof(PipeSmem<512>)); break;
       }
       if (st) return st;
     }

@@ -9,24 +9,45 @@
 // mesh.cpp:15,103-110), so walking the ring needs ONE new coordinate per
 // incidence instead of three.
 //
-//   tile nodes : per 256-edge tile, the sorted unique ids of every node the
+//   edge order : tiles are 256 consecutive positions p of a permutation
+//                eperm[p] = e of the edges.  Origins are visited in Morton
+//                (Z-curve) order of their coordinates and each origin's
+//                edge range [os[j], os[j+1]) is appended whole, so a tile
+//                covers a compact 3D block of origins whatever the node
+//                numbering: its node table (origins plus a one-node halo)
+//                is ~4x the origin count instead of ~13x for a strip of
+//                consecutive origins, and randomly numbered meshes keep
+//                the same locality.  Outputs still go to navs[e] / svals[e].
+//   coordinates: a copy of the coordinates in Morton rank order (mxy 16 B,
+//                mz 8 B per node), refreshed with every coordinate update,
+//                so a tile's table is a few contiguous rank ranges.
+//   tile nodes : per tile, the sorted unique Morton ranks of every node the
 //                tile touches (j, k, ring nodes), at a fixed stride of
 //                kTileNodeCap, count in tnode_cnt[tile].
 //   ring codes : per edge, n+3 16-bit words
-//                  [slot(j) | s<<15, slot(k), slot(m_0), slot(m_1), ...,
-//                   slot(m_n)]                  (slots into the tile list)
-//                stored lane-transposed per warp of 32 consecutive edges: the
-//                warp block holds S_w = max(n+3) steps x 32 lanes, entry
+//                  [slot(j) | s<<15, slot(k) | n<<11, slot(m_0) | b<<15,
+//                   slot(m_1), ..., slot(m_n)]  (slots into the tile list;
+//                                                b: edge has boundary facets)
+//                stored lane-transposed per warp of 32 consecutive positions:
+//                the warp block holds S_w = max(n+3) steps x 32 lanes, entry
 //                (step, lane) at wstart[w] + step*32 + lane, so the 32 lanes
 //                of a ring step read 64 contiguous bytes (one wavefront).
-//                where s is the common orientation of all terms of the edge:
+//                s is the common orientation of all terms of the edge:
 //                around a consistently oriented ring every term has the same
 //                parity, so the sign is applied once to the sum
 //                (sum(-c_i) == -sum(c_i) exactly in IEEE arithmetic).
-// Built once per topology.  Any tile with more than kTileNodeCap nodes, an
-// edge with more than kRingMax incidences or a non-manifold fan (the walk
-// does not consume every incident element) sets ring_ok = false and the
-// GATHER path falls back to the bit-exact row-table kernel.
+//   boundary   : the (edge, facet) list re-keyed by position, (p << 32 |
+//                facet), sorted, with per-tile slices.
+// Built once per topology (the Morton order uses the coordinates present at
+// build time; later coordinates only change locality, never results).  Any
+// tile with more than kTileNodeCap nodes, an edge with more than kRingMax
+// incidences or a non-manifold fan (the walk does not consume every incident
+// element) sets ring_ok = false and the GATHER path falls back to the
+// bit-exact row-table kernel.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <vector>
+
 #include "dm_internal.cuh"
 
 namespace dm {
@@ -35,29 +56,31 @@ namespace {
 constexpr int kCand = 8192;  // candidate ids gathered per tile (before dedup)
 
 __global__ void __launch_bounds__(kTileEdges)
-    k_tile_nodes(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
-                 const int32_t* __restrict__ inc, const int32_t* __restrict__ el, i64 ne,
+    k_tile_nodes(const int2* __restrict__ edges, const int32_t* __restrict__ eperm,
+                 const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+                 const int32_t* __restrict__ el, const int32_t* __restrict__ rank, i64 ne,
                  int32_t* __restrict__ tnodes, u32* __restrict__ tcnt, int* __restrict__ flag) {
   __shared__ int buf[kCand];
   __shared__ int s_n;
   __shared__ int s_w[kTileEdges / 32 + 1];
   const int t = threadIdx.x;
-  const i64 e = static_cast<i64>(blockIdx.x) * kTileEdges + t;
+  const i64 p = static_cast<i64>(blockIdx.x) * kTileEdges + t;
   if (t == 0) s_n = 0;
   __syncthreads();
-  if (e < ne) {
+  if (p < ne) {
+    const int e = eperm[p];
     const int2 jk = edges[e];
     const int pb = inc_ptr[e], pe = inc_ptr[e + 1];
     const int m = 2 + 2 * (pe - pb);
     int w = atomicAdd(&s_n, m);
     if (w + m <= kCand) {
-      buf[w++] = jk.x;
-      buf[w++] = jk.y;
+      buf[w++] = rank[jk.x];
+      buf[w++] = rank[jk.y];
       for (int q = pb; q < pe; ++q) {
         const int4 v = reinterpret_cast<const int4*>(el)[inc[q]];
         const int vs[4] = {v.x, v.y, v.z, v.w};
         for (int a = 0; a < 4; ++a)
-          if (vs[a] != jk.x && vs[a] != jk.y) buf[w++] = vs[a];
+          if (vs[a] != jk.x && vs[a] != jk.y) buf[w++] = rank[vs[a]];
       }
     }
   }
@@ -137,14 +160,17 @@ __device__ __forceinline__ int perm_sign(int a0, int a1, int a2, int b0, int b1,
   return x1 == b1 ? 1 : -1;
 }
 
-__global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
+__global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __restrict__ eperm,
+                             const int32_t* __restrict__ inc_ptr,
                              const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
+                             const int32_t* __restrict__ rank, const uint8_t* __restrict__ bmark,
                              const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt,
                              const u32* __restrict__ wstart, i64 ne,
                              uint16_t* __restrict__ rcodes, int* __restrict__ flag) {
-  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= ne) return;
-  const i64 tile = e / kTileEdges;
+  const i64 p = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= ne) return;
+  const int e = eperm[p];
+  const i64 tile = p / kTileEdges;
   const int32_t* list = tnodes + tile * kTileNodeCap;
   const int nl = static_cast<int>(tcnt[tile]);
   const int2 jk = edges[e];
@@ -180,9 +206,9 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
     }
   if (start < 0) start = a[0];
   // step s of this edge lives at out[s * 32]
-  uint16_t* out = rcodes + wstart[e >> 5] + (e & 31);
+  uint16_t* out = rcodes + wstart[p >> 5] + (p & 31);
   int sg0 = 0;
-  out[2 * 32] = static_cast<uint16_t>(tslot(list, nl, start));
+  out[2 * 32] = static_cast<uint16_t>(tslot(list, nl, rank[start]) | (bmark[e] ? 0x8000u : 0u));
   unsigned used = 0;
   int cur = start;
   for (int step = 0; step < n; ++step) {
@@ -204,20 +230,24 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
       atomicOr(flag, 16);  // inconsistently oriented fan
       return;
     }
-    out[(3 + step) * 32] = static_cast<uint16_t>(tslot(list, nl, nxt));
+    out[(3 + step) * 32] = static_cast<uint16_t>(tslot(list, nl, rank[nxt]));
     cur = nxt;
   }
-  out[0] = static_cast<uint16_t>(tslot(list, nl, j) | (sg0 < 0 ? 0x8000u : 0u));
-  out[32] = static_cast<uint16_t>(tslot(list, nl, k));
+  out[0] = static_cast<uint16_t>(tslot(list, nl, rank[j]) | (sg0 < 0 ? 0x8000u : 0u));
+  out[32] = static_cast<uint16_t>(tslot(list, nl, rank[k]) | n << 11);
 }
 
 // Codes per warp block: S_w * 32 with S_w = max over the warp's edges of n+3.
-__global__ void k_ring_warpsize(const int32_t* __restrict__ inc_ptr, i64 ne, i64 nwarps,
+__global__ void k_ring_warpsize(const int32_t* __restrict__ eperm,
+                                const int32_t* __restrict__ inc_ptr, i64 ne, i64 nwarps,
                                 u32* __restrict__ wsize) {
   const i64 w = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (w >= nwarps) return;
   int S = 3;
-  for (i64 e = w * 32; e < w * 32 + 32 && e < ne; ++e) S = max(S, inc_ptr[e + 1] - inc_ptr[e] + 3);
+  for (i64 p = w * 32; p < w * 32 + 32 && p < ne; ++p) {
+    const int e = eperm[p];
+    S = max(S, inc_ptr[e + 1] - inc_ptr[e] + 3);
+  }
   wsize[w] = static_cast<u32>(S * 32);
 }
 
@@ -244,6 +274,190 @@ __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restric
                               static_cast<int>(o[2]), static_cast<int>(o[3]));
 }
 
+
+// ---- Morton origin order and the edge permutation
+
+static_assert(kTileNodeCap <= 2048 && kRingMax < 32, "code word 1 packs slot(k) | n << 11");
+
+// per-block partial bounding box of the coordinates: part[6 * block + {lo, hi}]
+__global__ void __launch_bounds__(256) k_bbox(const d4* __restrict__ x4, i64 nv,
+                                              double* __restrict__ part) {
+  __shared__ double sh[6][256];
+  const int t = threadIdx.x;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (i64 v = static_cast<i64>(blockIdx.x) * 256 + t; v < nv;
+       v += static_cast<i64>(gridDim.x) * 256) {
+    const d4 r = x4[v];
+    lo[0] = fmin(lo[0], r.x);
+    lo[1] = fmin(lo[1], r.y);
+    lo[2] = fmin(lo[2], r.z);
+    hi[0] = fmax(hi[0], r.x);
+    hi[1] = fmax(hi[1], r.y);
+    hi[2] = fmax(hi[2], r.z);
+  }
+  for (int d = 0; d < 3; ++d) {
+    sh[d][t] = lo[d];
+    sh[3 + d][t] = hi[d];
+  }
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (t < h)
+      for (int d = 0; d < 3; ++d) {
+        sh[d][t] = fmin(sh[d][t], sh[d][t + h]);
+        sh[3 + d][t] = fmax(sh[3 + d][t], sh[3 + d][t + h]);
+      }
+    __syncthreads();
+  }
+  if (t < 6) part[6 * blockIdx.x + t] = sh[t][0];
+}
+
+__device__ __forceinline__ u64 spread21(u64 v) {  // bit i -> bit 3i
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+
+__global__ void k_morton(const d4* __restrict__ x4, i64 nv, double lx, double ly, double lz,
+                         double sc, u64* __restrict__ key, int32_t* __restrict__ id) {
+  const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const d4 r = x4[v];
+  auto q = [&](double x) -> u64 {
+    const double f = x * sc;
+    return f <= 0.0 ? 0ull : (f >= 2097151.0 ? 2097151ull : static_cast<u64>(f));
+  };
+  key[v] = spread21(q(r.x - lx)) | spread21(q(r.y - ly)) << 1 | spread21(q(r.z - lz)) << 2;
+  id[v] = static_cast<int32_t>(v);
+}
+
+__global__ void k_origin_count(const int32_t* __restrict__ ord, const u32* __restrict__ os, i64 nv,
+                               u32* __restrict__ cnt) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const int o = ord[i];
+  cnt[i] = os[o + 1] - os[o];
+}
+
+__global__ void k_eperm(const int32_t* __restrict__ ord, const u32* __restrict__ os,
+                        const u32* __restrict__ pstart, i64 nv, int32_t* __restrict__ eperm,
+                        int32_t* __restrict__ pinv) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const u32 base = os[ord[i]], p0 = pstart[i], n = pstart[i + 1] - p0;
+  for (u32 q = 0; q < n; ++q) {
+    eperm[p0 + q] = static_cast<int32_t>(base + q);
+    pinv[base + q] = static_cast<int32_t>(p0 + q);
+  }
+}
+
+__global__ void k_bkey(const u64* __restrict__ bedge, i64 n, const int32_t* __restrict__ pinv,
+                       u64* __restrict__ out) {
+  const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const u64 it = bedge[q];
+  out[q] = static_cast<u64>(pinv[it >> 32]) << 32 | (it & 0xffffffffull);
+}
+
+__global__ void k_rank(const int32_t* __restrict__ order, i64 nv, int32_t* __restrict__ rank) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < nv) rank[order[r]] = static_cast<int32_t>(r);
+}
+
+__global__ void k_bmark(const u64* __restrict__ bedge, i64 n, uint8_t* __restrict__ mark) {
+  const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < n) mark[bedge[q] >> 32] = 1;
+}
+
+__global__ void k_morton_coords(const d4* __restrict__ x4, const int32_t* __restrict__ order,
+                                i64 nv, double2* __restrict__ xy, double* __restrict__ z) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const d4 p = x4[order[r]];
+  xy[r] = make_double2(p.x, p.y);
+  z[r] = p.z;
+}
+
+int bits_for(u64 v) {
+  int b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// eperm (Morton origin order), bedge_p and its per-tile slices.
+int build_edge_order(dm_ctx* c) {
+  const i64 nv = c->nv, ne = c->ne, nb = c->n_bedge;
+  const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
+  // bounding box
+  const int nblk = static_cast<int>(std::max<i64>(1, std::min<i64>(1024, (nv + 255) / 256)));
+  DevBuf<double> part;
+  DM_CK(c, part.ensure(6 * nblk));
+  DM_LAUNCH(c, k_bbox, nblk, 256, 0, c->x4.p, nv, part.p);
+  std::vector<double> hp(6 * nblk);
+  DM_CK(c, cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int b = 0; b < nblk; ++b)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(lo[d], hp[6 * b + d]);
+      hi[d] = std::max(hi[d], hp[6 * b + 3 + d]);
+    }
+  double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
+  if (!(ext > 0.0) || !std::isfinite(ext)) ext = 1.0;
+  const double sc = 2097151.0 / ext;
+  // Morton keys -> origin order (stable radix sort: ties keep id order)
+  DevBuf<u64> k0, k1;
+  DevBuf<int32_t> i0;
+  DM_CK(c, k0.ensure(nv));
+  DM_CK(c, k1.ensure(nv));
+  DM_CK(c, i0.ensure(nv));
+  DM_CK(c, c->morder.ensure(nv));
+  int32_t* i1p = c->morder.p;
+  DM_LAUNCH(c, k_morton, grid_for(nv, 256), 256, 0, c->x4.p, nv, lo[0], lo[1], lo[2], sc, k0.p,
+            i0.p);
+  size_t tb = 0;
+  DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
+                                           c->stream));
+  DevBuf<unsigned char> tmp;
+  DM_CK(c, tmp.ensure(tb));
+  DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, tb, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
+                                           c->stream));
+  // edge permutation: each origin's edge range appended whole, in that order
+  DevBuf<u32> pstart;
+  DevBuf<int32_t> pinv;
+  DM_CK(c, pstart.ensure(nv + 1));
+  DM_CK(c, pinv.ensure(ne > 0 ? ne : 1));
+  DM_CK(c, c->eperm.ensure(ne > 0 ? ne : 1));
+  DM_LAUNCH(c, k_origin_count, grid_for(nv, 256), 256, 0, i1p, c->os.p, nv, pstart.p);
+  int st = scan_exclusive(c, pstart.p, pstart.p, nv);
+  if (st) return st;
+  DM_LAUNCH(c, k_eperm, grid_for(nv, 256), 256, 0, i1p, c->os.p, pstart.p, nv, c->eperm.p,
+            pinv.p);
+  // boundary (edge, facet) list re-keyed by position
+  DM_CK(c, c->bedge_p.ensure(nb > 0 ? nb : 1));
+  DM_CK(c, c->tile_bptr_p.ensure(ntiles + 1));
+  if (nb > 0) {
+    DevBuf<u64> bk;
+    DM_CK(c, bk.ensure(nb));
+    DM_LAUNCH(c, k_bkey, grid_for(nb, 256), 256, 0, c->bedge.p, nb, pinv.p, bk.p);
+    const int hb = 32 + bits_for(static_cast<u64>(ne));
+    tb = 0;
+    DM_CK(c, cub::DeviceRadixSort::SortKeys(nullptr, tb, bk.p, c->bedge_p.p, nb, 0, hb,
+                                            c->stream));
+    DM_CK(c, tmp.ensure(tb));
+    DM_CK(c, cub::DeviceRadixSort::SortKeys(tmp.p, tb, bk.p, c->bedge_p.p, nb, 0, hb,
+                                            c->stream));
+  }
+  DM_LAUNCH(c, k_tile_bptr, grid_for(ntiles + 1, 256), 256, 0, c->bedge_p.p,
+            static_cast<u32>(nb), ne, ntiles, c->tile_bptr_p.p);
+  DM_CK(c, cudaStreamSynchronize(c->stream));  // scratch buffers die here
+  return DM_OK;
+}
+
 }  // namespace
 
 int ensure_rings(dm_ctx* c) {
@@ -258,6 +472,13 @@ int ensure_rings(dm_ctx* c) {
   const i64 ne = c->ne;
   const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
   const i64 nwarps = (ne + 31) / 32;
+  if (ne == 0 || !c->x4.p) {
+    c->ring_ok = false;
+    c->have_rings = true;
+    return DM_OK;
+  }
+  int st1 = build_edge_order(c);
+  if (st1) return st1;
   DM_CK(c, c->tnodes.ensure(static_cast<size_t>(ntiles * kTileNodeCap)));
   DM_CK(c, c->tnode_cnt.ensure(static_cast<size_t>(ntiles)));
   // tiles that overflow the caps keep count 0 (their codes are never used:
@@ -266,7 +487,7 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(2 * ntiles)));
   DevBuf<u32> wstart;
   DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
-  DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->inc_ptr.p, ne, nwarps, wstart.p);
+  DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->eperm.p, c->inc_ptr.p, ne, nwarps, wstart.p);
   int st = scan_exclusive(c, wstart.p, wstart.p, nwarps);
   if (st) return st;
   u32 ncodes = 0;
@@ -278,12 +499,22 @@ int ensure_rings(dm_ctx* c) {
                            c->stream));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
+  DevBuf<int32_t> rank;
+  DevBuf<uint8_t> bmark;
+  DM_CK(c, rank.ensure(c->nv));
+  DM_CK(c, bmark.ensure(ne));
+  DM_LAUNCH(c, k_rank, grid_for(c->nv, 256), 256, 0, c->morder.p, c->nv, rank.p);
+  DM_CK(c, cudaMemsetAsync(bmark.p, 0, ne, c->stream));
+  if (c->n_bedge > 0)
+    DM_LAUNCH(c, k_bmark, grid_for(c->n_bedge, 256), 256, 0, c->bedge.p, c->n_bedge, bmark.p);
   DM_LAUNCH(c, k_tile_nodes, static_cast<unsigned>(ntiles), kTileEdges, 0, c->edges.p,
-            c->inc_ptr.p, c->inc.p, c->elems.p, ne, c->tnodes.p, c->tnode_cnt.p, c->flag.p);
-  DM_LAUNCH(c, k_ring_codes, grid_for(ne, 128), 128, 0, c->edges.p, c->inc_ptr.p, c->inc.p,
-            c->elems.p, c->tnodes.p, c->tnode_cnt.p, wstart.p, ne, c->rcodes.p, c->flag.p);
+            c->eperm.p, c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, ne, c->tnodes.p,
+            c->tnode_cnt.p, c->flag.p);
+  DM_LAUNCH(c, k_ring_codes, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p, c->inc_ptr.p,
+            c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p, wstart.p, ne,
+            c->rcodes.p, c->flag.p);
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
-            c->tile_bptr.p, nwarps, ntiles, c->ring_meta.p);
+            c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
   int fl[2] = {0, 0};
   DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
@@ -291,6 +522,15 @@ int ensure_rings(dm_ctx* c) {
   c->ring_max_nodes = fl[1];
   c->ring_ok = (fl[0] == 0);
   c->have_rings = true;
+  return c->ring_ok ? refresh_ring_coords(c) : DM_OK;
+}
+
+int refresh_ring_coords(dm_ctx* c) {
+  const i64 nv = c->nv;
+  DM_CK(c, c->mxy.ensure(nv));
+  DM_CK(c, c->mz.ensure(nv));
+  DM_LAUNCH(c, k_morton_coords, grid_for(nv, 256), 256, 0, c->x4.p, c->morder.p, nv, c->mxy.p,
+            c->mz.p);
   return DM_OK;
 }
 

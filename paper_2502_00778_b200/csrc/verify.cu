@@ -201,30 +201,10 @@ int device_sum(dm_ctx* c, const double* x, i64 n, double* out) {
 
 int pad_coords(dm_ctx* c) {
   if (c->dim != 3) return DM_OK;
-  const bool realloc = c->x4.n < static_cast<size_t>(c->nv) || !c->x4.p;
   DM_CK(c, c->x4.ensure(static_cast<size_t>(c->nv)));
   DM_LAUNCH(c, k_pad3, grid_for(c->nv, 256), 256, 0, c->coords.p, c->nv, c->x4.p);
-  if (realloc || !c->x4_map_ok) {
-    // TMA tensor map over the padded coordinates for tile::gather4 (navs.cu)
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-      cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc),
-                                  cudaEnableDefault, &q) != cudaSuccess)
-        enc = nullptr;
-    }
-    c->x4_map_ok = false;
-    if (enc && c->nv > 0) {
-      cuuint64_t gdim[2] = {4, static_cast<cuuint64_t>(c->nv)};
-      cuuint64_t gstride[1] = {sizeof(d4)};
-      cuuint32_t box[2] = {4, 1};
-      cuuint32_t estr[2] = {1, 1};
-      c->x4_map_ok = enc(&c->x4_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->x4.p, gdim, gstride,
-                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    }
-  }
+  // the ring path's Morton-ordered copy follows every coordinate update
+  if (c->have_rings && c->ring_ok) return refresh_ring_coords(c);
   return DM_OK;
 }
 
