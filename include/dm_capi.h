@@ -157,7 +157,8 @@ int dm_get_timings(dm_ctx* ctx, float* ms, int n);
 int64_t dm_kernel_launches(const dm_ctx* ctx);
 /* Which element-loop kernels the plan enables: info[0] ring path built,
  * [1] ring path usable, [2] row tables built, [3] row tables usable,
- * [4] max tile node count (ring path), [5] failure flag of the ring build. */
+ * [4] max tile node count (ring path), [5] failure flag of the ring build,
+ * [6] edge-volume pass walks nodes in Morton order (1) or id order (0). */
 int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
 /* Pinned host memory for end-to-end transfers. */
 int dm_host_alloc(size_t bytes, void** ptr);

@@ -221,6 +221,7 @@ int dm_put_navs(dm_ctx* c, const double* navs) {
                            cudaMemcpyHostToDevice, c->stream));
   DM_CK(c, c->svals.ensure(static_cast<size_t>(c->ne)));
   int st = svals_from_navs(c);
+  c->svals_pos = false;
   if (st) return st;
   c->have_navs = true;
   c->have_vols = false;
@@ -334,6 +335,7 @@ int dm_plan_info(dm_ctx* c, int64_t info[8]) {
   info[3] = c->table_ok;
   info[4] = c->ring_max_nodes;
   info[5] = c->ring_fail;
+  info[6] = c->vol_by_rank;
   return DM_OK;
 }
 

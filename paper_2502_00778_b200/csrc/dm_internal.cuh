@@ -95,6 +95,11 @@ struct dm_ctx {
   dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU | nbnd << 16, bptr}, offsets
   dm::DevBuf<int32_t> eperm;       // tile position p -> edge id (Morton origin order)
   dm::DevBuf<int32_t> morder;      // Morton rank -> node id
+  dm::DevBuf<dm::u32> rpstart;     // rank r's outgoing edges at positions [rpstart[r], rpstart[r+1])
+  dm::DevBuf<dm::u32> rin_ptr;     // rank r's incoming edges, as positions, in
+  dm::DevBuf<int32_t> rin_list;    //   ascending edge id (rin_list[rin_ptr[r] ..])
+  bool vol_by_rank = false;        // node ids lack locality: s in position order,
+                                   // volume pass in Morton rank order
   dm::DevBuf<double2> mxy;         // coordinates in Morton rank order: (x, y)
   dm::DevBuf<double> mz;           //                                    z
   dm::DevBuf<dm::u64> bedge_p;     // (p << 32 | facet), sorted
@@ -107,6 +112,7 @@ struct dm_ctx {
   bool have_navs = false, have_vols = false;
   int navs_algo = -1;
   dm::DevBuf<double> navs, svals, vols, velem;
+  bool svals_pos = false;  // svals indexed by ring position p (rings.cu), not edge id
 
   // verify / reductions scratch
   dm::DevBuf<double> red;

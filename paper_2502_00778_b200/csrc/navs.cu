@@ -471,12 +471,13 @@ __device__ __forceinline__ bool ring_walk(const TabFn& T, const uint16_t* __rest
   return (w2 & 0x8000u) != 0;
 }
 
-template <int CAP, int MINB, int RU = 1>
+template <int CAP, int MINB, int RU = 1, int FAKE = 0>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint16_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      const double2* __restrict__ mxy, const double* __restrict__ mz,
-                     Coords<3> X, i64 ne, int ntiles, const u64* __restrict__ bedge_p,
+                     Coords<3> X, i64 ne, int ntiles, bool pos_s,
+                     const u64* __restrict__ bedge_p,
                      const int32_t* __restrict__ bnd, double* __restrict__ navs,
                      double* __restrict__ svals) {
   PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(dm_smem);
@@ -523,6 +524,7 @@ __global__ void __launch_bounds__(kEB, MINB)
         const double2* xy = S.xy[b];
         const double* zz = S.z[b];
         auto T = [&](unsigned i) -> d4 {
+          if (FAKE) i = (i & ~15u) | (lane & 15u);  // timing probe: conflict-free slots
           const double2 v = xy[i];
           d4 r;
           r.x = v.x;
@@ -552,7 +554,7 @@ __global__ void __launch_bounds__(kEB, MINB)
       const u32 rb = static_cast<u32>(m.w);
       const u32 re = bflag ? rb + (static_cast<u32>(m.z) >> 16) : rb;
       edge_tail_values<3, kDualFree>(X, p, acc, xj, xk, bedge_p, rb, re, bnd, nv, s);
-      svals[e] = s;
+      svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
     }
     if (valid) store_nav_row(navs, e, nv);
     __syncthreads();  // buffer b is refilled next iteration
@@ -781,7 +783,8 @@ int launch_navs(dm_ctx* c, int variant) {
         const unsigned grid = static_cast<unsigned>(std::min<i64>(
             static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
         DM_LAUNCH(c, kern, grid, kEB, smem, c->eperm.p, c->rcodes.p, c->tnodes.p,
-                  c->ring_meta.p, c->mxy.p, c->mz.p, X, ne, static_cast<int>(tiles), c->bedge_p.p, c->bnd.p,
+                  c->ring_meta.p, c->mxy.p, c->mz.p, X, ne, static_cast<int>(tiles),
+                  c->vol_by_rank, c->bedge_p.p, c->bnd.p,
                   c->navs.p, c->svals.p);
         return DM_OK;
       };
@@ -791,6 +794,7 @@ int launch_navs(dm_ctx* c, int variant) {
         case 8: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
         case 9: st = launch(k_navs_ring_pipe<256, 3>, sizeof(PipeSmem<256>)); break;
         case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
+        case 20: st = launch(k_navs_ring_pipe<512, 3, 1, 1>, sizeof(PipeSmem<512>)); break;
         default: st = launch(k_navs_ring_pipe<512, 3>, sizeof(PipeSmem<512>)); break;
       }
       if (st) return st;
@@ -869,6 +873,8 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
                                  : launch_navs<2, kTraditional>(c, variant);
   }
   if (st) return st;
+  c->svals_pos = variant == DM_VARIANT_GATHER && c->dim == 3 && algo == DM_NAV_DUALFREE &&
+                 c->ring_ok && c->vol_by_rank;
   c->have_navs = true;
   c->navs_algo = algo;
   c->have_vols = false;

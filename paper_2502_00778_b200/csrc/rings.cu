@@ -17,7 +17,13 @@
 //                numbering: its node table (origins plus a one-node halo)
 //                is ~4x the origin count instead of ~13x for a strip of
 //                consecutive origins, and randomly numbered meshes keep
-//                the same locality.  Outputs still go to navs[e] / svals[e].
+//                the same locality.  navs go to navs[e].  For node
+//                numberings without spatial locality the edge-volume terms
+//                stay in position order, svals[p], and the volume kernel
+//                walks nodes in Morton rank order with each rank's incoming
+//                (rin_ptr/rin_list) and outgoing (rpstart) edges as
+//                positions -- the same per-node fold order as the edge-id
+//                kernel, so the same bits.
 //   coordinates: a copy of the coordinates in Morton rank order (mxy 16 B,
 //                mz 8 B per node), refreshed with every coordinate update,
 //                so a tile's table is a few contiguous rank ranges.
@@ -354,6 +360,34 @@ __global__ void k_eperm(const int32_t* __restrict__ ord, const u32* __restrict__
   }
 }
 
+// rank-ordered incoming lists as positions: rin_list[rin_ptr[r] + q] =
+// pinv[in_list[in_ptr[morder[r]] + q]]
+__global__ void k_rin_count(const int32_t* __restrict__ ord, const u32* __restrict__ in_ptr, i64 nv,
+                            u32* __restrict__ cnt) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const int n = ord[r];
+  cnt[r] = in_ptr[n + 1] - in_ptr[n];
+}
+
+__global__ void k_rin_fill(const int32_t* __restrict__ ord, const u32* __restrict__ in_ptr,
+                           const int32_t* __restrict__ in_list, const int32_t* __restrict__ pinv,
+                           const u32* __restrict__ rptr, i64 nv, int32_t* __restrict__ out) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const int n = ord[r];
+  const u32 b = in_ptr[n], m = in_ptr[n + 1] - b, o = rptr[r];
+  for (u32 q = 0; q < m; ++q) out[o + q] = pinv[in_list[b + q]];
+}
+
+// number of nodes n whose successor n+1 is within 8 Morton ranks
+__global__ void k_locality(const int32_t* __restrict__ rank, i64 nv, u32* __restrict__ cnt) {
+  const i64 n = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool near = n + 1 < nv && abs(rank[n + 1] - rank[n]) <= 8;
+  const unsigned b = __ballot_sync(0xffffffffu, near);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(cnt, static_cast<u32>(__popc(b)));
+}
+
 __global__ void k_bkey(const u64* __restrict__ bedge, i64 n, const int32_t* __restrict__ pinv,
                        u64* __restrict__ out) {
   const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -427,16 +461,46 @@ int build_edge_order(dm_ctx* c) {
   DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, tb, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
                                            c->stream));
   // edge permutation: each origin's edge range appended whole, in that order
-  DevBuf<u32> pstart;
+  u32* pstart = nullptr;
   DevBuf<int32_t> pinv;
-  DM_CK(c, pstart.ensure(nv + 1));
+  DM_CK(c, c->rpstart.ensure(nv + 1));
+  pstart = c->rpstart.p;
   DM_CK(c, pinv.ensure(ne > 0 ? ne : 1));
   DM_CK(c, c->eperm.ensure(ne > 0 ? ne : 1));
-  DM_LAUNCH(c, k_origin_count, grid_for(nv, 256), 256, 0, i1p, c->os.p, nv, pstart.p);
-  int st = scan_exclusive(c, pstart.p, pstart.p, nv);
+  DM_LAUNCH(c, k_origin_count, grid_for(nv, 256), 256, 0, i1p, c->os.p, nv, pstart);
+  int st = scan_exclusive(c, pstart, pstart, nv);
   if (st) return st;
-  DM_LAUNCH(c, k_eperm, grid_for(nv, 256), 256, 0, i1p, c->os.p, pstart.p, nv, c->eperm.p,
+  DM_LAUNCH(c, k_eperm, grid_for(nv, 256), 256, 0, i1p, c->os.p, pstart, nv, c->eperm.p,
             pinv.p);
+  // Edge-volume terms: for a spatially coherent node numbering the edge-id
+  // order is already local, so s goes to svals[e] and the id-order volume
+  // pass reads it coalesced; otherwise s stays in position order and the
+  // volume pass walks Morton ranks (vol_by_rank).
+  {
+    DevBuf<int32_t> rk;
+    DevBuf<u32> cnt;
+    DM_CK(c, rk.ensure(nv));
+    DM_CK(c, cnt.ensure(1));
+    DM_CK(c, cudaMemsetAsync(cnt.p, 0, sizeof(u32), c->stream));
+    DM_LAUNCH(c, k_rank, grid_for(nv, 256), 256, 0, i1p, nv, rk.p);
+    DM_LAUNCH(c, k_locality, static_cast<unsigned>((nv + 255) / 256), 256, 0, rk.p, nv, cnt.p);
+    u32 near = 0;
+    DM_CK(c, cudaMemcpyAsync(&near, cnt.p, sizeof(u32), cudaMemcpyDeviceToHost, c->stream));
+    DM_CK(c, cudaStreamSynchronize(c->stream));
+    c->vol_by_rank = static_cast<double>(near) < 0.25 * static_cast<double>(nv);
+  }
+  if (c->vol_by_rank) {  // incoming edges per rank, as positions (volumes.cu)
+    st = ensure_incoming(c);
+    if (st) return st;
+    DM_CK(c, c->rin_ptr.ensure(nv + 1));
+    DM_CK(c, c->rin_list.ensure(ne));
+    DM_LAUNCH(c, k_rin_count, grid_for(nv, 256), 256, 0, i1p, c->in_ptr.p, nv, c->rin_ptr.p);
+    st = scan_exclusive(c, c->rin_ptr.p, c->rin_ptr.p, nv);
+    if (st) return st;
+    DM_LAUNCH(c, k_rin_fill, grid_for(nv, 256), 256, 0, i1p, c->in_ptr.p, c->in_list.p, pinv.p,
+              c->rin_ptr.p, nv, c->rin_list.p);
+  }
+
   // boundary (edge, facet) list re-keyed by position
   DM_CK(c, c->bedge_p.ensure(nb > 0 ? nb : 1));
   DM_CK(c, c->tile_bptr_p.ensure(ntiles + 1));

@@ -14,6 +14,24 @@
 namespace dm {
 namespace {
 
+// acc += s[idx(q)] for q in [b, e), in order; the loads of each batch of
+// kB terms are issued before any add (memory-level parallelism on a
+// latency-bound gather; the fold order is unchanged).
+constexpr int kB = 8;
+template <typename Idx>
+__device__ __forceinline__ double fold_terms(double acc, u32 b, u32 e, const Idx& idx,
+                                             const double* __restrict__ s) {
+  for (u32 q0 = b; q0 < e; q0 += kB) {
+    double v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) v[u] = q0 + u < e ? s[idx(q0 + u)] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (q0 + u < e) acc += v[u];
+  }
+  return acc;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256)
     k_vol_edge(const u32* __restrict__ in_ptr, const int32_t* __restrict__ in_list,
@@ -21,12 +39,25 @@ __global__ void __launch_bounds__(256)
                double* __restrict__ V) {
   const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= nv) return;
-  double acc = 0.0;
-  const u32 ib = in_ptr[v], ie = in_ptr[v + 1];
-  for (u32 q = ib; q < ie; ++q) acc += svals[__ldg(in_list + q)];
-  const u32 ob = os[v], oe = os[v + 1];
-  for (u32 q = ob; q < oe; ++q) acc += svals[q];
+  const u32 ib = in_ptr[v], ie = in_ptr[v + 1], ob = os[v], oe = os[v + 1];
+  double acc = fold_terms(0.0, ib, ie, [&](u32 q) { return __ldg(in_list + q); }, svals);
+  acc = fold_terms(acc, ob, oe, [](u32 q) { return q; }, svals);
   V[v] = acc * (1.0 / static_cast<double>(2 * D));
+}
+
+// Same fold with the ring path's position-ordered s: one thread per Morton
+// rank r (node morder[r]), incoming positions rin_list, outgoing positions
+// [rpstart[r], rpstart[r+1]) -- each node's terms in the same order as above.
+__global__ void __launch_bounds__(256)
+    k_vol_edge_pos(const int32_t* __restrict__ morder, const u32* __restrict__ rin_ptr,
+                   const int32_t* __restrict__ rin_list, const u32* __restrict__ rpstart,
+                   const double* __restrict__ svals, i64 nv, double* __restrict__ V) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const u32 ib = rin_ptr[r], ie = rin_ptr[r + 1], ob = rpstart[r], oe = rpstart[r + 1];
+  double acc = fold_terms(0.0, ib, ie, [&](u32 q) { return __ldg(rin_list + q); }, svals);
+  acc = fold_terms(acc, ob, oe, [](u32 q) { return q; }, svals);
+  V[morder[r]] = acc * (1.0 / 6.0);
 }
 
 template <int D>
@@ -75,7 +106,10 @@ int volumes_impl(dm_ctx* c, int algo) {
     int st = ensure_incoming(c);
     if (st) return st;
     tmark(c, 2);
-    if (c->dim == 3) {
+    if (c->svals_pos) {
+      DM_LAUNCH(c, k_vol_edge_pos, grid_for(nv, 256), 256, 0, c->morder.p, c->rin_ptr.p,
+                c->rin_list.p, c->rpstart.p, c->svals.p, nv, c->vols.p);
+    } else if (c->dim == 3) {
       DM_LAUNCH(c, k_vol_edge<3>, grid_for(nv, 256), 256, 0, c->in_ptr.p, c->in_list.p, c->os.p,
                 c->svals.p, nv, c->vols.p);
     } else {

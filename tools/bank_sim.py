@@ -260,3 +260,18 @@ def color_online(rs, u, nslots=256, lanes=32):
         slot[v] = c + 16 * nxt[c]
         nxt[c] += 1
     return slot
+
+
+def color_rank_bits(u, nslots=256, key=lambda r: r % 16):
+    """Colour = a function of the Morton rank (no access analysis); full
+    colour classes spill to the least used class."""
+    cap = nslots // 16
+    used = [0] * 16
+    slot = {}
+    for r in u:
+        c = key(r)
+        if used[c] >= cap:
+            c = min(range(16), key=lambda q: used[q])
+        slot[r] = c + 16 * used[c]
+        used[c] += 1
+    return slot
