@@ -104,6 +104,9 @@ struct dm_ctx {
   dm::DevBuf<double> mz;           //                                    z
   dm::DevBuf<dm::u64> bedge_p;     // (p << 32 | facet), sorted
   dm::DevBuf<dm::u32> tile_bptr_p; // bedge_p slice per tile
+  dm::i64 n_bseg = 0;              // boundary edges (segments of bedge_p)
+  dm::DevBuf<int4> bseg;           // per boundary edge {e, j, k, p}
+  dm::DevBuf<dm::u32> bseg_start;  // its facets: bedge_p[bseg_start[i] .. bseg_start[i+1])
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
   dm::DevBuf<int32_t> n2e;
@@ -112,6 +115,7 @@ struct dm_ctx {
   bool have_navs = false, have_vols = false;
   int navs_algo = -1;
   dm::DevBuf<double> navs, svals, vols, velem;
+  dm::DevBuf<double> bterms;  // ring path: fb * n_B per boundary facet
   bool svals_pos = false;  // svals indexed by ring position p (rings.cu), not edge id
 
   // verify / reductions scratch

@@ -429,15 +429,16 @@ __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __
 // Walks one edge's ring; T(slot) returns the node record of a tile slot;
 // cd points at this lane's step-0 code, step s at cd[s * 32] (rings.cu
 // layout: word 0 = slot(j) | sign << 15, word 1 = slot(k) | n << 11,
-// word 2 = slot(m_0) | boundary << 15).  Returns the boundary bit.
+// word 2 = slot(m_0) | boundary << 15).  Returns the boundary bit.  x_j
+// is not needed by the walk; the caller reads it afterwards (fewer live
+// registers across the loop).
 template <int RU = 1, typename TabFn>
 __device__ __forceinline__ bool ring_walk(const TabFn& T, const uint16_t* __restrict__ cd,
-                                          double* acc, d4& xj, d4& xk) {
+                                          double* acc, d4& xk) {
   const unsigned w0 = cd[0];
   const unsigned w1 = cd[32];
   const unsigned w2 = cd[64];
   const int n = static_cast<int>(w1 >> 11);
-  xj = T(w0 & 0x7ffu);
   xk = T(w1 & 0x7ffu);
   const d4 mp = T(w2 & 0x7ffu);
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
@@ -476,9 +477,7 @@ __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint16_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      const double2* __restrict__ mxy, const double* __restrict__ mz,
-                     Coords<3> X, i64 ne, int ntiles, bool pos_s,
-                     const u64* __restrict__ bedge_p,
-                     const int32_t* __restrict__ bnd, double* __restrict__ navs,
+                     Coords<3> X, i64 ne, int ntiles, bool pos_s, double* __restrict__ navs,
                      double* __restrict__ svals) {
   PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(dm_smem);
   const int t = threadIdx.x;
@@ -532,8 +531,9 @@ __global__ void __launch_bounds__(kEB, MINB)
           r.z = zz[i];
           return r;
         };
-        bflag = ring_walk<RU>(T, reinterpret_cast<const uint16_t*>(S.cd[b]) + wo + lane, acc,
-                              xj, xk);
+        const uint16_t* cd = reinterpret_cast<const uint16_t*>(S.cd[b]) + wo + lane;
+        bflag = ring_walk<RU>(T, cd, acc, xk);
+        xj = T(cd[0] & 0x7ffu);
       } else {
         auto T = [&](unsigned i) -> d4 {
           const int r = __ldg(tn + i);
@@ -544,16 +544,18 @@ __global__ void __launch_bounds__(kEB, MINB)
           q.z = __ldg(mz + r);
           return q;
         };
-        bflag = ring_walk(T, rcodes + m.x + wo + lane, acc, xj, xk);
+        const uint16_t* cd = rcodes + m.x + wo + lane;
+        bflag = ring_walk(T, cd, acc, xk);
+        xj = T(cd[0] & 0x7ffu);
       }
     }
     double nv[3] = {0.0, 0.0, 0.0};
     double s = 0.0;
+    (void)bflag;
     if (valid) {
-      // boundary terms: the tile's slice of the position-keyed facet list
-      const u32 rb = static_cast<u32>(m.w);
-      const u32 re = bflag ? rb + (static_cast<u32>(m.z) >> 16) : rb;
-      edge_tail_values<3, kDualFree>(X, p, acc, xj, xk, bedge_p, rb, re, bnd, nv, s);
+      // scale pass; boundary edges get their facet terms (and s) from
+      // k_ring_boundary, launched right after on the same stream
+      edge_tail_values<3, kDualFree>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
       svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
     }
     if (valid) store_nav_row(navs, e, nv);
@@ -724,6 +726,51 @@ __global__ void __launch_bounds__(kEB)
                      ALGO == kDualFree ? tile_bptr[blockIdx.x + 1] : 0u, bnd, navs, svals);
 }
 
+// Boundary pass of the ring path, in two steps: (1) the facet terms
+// fb * n_B once per facet (coalesced over the facet list), (2) one thread per
+// segment of the position-keyed (p << 32 | facet) list, i.e. per boundary
+// edge, adds its facets' terms in ascending facet id to the scaled navs row
+// and recomputes s -- the same values added in the same order as the fused
+// tail, so the same bits.
+__global__ void __launch_bounds__(256)
+    k_facet_terms(Coords<3> X, const int32_t* __restrict__ bnd, i64 nB,
+                  double* __restrict__ terms) {
+  const i64 f = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (f >= nB) return;
+  constexpr double fb = 1.0 / 12.0;
+  double b0, b1, b2;
+  bnormal3(X, bnd + 3 * f, b0, b1, b2);
+  terms[3 * f] = fb * b0;
+  terms[3 * f + 1] = fb * b1;
+  terms[3 * f + 2] = fb * b2;
+}
+
+__global__ void __launch_bounds__(256)
+    k_ring_boundary(const int4* __restrict__ seg, const u32* __restrict__ start, i64 ns,
+                    const u64* __restrict__ bedge_p, Coords<3> X,
+                    const double* __restrict__ terms, bool pos_s, double* __restrict__ navs,
+                    double* __restrict__ svals) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const int4 g = seg[i];  // {e, j, k, p}
+  const i64 e = g.x;
+  const u32 q0 = start[i], q1 = start[i + 1];
+  const d4 xj = X[g.y], xk = X[g.z];
+  double n[3] = {navs[3 * e], navs[3 * e + 1], navs[3 * e + 2]};  // already scaled
+  for (u32 q = q0; q < q1; ++q) {
+    const double* t = terms + 3 * static_cast<i64>(bedge_p[q] & 0xffffffffu);
+    n[0] += t[0];
+    n[1] += t[1];
+    n[2] += t[2];
+  }
+  double s = (xk.x - xj.x) * n[0] + (xk.y - xj.y) * n[1];
+  s = s + (xk.z - xj.z) * n[2];
+  navs[3 * e] = n[0];
+  navs[3 * e + 1] = n[1];
+  navs[3 * e + 2] = n[2];
+  svals[pos_s ? static_cast<i64>(g.w) : e] = s;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256)
     k_svals(const int2* __restrict__ edges, Coords<D> X, i64 ne, const double* __restrict__ navs,
@@ -784,8 +831,7 @@ int launch_navs(dm_ctx* c, int variant) {
             static_cast<i64>(tiles), static_cast<i64>(nsm) * std::max(per_sm, 1)));
         DM_LAUNCH(c, kern, grid, kEB, smem, c->eperm.p, c->rcodes.p, c->tnodes.p,
                   c->ring_meta.p, c->mxy.p, c->mz.p, X, ne, static_cast<int>(tiles),
-                  c->vol_by_rank, c->bedge_p.p, c->bnd.p,
-                  c->navs.p, c->svals.p);
+                  c->vol_by_rank, c->navs.p, c->svals.p);
         return DM_OK;
       };
       int st = DM_OK;
@@ -795,11 +841,27 @@ int launch_navs(dm_ctx* c, int variant) {
         case 9: st = launch(k_navs_ring_pipe<256, 3>, sizeof(PipeSmem<256>)); break;
         case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
         case 20: st = launch(k_navs_ring_pipe<512, 3, 1, 1>, sizeof(PipeSmem<512>)); break;
-        default: st = launch(k_navs_ring_pipe<512, 3>, sizeof(PipeSmem<512>)); break;
+        case 11: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
+        case 12: st = launch(k_navs_ring_pipe<256, 4>, sizeof(PipeSmem<256>)); break;
+        case 13: st = launch(k_navs_ring_pipe<512, 3>, sizeof(PipeSmem<512>)); break;
+        default:  // smallest table that holds every tile
+          st = c->ring_max_nodes <= 256 ? launch(k_navs_ring_pipe<256, 4>, sizeof(PipeSmem<256>))
+                                        : launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>));
+          break;
       }
       if (st) return st;
     }
     tmark(c, 1);
+    if constexpr (D == 3) {
+      if (c->n_bedge > 0) {
+        DM_CK(c, c->bterms.ensure(static_cast<size_t>(3 * c->nB)));
+        DM_LAUNCH(c, k_facet_terms, grid_for(c->nB, 256), 256, 0, X, c->bnd.p, c->nB,
+                  c->bterms.p);
+        DM_LAUNCH(c, k_ring_boundary, grid_for(c->n_bseg, 256), 256, 0, c->bseg.p,
+                  c->bseg_start.p, c->n_bseg, c->bedge_p.p, X, c->bterms.p, c->vol_by_rank,
+                  c->navs.p, c->svals.p);
+      }
+    }
     tmark(c, 2);
   } else if (variant == DM_VARIANT_GATHER_FACES || !c->table_ok || ALGO != kDualFree) {
     // face-list gather: traditional algorithm, meshes with node degree > 32

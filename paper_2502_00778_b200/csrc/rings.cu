@@ -388,6 +388,26 @@ __global__ void k_locality(const int32_t* __restrict__ rank, i64 nv, u32* __rest
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(cnt, static_cast<u32>(__popc(b)));
 }
 
+// boundary-edge segments of the sorted position-keyed facet list
+__global__ void k_bseg_flag(const u64* __restrict__ b, i64 n, u32* __restrict__ flag) {
+  const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < n) flag[q] = (q == 0 || (b[q] >> 32) != (b[q - 1] >> 32)) ? 1u : 0u;
+}
+
+__global__ void k_bseg_fill(const u64* __restrict__ b, i64 n, const u32* __restrict__ idx,
+                            const int32_t* __restrict__ eperm, const int2* __restrict__ edges,
+                            int4* __restrict__ seg, u32* __restrict__ start) {
+  const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  if (q == n - 1) start[idx[n]] = static_cast<u32>(n);
+  if (idx[q + 1] == idx[q]) return;  // not a segment start
+  const int p = static_cast<int>(b[q] >> 32);
+  const int e = eperm[p];
+  const int2 jk = edges[e];
+  seg[idx[q]] = make_int4(e, jk.x, jk.y, p);
+  start[idx[q]] = static_cast<u32>(q);
+}
+
 __global__ void k_bkey(const u64* __restrict__ bedge, i64 n, const int32_t* __restrict__ pinv,
                        u64* __restrict__ out) {
   const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -518,6 +538,22 @@ int build_edge_order(dm_ctx* c) {
   }
   DM_LAUNCH(c, k_tile_bptr, grid_for(ntiles + 1, 256), 256, 0, c->bedge_p.p,
             static_cast<u32>(nb), ne, ntiles, c->tile_bptr_p.p);
+  c->n_bseg = 0;
+  if (nb > 0) {
+    DevBuf<u32> idx;
+    DM_CK(c, idx.ensure(nb + 1));
+    DM_LAUNCH(c, k_bseg_flag, grid_for(nb, 256), 256, 0, c->bedge_p.p, nb, idx.p);
+    st = scan_exclusive(c, idx.p, idx.p, nb);
+    if (st) return st;
+    u32 ns = 0;
+    DM_CK(c, cudaMemcpyAsync(&ns, idx.p + nb, sizeof(u32), cudaMemcpyDeviceToHost, c->stream));
+    DM_CK(c, cudaStreamSynchronize(c->stream));
+    DM_CK(c, c->bseg.ensure(ns));
+    DM_CK(c, c->bseg_start.ensure(ns + 1));
+    DM_LAUNCH(c, k_bseg_fill, grid_for(nb, 256), 256, 0, c->bedge_p.p, nb, idx.p, c->eperm.p,
+              c->edges.p, c->bseg.p, c->bseg_start.p);
+    c->n_bseg = ns;
+  }
   DM_CK(c, cudaStreamSynchronize(c->stream));  // scratch buffers die here
   return DM_OK;
 }
