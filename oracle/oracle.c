@@ -456,3 +456,180 @@ double or_max_element_volume(int dim, const double* x, const int32_t* el, int64_
   }
   return m;
 }
+
+/* ---- multi-threaded form (bench reference arm) --------------------------- */
+/* The serial loops above accumulate, for every edge, its element terms in
+ * ascending element id and then its facet terms in ascending facet id, and
+ * for every node its edge terms in ascending edge id (incoming edges first,
+ * as they precede the node's own row).  The gathers below visit exactly those
+ * terms in exactly that order -- one edge (node) per task -- so they produce
+ * the same bits on any number of threads. */
+#include <pthread.h>
+
+struct or_plan {
+  int dim;
+  int64_t n_nodes, n_elements, n_edges;
+  const int32_t *el, *bnd, *edges;
+  int32_t *inc_ptr, *inc;  /* edge -> elements (ascending) */
+  int32_t *bptr, *blist;   /* edge -> boundary facets (ascending) */
+  int32_t *in_ptr, *in_list; /* node -> incoming edges (ascending) */
+  uint64_t* os;
+};
+
+or_plan* or_plan_create(int dim, int64_t n_nodes, const int32_t* el, int64_t n_elements,
+                        const int32_t* bnd, int64_t n_boundary, const int32_t* edges,
+                        const uint64_t* os, int64_t n_edges) {
+  or_plan* p = (or_plan*)calloc(1, sizeof(or_plan));
+  if (!p) return NULL;
+  const int L = dim == 2 ? 3 : 6, nbe = dim == 2 ? 1 : 3;
+  p->dim = dim;
+  p->n_nodes = n_nodes;
+  p->n_elements = n_elements;
+  p->n_edges = n_edges;
+  p->el = el;
+  p->bnd = bnd;
+  p->edges = edges;
+  p->inc_ptr = (int32_t*)malloc((size_t)(n_edges + 1) * sizeof(int32_t));
+  p->inc = (int32_t*)malloc((size_t)(L * n_elements + 1) * sizeof(int32_t));
+  p->bptr = (int32_t*)calloc((size_t)(n_edges + 1), sizeof(int32_t));
+  p->blist = (int32_t*)malloc((size_t)(nbe * n_boundary + 1) * sizeof(int32_t));
+  p->in_ptr = (int32_t*)calloc((size_t)(n_nodes + 1), sizeof(int32_t));
+  p->in_list = (int32_t*)malloc((size_t)(n_edges + 1) * sizeof(int32_t));
+  p->os = (uint64_t*)malloc((size_t)(n_nodes + 1) * sizeof(uint64_t));
+  int32_t* fill = (int32_t*)malloc((size_t)(n_nodes + n_edges + 2) * sizeof(int32_t));
+  if (!p->inc_ptr || !p->inc || !p->bptr || !p->blist || !p->in_ptr || !p->in_list || !p->os ||
+      !fill || or_edge_maps(dim, n_nodes, el, n_elements, edges, os, n_edges, NULL, p->inc_ptr,
+                            p->inc)) {
+    free(fill);
+    or_plan_free(p);
+    return NULL;
+  }
+  memcpy(p->os, os, (size_t)(n_nodes + 1) * sizeof(uint64_t));
+  for (int64_t b = 0; b < n_boundary; ++b)
+    for (int t = 0; t < nbe; ++t) {
+      const int32_t* bl = bnd + dim * b;
+      int32_t id = or_edge_of(edges, os, n_nodes, bl[t], bl[(t + 1) % dim]);
+      if (id < 0) {
+        free(fill);
+        or_plan_free(p);
+        return NULL;
+      }
+      p->bptr[id + 1]++;
+    }
+  for (int64_t e = 0; e < n_edges; ++e) p->bptr[e + 1] += p->bptr[e];
+  memcpy(fill, p->bptr, (size_t)(n_edges + 1) * sizeof(int32_t));
+  for (int64_t b = 0; b < n_boundary; ++b)
+    for (int t = 0; t < nbe; ++t) {
+      const int32_t* bl = bnd + dim * b;
+      int32_t id = or_edge_of(edges, os, n_nodes, bl[t], bl[(t + 1) % dim]);
+      p->blist[fill[id]++] = (int32_t)b;
+    }
+  for (int64_t e = 0; e < n_edges; ++e) p->in_ptr[edges[2 * e + 1] + 1]++;
+  for (int64_t v = 0; v < n_nodes; ++v) p->in_ptr[v + 1] += p->in_ptr[v];
+  memcpy(fill, p->in_ptr, (size_t)(n_nodes + 1) * sizeof(int32_t));
+  for (int64_t e = 0; e < n_edges; ++e) p->in_list[fill[edges[2 * e + 1]]++] = (int32_t)e;
+  free(fill);
+  return p;
+}
+
+void or_plan_free(or_plan* p) {
+  if (!p) return;
+  free(p->inc_ptr);
+  free(p->inc);
+  free(p->bptr);
+  free(p->blist);
+  free(p->in_ptr);
+  free(p->in_list);
+  free(p->os);
+  free(p);
+}
+
+typedef struct {
+  const or_plan* p;
+  const double* x;
+  double *navs, *s, *V;
+  int64_t lo, hi;
+  int phase;
+} mt_task;
+
+static void mt_edges(const or_plan* p, const double* x, double* navs, double* sv, int64_t lo,
+                     int64_t hi) {
+  const int dim = p->dim, npe = dim + 1;
+  const double fb = 1.0 / (double)(dim * (dim + 1));
+  for (int64_t e = lo; e < hi; ++e) {
+    const int32_t j = p->edges[2 * e], k = p->edges[2 * e + 1];
+    double n[3] = {0.0, 0.0, 0.0};
+    for (int32_t q = p->inc_ptr[e]; q < p->inc_ptr[e + 1]; ++q) {
+      const int32_t* t = p->el + (int64_t)npe * p->inc[q];
+      int ij = 0;
+      while (t[ij] != j) ++ij;
+      if (dim == 3) {
+        const int* f = kOppFace[ij];
+        const double *p0 = x + 3 * (int64_t)t[f[0]], *p1 = x + 3 * (int64_t)t[f[1]],
+                     *p2 = x + 3 * (int64_t)t[f[2]];
+        double d1[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+        double d2[3] = {p2[0] - p0[0], p2[1] - p0[1], p2[2] - p0[2]};
+        double c[3];
+        cross3(d1, d2, c);
+        n[0] += c[0];
+        n[1] += c[1];
+        n[2] += c[2];
+      } else {
+        double nj[3];
+        or_opposite_face_normal(2, x, t, ij, nj);
+        n[0] += (1.0 / 3.0) * nj[0];
+        n[1] += (1.0 / 3.0) * nj[1];
+      }
+    }
+    if (dim == 3) {
+      n[0] *= (1.0 / 12.0);
+      n[1] *= (1.0 / 12.0);
+      n[2] *= (1.0 / 12.0);
+    }
+    for (int32_t q = p->bptr[e]; q < p->bptr[e + 1]; ++q) {
+      double nb[3];
+      or_boundary_normal(dim, x, p->bnd + (int64_t)dim * p->blist[q], nb);
+      for (int d = 0; d < dim; ++d) n[d] += fb * nb[d];
+    }
+    for (int d = 0; d < dim; ++d) navs[(int64_t)dim * e + d] = n[d];
+    const double *xj = x + (int64_t)dim * j, *xk = x + (int64_t)dim * k;
+    double s = (xk[0] - xj[0]) * n[0] + (xk[1] - xj[1]) * n[1];
+    if (dim == 3) s = s + (xk[2] - xj[2]) * n[2];
+    sv[e] = s;
+  }
+}
+
+static void mt_nodes(const or_plan* p, const double* sv, double* V, int64_t lo, int64_t hi) {
+  const double f = 1.0 / (double)(2 * p->dim);
+  for (int64_t v = lo; v < hi; ++v) {
+    double acc = 0.0;
+    for (int32_t q = p->in_ptr[v]; q < p->in_ptr[v + 1]; ++q) acc += sv[p->in_list[q]];
+    for (uint64_t e = p->os[v]; e < p->os[v + 1]; ++e) acc += sv[e];
+    V[v] = acc * f;
+  }
+}
+
+static void* mt_run(void* arg) {
+  mt_task* t = (mt_task*)arg;
+  if (t->phase == 0) mt_edges(t->p, t->x, t->navs, t->s, t->lo, t->hi);
+  else mt_nodes(t->p, t->s, t->V, t->lo, t->hi);
+  return NULL;
+}
+
+int or_metrics_mt(const or_plan* p, const double* x, int nthreads, double* navs, double* s,
+                  double* V) {
+  if (!p || nthreads < 1) return -1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  mt_task tk[256];
+  for (int phase = 0; phase < 2; ++phase) {
+    const int64_t n = phase == 0 ? p->n_edges : p->n_nodes;
+    for (int i = 0; i < nthreads; ++i) {
+      tk[i] = (mt_task){p, x, navs, s, V, n * i / nthreads, n * (i + 1) / nthreads, phase};
+      if (i > 0 && pthread_create(&th[i], NULL, mt_run, &tk[i])) return -2;
+    }
+    mt_run(&tk[0]);
+    for (int i = 1; i < nthreads; ++i) pthread_join(th[i], NULL);
+  }
+  return 0;
+}

@@ -71,6 +71,18 @@ double or_max_face_area(int dim, const double* x, const int32_t* elements, int64
 double or_max_element_volume(int dim, const double* x, const int32_t* elements,
                              int64_t n_elements);
 
+/* Multi-threaded dual-free navs + edge volumes (bench reference arm): per-edge
+ * and per-node gathers in the serial loops' summation order (same bits on any
+ * thread count).  The plan holds the incidence / boundary / incoming lists
+ * (topology only); s receives the per-edge volume terms. */
+typedef struct or_plan or_plan;
+or_plan* or_plan_create(int dim, int64_t n_nodes, const int32_t* elements, int64_t n_elements,
+                        const int32_t* boundary, int64_t n_boundary, const int32_t* edges,
+                        const uint64_t* origin_start, int64_t n_edges);
+void or_plan_free(or_plan* plan);
+int or_metrics_mt(const or_plan* plan, const double* x, int nthreads, double* navs, double* s,
+                  double* volumes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,9 @@ class Oracle:
             "or_check_total_volume": (C.c_int, [C.c_int, DP, i64, I32P, i64, DP, DP, DP, DP]),
             "or_max_face_area": (C.c_double, [C.c_int, DP, I32P, i64]),
             "or_max_element_volume": (C.c_double, [C.c_int, DP, I32P, i64]),
+            "or_plan_create": (P, [C.c_int, i64, I32P, i64, I32P, i64, I32P, U64P, i64]),
+            "or_plan_free": (None, [P]),
+            "or_metrics_mt": (C.c_int, [P, DP, C.c_int, DP, DP, DP]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -86,6 +89,34 @@ class Oracle:
         if st:
             raise RuntimeError(f"or_edge_maps: {st}")
         return e2l, ip, inc
+
+    # multi-threaded dual-free navs + edge volumes (same bits as the serial pair)
+    def plan(self, mesh, edges, os_):
+        """Topology lists for metrics_mt; keeps references to the arrays it reads."""
+        el, bd = mesh.elements, mesh.boundary if mesh.boundary.size else np.zeros(1, np.int32)
+        h = self.L.or_plan_create(mesh.dim, mesh.num_nodes(), _p(el, C.c_int32),
+                                  mesh.num_elements(), _p(bd, C.c_int32), mesh.num_boundary(),
+                                  _p(edges, C.c_int32), _p(os_, C.c_uint64), edges.shape[0])
+        if not h:
+            raise MemoryError("or_plan_create")
+        return {"h": h, "keep": (el, bd, edges, os_), "dim": mesh.dim, "ne": edges.shape[0],
+                "nv": mesh.num_nodes()}
+
+    def plan_free(self, plan):
+        if plan.get("h"):
+            self.L.or_plan_free(plan["h"])
+            plan["h"] = None
+
+    def metrics_mt(self, plan, coords, nthreads, out=None):
+        if out is None:
+            out = (np.empty(plan["dim"] * plan["ne"]), np.empty(max(plan["ne"], 1)),
+                   np.empty(plan["nv"]))
+        navs, s, V = out
+        st = self.L.or_metrics_mt(plan["h"], _p(coords, C.c_double), nthreads,
+                                  _p(navs, C.c_double), _p(s, C.c_double), _p(V, C.c_double))
+        if st:
+            raise RuntimeError(f"or_metrics_mt: {st}")
+        return navs, V
 
     # metrics ---------------------------------------------------------------
     def navs_dualfree(self, mesh, edges, os_, e2l=None):
