@@ -190,3 +190,26 @@ def test_edge_of_and_helpers(engine, oracle):
     want_mask = np.zeros(m.num_nodes(), bool)
     want_mask[m.boundary] = True
     np.testing.assert_array_equal(mask, want_mask)
+
+
+@pytest.mark.parametrize("name,scale,order", [("C2", 1, "node"), ("C3", 2, "morton"),
+                                              ("C5", 4, "node")])
+def test_ring_path_volume_orders_bitwise(engine, oracle, name, scale, order):
+    """The ring path's s_e (edge order, or Morton position order for node
+    numberings without locality) feeds the edge-volume fold in the serial
+    order: the volumes equal the oracle's volumes of the GPU navs bit for bit;
+    a navs row put back by the caller takes the edge-order path."""
+    m = meshgen.baseline_config(name, scale)
+    engine.set_mesh(m)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    info = engine.plan_info()
+    assert info["ring_ok"] and info["volume_order"] == order
+    nf = engine.get_navs()
+    engine.volumes(EDGE)
+    e, _ = oracle.build_edges(m)
+    np.testing.assert_array_equal(engine.get_volumes(), oracle.volumes_edge(m, e, nf))
+    nput = nf * 0.5
+    engine.put_navs(nput)
+    engine.volumes(EDGE)
+    np.testing.assert_array_equal(engine.get_volumes(), oracle.volumes_edge(m, e, nput))
