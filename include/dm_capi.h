@@ -115,6 +115,12 @@ int dm_metrics_host(dm_ctx* ctx, const double* coords, int nav_algo, int variant
 
 /* Verification on the resident navs / volumes. */
 int dm_check_closure(dm_ctx* ctx, double* residual, double* interior_residual);
+/* SPEC.md:265-274 check_linear_exactness: affine flux F(x) = A x + b (A row-major
+ * dim x dim, host).  trace(A) != 0: max over interior nodes of
+ * |Res_j / V_j - trace(A)| / |trace(A)| (needs navs and volumes); A == 0:
+ * constant flux, max_j |Res_j| / max_e |phi_e| after the boundary closure.
+ * trace(A) == 0 with A != 0 -> DM_ERR_INVALID_ARG. */
+int dm_check_linear_exactness(dm_ctx* ctx, const double* A, const double* b, double* residual);
 int dm_check_total_volume(dm_ctx* ctx, double* rel_err, double* sum_volumes,
                           double* sum_elements);
 /* SPEC.md:455,482 hidden test hook: add delta to every component of one nav. */

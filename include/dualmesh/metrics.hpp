@@ -60,6 +60,14 @@ double check_closure(const Mesh& mesh, const EdgeList& edges, const LumpedNavFie
 // |sum V_j - sum V_E| / sum V_E, compensated sums.
 double check_total_volume(const Mesh& mesh, const DualVolumeField& volumes);
 
+// affine flux F(x) = A x + b (A row-major D x D).  Relative
+// interior residual of Res_j / V_j against trace(A); constant flux (A == 0)
+// checks the balance with the boundary closure.  trace(A) == 0 with A != 0
+// throws std::invalid_argument.
+double check_linear_exactness(const Mesh& mesh, const EdgeList& edges,
+                              const LumpedNavField& navs, const DualVolumeField& volumes,
+                              const std::vector<double>& A, const std::vector<double>& b);
+
 }  // namespace dualmesh
 
 #endif  // DUALMESH_METRICS_HPP

@@ -407,6 +407,68 @@ int or_check_closure(int dim, const double* x, int64_t n_nodes, const int32_t* b
   return 0;
 }
 
+int or_check_linear_exactness(int dim, const double* x, int64_t n_nodes, const int32_t* bnd,
+                              int64_t n_boundary, const int32_t* edges, int64_t n_edges,
+                              const double* navs, const double* V, const double* A,
+                              const double* b, double* residual) {
+  /* SPEC.md:265-274 (check_linear_exactness): F(x) = A x + b, arithmetic-average
+   * edge flux phi = ((F_j + F_k) * 0.5) . n_jk; Res_j += phi, Res_k -= phi.
+   * trace(A) != 0: max over interior nodes of |Res_j / V_j - tr| / |tr|.
+   * A == 0: constant flux, boundary closure b . (1/D) n_B added at every node
+   * of every boundary element, max_j |Res_j| / max_e |phi_e|. */
+  int zero = 1;
+  double tr = 0.0;
+  for (int i = 0; i < dim * dim; ++i) zero &= A[i] == 0.0;
+  for (int i = 0; i < dim; ++i) tr += A[i * dim + i];
+  if (!zero && tr == 0.0) return -1;
+  double* res = (double*)calloc((size_t)n_nodes + 1, sizeof(double));
+  unsigned char* isb = (unsigned char*)calloc((size_t)n_nodes + 1, 1);
+  if (!res || !isb) return -2;
+  double pmax = 0.0;
+  for (int64_t e = 0; e < n_edges; ++e) {
+    const int32_t j = edges[2 * e], k = edges[2 * e + 1];
+    const double *xj = x + (int64_t)dim * j, *xk = x + (int64_t)dim * k;
+    const double* n = navs + (int64_t)dim * e;
+    double phi = 0.0;
+    for (int r = 0; r < dim; ++r) {
+      double fj = b[r], fk = b[r];
+      for (int c = 0; c < dim; ++c) {
+        fj += A[r * dim + c] * xj[c];
+        fk += A[r * dim + c] * xk[c];
+      }
+      phi += ((fj + fk) * 0.5) * n[r];
+    }
+    res[j] += phi;
+    res[k] -= phi;
+    if (fabs(phi) > pmax) pmax = fabs(phi);
+  }
+  double out = 0.0;
+  if (zero) {
+    const double f = 1.0 / (double)dim;
+    for (int64_t q = 0; q < n_boundary; ++q) {
+      double nb[3];
+      or_boundary_normal(dim, x, bnd + dim * q, nb);
+      double bn = 0.0;
+      for (int d = 0; d < dim; ++d) bn += b[d] * nb[d];
+      for (int t = 0; t < dim; ++t) res[bnd[dim * q + t]] += f * bn;
+    }
+    for (int64_t v = 0; v < n_nodes; ++v)
+      if (fabs(res[v]) > out) out = fabs(res[v]);
+    out = pmax > 0.0 ? out / pmax : out;
+  } else {
+    for (int64_t t = 0; t < dim * n_boundary; ++t) isb[bnd[t]] = 1;
+    for (int64_t v = 0; v < n_nodes; ++v)
+      if (!isb[v]) {
+        const double r = fabs(res[v] / V[v] - tr) / fabs(tr);
+        if (r > out) out = r;
+      }
+  }
+  *residual = out;
+  free(res);
+  free(isb);
+  return 0;
+}
+
 /* Neumaier summation. */
 typedef struct {
   double s, c;

@@ -63,6 +63,12 @@ int or_volumes_element(int dim, const double* x, int64_t n_nodes, const int32_t*
 int or_check_closure(int dim, const double* x, int64_t n_nodes, const int32_t* boundary,
                      int64_t n_boundary, const int32_t* edges, int64_t n_edges,
                      const double* navs, double* residual, double* interior_residual);
+/* affine flux F(x) = A x + b (A row-major D x D).  Returns -1
+ * if trace(A) == 0 with A != 0.  See oracle.c for the residual definition. */
+int or_check_linear_exactness(int dim, const double* x, int64_t n_nodes, const int32_t* boundary,
+                              int64_t n_boundary, const int32_t* edges, int64_t n_edges,
+                              const double* navs, const double* volumes, const double* A,
+                              const double* b, double* residual);
 /* Neumaier-compensated sums; returns |sV - sE| / sE in *rel. */
 int or_check_total_volume(int dim, const double* x, int64_t n_nodes, const int32_t* elements,
                           int64_t n_elements, const double* volumes, double* rel,

@@ -55,6 +55,8 @@ class Oracle:
             "or_check_total_volume": (C.c_int, [C.c_int, DP, i64, I32P, i64, DP, DP, DP, DP]),
             "or_max_face_area": (C.c_double, [C.c_int, DP, I32P, i64]),
             "or_max_element_volume": (C.c_double, [C.c_int, DP, I32P, i64]),
+            "or_check_linear_exactness": (C.c_int, [C.c_int, DP, i64, I32P, i64, I32P, i64, DP,
+                                                     DP, DP, DP, DP]),
             "or_plan_create": (P, [C.c_int, i64, I32P, i64, I32P, i64, I32P, U64P, i64]),
             "or_plan_free": (None, [P]),
             "or_metrics_mt": (C.c_int, [P, DP, C.c_int, DP, DP, DP]),
@@ -162,6 +164,21 @@ class Oracle:
                                 _p(edges, C.c_int32), edges.shape[0], _p(navs, C.c_double),
                                 C.byref(r), C.byref(ri))
         return r.value, ri.value
+
+    def check_linear_exactness(self, mesh, edges, navs, vols, A, b):
+        A = np.ascontiguousarray(A, np.float64).ravel()
+        b = np.ascontiguousarray(b, np.float64).ravel()
+        r = C.c_double()
+        bd = mesh.boundary if mesh.boundary.size else np.zeros(1, np.int32)
+        st = self.L.or_check_linear_exactness(
+            mesh.dim, _p(mesh.coords, C.c_double), mesh.num_nodes(), _p(bd, C.c_int32),
+            mesh.num_boundary(), _p(edges, C.c_int32), edges.shape[0], _p(navs, C.c_double),
+            _p(vols, C.c_double), _p(A, C.c_double), _p(b, C.c_double), C.byref(r))
+        if st == -1:
+            raise ValueError("trace(A) = 0: relative residual undefined")
+        if st:
+            raise MemoryError("or_check_linear_exactness")
+        return r.value
 
     def check_total_volume(self, mesh, vols):
         r, sv, se = C.c_double(), C.c_double(), C.c_double()

@@ -320,6 +320,20 @@ double check_closure(const Mesh& mesh, const EdgeList& edges, const LumpedNavFie
   return r;
 }
 
+double check_linear_exactness(const Mesh& mesh, const EdgeList& edges,
+                              const LumpedNavField& navs, const DualVolumeField& volumes,
+                              const std::vector<double>& A, const std::vector<double>& b) {
+  const size_t D = static_cast<size_t>(mesh.dim);
+  if (A.size() != D * D || b.size() != D) throw std::invalid_argument("flux/mesh mismatch");
+  if (volumes.size() != mesh.num_nodes()) throw std::invalid_argument("field/mesh mismatch");
+  dm_ctx* c = upload_with_edges(mesh, edges);
+  put_navs(c, mesh, edges, navs);
+  check(c, dm_put_volumes(c, volumes.volumes.data()), "dm_put_volumes");
+  double r = 0.0;
+  check(c, dm_check_linear_exactness(c, A.data(), b.data(), &r), "dm_check_linear_exactness");
+  return r;
+}
+
 double check_total_volume(const Mesh& mesh, const DualVolumeField& volumes) {
   if (volumes.size() != mesh.num_nodes()) throw std::invalid_argument("field/mesh mismatch");
   dm_ctx* c = upload(mesh);

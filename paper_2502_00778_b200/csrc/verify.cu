@@ -2,6 +2,7 @@
 //
 //   closure      SPEC.md:245-253 / PAPER.md:399-424
 //   total volume SPEC.md:255-263 / PAPER.md:§4.3, double-double block sums
+//   linear exactness SPEC.md:265-274 (affine flux, average edge flux)
 //   max_face_area, max_element_volume, total_volume, boundary_node_mask
 //                ref mesh.cpp:325-349
 #include <cmath>
@@ -72,6 +73,91 @@ __global__ void k_closure_bnd(const int32_t* __restrict__ bnd, Coords<D> X, i64 
     const i64 v = bnd[D * b + t];
     for (int d = 0; d < D; ++d) atomicAdd(a + D * v + d, f * n[d]);
   }
+}
+
+// ---- linear exactness
+struct Affine {
+  double A[9], b[3], tr;
+  int zero;
+};
+
+// phi_e = ((F_j + F_k) * 0.5) . n_e with F(x) = A x + b, in the oracle's
+// operation order; max |phi| into mx.
+template <int D>
+__global__ void k_lin_phi(const int2* __restrict__ edges, Coords<D> X,
+                          const double* __restrict__ navs, i64 ne, Affine F,
+                          double* __restrict__ phi, u64* __restrict__ mx) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double ap = 0.0;
+  if (e < ne) {
+    const int2 jk = edges[e];
+    double xj[3], xk[3];
+    if constexpr (D == 3) {
+      const d4 a = X[jk.x], c = X[jk.y];
+      xj[0] = a.x; xj[1] = a.y; xj[2] = a.z;
+      xk[0] = c.x; xk[1] = c.y; xk[2] = c.z;
+    } else {
+      const double2 a = X[jk.x], c = X[jk.y];
+      xj[0] = a.x; xj[1] = a.y; xj[2] = 0.0;
+      xk[0] = c.x; xk[1] = c.y; xk[2] = 0.0;
+    }
+    double p = 0.0;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double fj = F.b[r], fk = F.b[r];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        fj += F.A[r * D + c] * xj[c];
+        fk += F.A[r * D + c] * xk[c];
+      }
+      p += ((fj + fk) * 0.5) * navs[D * e + r];
+    }
+    phi[e] = p;
+    ap = fabs(p);
+  }
+  for (int o = 16; o > 0; o >>= 1) ap = fmax(ap, __shfl_xor_sync(0xffffffffu, ap, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(mx, ap);
+}
+
+// Res_v = -sum_in phi + sum_out phi (the serial edge loop's order per node);
+// affine flux: max over interior nodes of |Res/V - tr| / |tr| into mx[1];
+// constant flux: Res kept for the boundary closure.
+__global__ void k_lin_nodes(const u32* __restrict__ in_ptr, const int32_t* __restrict__ in_list,
+                            const u32* __restrict__ os, const double* __restrict__ phi,
+                            const double* __restrict__ V, const uint8_t* __restrict__ bmask,
+                            i64 nv, Affine F, double* __restrict__ res, u64* __restrict__ mx) {
+  const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double r = 0.0;
+  if (v < nv) {
+    double acc = 0.0;
+    for (u32 q = in_ptr[v]; q < in_ptr[v + 1]; ++q) acc -= phi[in_list[q]];
+    for (u32 q = os[v]; q < os[v + 1]; ++q) acc += phi[q];
+    if (F.zero) res[v] = acc;
+    else if (!bmask[v]) r = fabs(acc / V[v] - F.tr) / fabs(F.tr);
+  }
+  for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(mx + 1, r);
+}
+
+template <int D>
+__global__ void k_lin_bnd(const int32_t* __restrict__ bnd, Coords<D> X, i64 nB, Affine F,
+                          double* __restrict__ res) {
+  const i64 q = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nB) return;
+  double n[3] = {0.0, 0.0, 0.0};
+  if constexpr (D == 3) bnormal3(X, bnd + 3 * q, n[0], n[1], n[2]);
+  else bnormal2(X, bnd + 2 * q, n[0], n[1]);
+  double bn = 0.0;
+  for (int d = 0; d < D; ++d) bn += F.b[d] * n[d];
+  const double f = 1.0 / static_cast<double>(D);
+  for (int t = 0; t < D; ++t) atomicAdd(res + bnd[D * q + t], f * bn);
+}
+
+__global__ void k_abs_max(const double* __restrict__ x, i64 n, u64* __restrict__ mx) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double r = i < n ? fabs(x[i]) : 0.0;
+  for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(mx, r);
 }
 
 template <int D>
@@ -268,6 +354,67 @@ extern "C" int dm_check_closure(dm_ctx* c, double* residual, double* interior_re
   std::memcpy(&rall, &h[2], 8);
   *residual = nmax > 0.0 ? rall / nmax : rall;
   if (interior_residual) *interior_residual = nmax > 0.0 ? rint / nmax : rint;
+  return DM_OK;
+}
+
+extern "C" int dm_check_linear_exactness(dm_ctx* c, const double* A, const double* b,
+                                         double* residual) {
+  if (!c || !A || !b || !residual) return DM_ERR_INVALID_ARG;
+  if (!c->have_navs) return fail(c, DM_ERR_STATE, "exactness check needs navs");
+  const int D = c->dim;
+  Affine F{};
+  F.zero = 1;
+  for (int i = 0; i < D * D; ++i) {
+    F.A[i] = A[i];
+    F.zero &= A[i] == 0.0;
+  }
+  for (int i = 0; i < D; ++i) {
+    F.b[i] = b[i];
+    F.tr += A[i * D + i];
+  }
+  if (!F.zero && F.tr == 0.0)
+    return fail(c, DM_ERR_INVALID_ARG, "trace(A) = 0: relative residual undefined");
+  if (!F.zero && !c->have_vols) return fail(c, DM_ERR_STATE, "exactness check needs volumes");
+  int st = ensure_incoming(c);
+  if (st) return st;
+  const i64 nv = c->nv, ne = c->ne;
+  DevBuf<uint8_t> mask;
+  DevBuf<double> phi;
+  DM_CK(c, mask.ensure(static_cast<size_t>(nv)));
+  DM_CK(c, phi.ensure(static_cast<size_t>(ne)));
+  DM_CK(c, c->red.ensure(static_cast<size_t>(D * nv)));
+  DM_CK(c, c->redu.ensure(4));
+  DM_CK(c, cudaMemsetAsync(mask.p, 0, nv, c->stream));
+  DM_CK(c, cudaMemsetAsync(c->redu.p, 0, 4 * sizeof(u64), c->stream));
+  DM_LAUNCH(c, k_bmask, grid_for(c->nB * D, 256), 256, 0, c->bnd.p, c->nB * D, mask.p);
+  if (D == 3) {
+    Coords<3> X{c->x4.p};
+    DM_LAUNCH(c, k_lin_phi<3>, grid_for(ne, 256), 256, 0, c->edges.p, X, c->navs.p, ne, F,
+              phi.p, c->redu.p);
+  } else {
+    Coords<2> X{reinterpret_cast<const double2*>(c->coords.p)};
+    DM_LAUNCH(c, k_lin_phi<2>, grid_for(ne, 256), 256, 0, c->edges.p, X, c->navs.p, ne, F,
+              phi.p, c->redu.p);
+  }
+  DM_LAUNCH(c, k_lin_nodes, grid_for(nv, 256), 256, 0, c->in_ptr.p, c->in_list.p, c->os.p, phi.p,
+            F.zero ? nullptr : c->vols.p, mask.p, nv, F, c->red.p, c->redu.p);
+  if (F.zero) {
+    if (D == 3) {
+      Coords<3> X{c->x4.p};
+      DM_LAUNCH(c, k_lin_bnd<3>, grid_for(c->nB, 256), 256, 0, c->bnd.p, X, c->nB, F, c->red.p);
+    } else {
+      Coords<2> X{reinterpret_cast<const double2*>(c->coords.p)};
+      DM_LAUNCH(c, k_lin_bnd<2>, grid_for(c->nB, 256), 256, 0, c->bnd.p, X, c->nB, F, c->red.p);
+    }
+    DM_LAUNCH(c, k_abs_max, grid_for(nv, 256), 256, 0, c->red.p, nv, c->redu.p + 1);
+  }
+  u64 h[2];
+  DM_CK(c, cudaMemcpyAsync(h, c->redu.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  double pmax, r;
+  std::memcpy(&pmax, &h[0], 8);
+  std::memcpy(&r, &h[1], 8);
+  *residual = F.zero && pmax > 0.0 ? r / pmax : r;
   return DM_OK;
 }
 

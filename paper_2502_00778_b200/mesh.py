@@ -215,6 +215,16 @@ class Engine:
                  "dm_check_total_volume")
         return r.value, sv.value, se.value
 
+    def check_linear_exactness(self, A, b) -> float:
+        """SPEC.md:265-274 (affine flux A x + b; constant flux when A == 0)."""
+        A = np.ascontiguousarray(A, np.float64).ravel()
+        b = np.ascontiguousarray(b, np.float64).ravel()
+        r = C.c_double()
+        self._ck(self._lib.dm_check_linear_exactness(self._c, ptr(A, C.c_double),
+                                                     ptr(b, C.c_double), C.byref(r)),
+                 "dm_check_linear_exactness")
+        return r.value
+
     def corrupt_nav(self, edge: int, delta: float):
         self._ck(self._lib.dm_corrupt_nav(self._c, edge, delta), "dm_corrupt_nav")
 

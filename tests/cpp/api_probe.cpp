@@ -87,6 +87,24 @@ int probe_compute_metrics(int dim, const double* x, int64_t nv, const int32_t* e
   }
 }
 
+// SPEC.md:265-274 through the C++ API: dual-free navs + edge volumes, then
+// check_linear_exactness with A (row-major) and b; -1 on invalid_argument.
+int probe_linear_exactness(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,
+                           const int32_t* b, int64_t nb, const double* A, const double* f,
+                           double* residual) {
+  try {
+    auto m = make(dim, x, nv, el, ne, b, nb);
+    auto r = dualmesh::compute_metrics(m, dualmesh::NavAlgo::dualfree, dualmesh::VolAlgo::edge);
+    std::vector<double> AA(A, A + dim * dim), ff(f, f + dim);
+    *residual = dualmesh::check_linear_exactness(m, r.edges, r.navs, r.volumes, AA, ff);
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  } catch (const std::exception&) {
+    return -2;
+  }
+}
+
 // mesh/edge mismatch must raise std::invalid_argument.
 int probe_mismatch(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne) {
   auto m = make(dim, x, nv, el, ne, nullptr, 0);

@@ -32,6 +32,8 @@ def probe():
     lib.probe_compute_metrics.restype = C.c_int
     lib.probe_compute_metrics.argtypes = [C.c_int, D, I64, I32, I64, I32, I64, C.c_int, C.c_int, D,
                                           D, D, D]
+    lib.probe_linear_exactness.restype = C.c_int
+    lib.probe_linear_exactness.argtypes = [C.c_int, D, I64, I32, I64, I32, I64, D, D, D]
     lib.probe_mismatch.restype = C.c_int
     lib.probe_mismatch.argtypes = [C.c_int, D, I64, I32, I64]
     lib.probe_element_volume.restype = C.c_double
@@ -142,3 +144,28 @@ def test_compute_metrics_facade(probe, oracle, name, scale):
     assert np.abs(vols - vw).max() <= 1e-12 * np.abs(vw).max()
     assert cl.value <= 1e-13 and tv.value <= 1e-12
     assert probe.probe_mismatch(*_a(m)) == 1  # std::invalid_argument
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 4), ("C2", 4)])
+def test_linear_exactness_cpp_api(probe, oracle, name, scale):
+    """dualmesh::check_linear_exactness (metrics.hpp) against the oracle's
+    check on the oracle's own fields (SPEC.md:265-274 bars)."""
+    m = meshgen.baseline_config(name, scale)
+    D = m.dim
+    p = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    rng = np.random.default_rng(3)
+    A = rng.uniform(-1, 1, (D, D))
+    A[0, 0] += 2.0
+    f = rng.uniform(-1, 1, D)
+    r = C.c_double()
+    assert probe.probe_linear_exactness(*_a(m), p(m.boundary, C.c_int32), m.num_boundary(),
+                                        p(np.ascontiguousarray(A), C.c_double), p(f, C.c_double),
+                                        C.byref(r)) == 0
+    e, o = oracle.build_edges(m)
+    n = oracle.navs_dualfree(m, e, o)
+    want = oracle.check_linear_exactness(m, e, n, oracle.volumes_edge(m, e, n), A, f)
+    assert r.value <= 1e-11 and want <= 1e-11
+    bad = np.diag([1.0, -1.0] + [0.0] * (D - 2))
+    assert probe.probe_linear_exactness(*_a(m), p(m.boundary, C.c_int32), m.num_boundary(),
+                                        p(np.ascontiguousarray(bad), C.c_double),
+                                        p(f, C.c_double), C.byref(r)) == -1

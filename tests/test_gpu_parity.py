@@ -213,3 +213,60 @@ def test_ring_path_volume_orders_bitwise(engine, oracle, name, scale, order):
     engine.put_navs(nput)
     engine.volumes(EDGE)
     np.testing.assert_array_equal(engine.get_volumes(), oracle.volumes_edge(m, e, nput))
+
+
+def _affine(dim, seed):
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1.0, 1.0, (dim, dim))
+    if abs(np.trace(A)) < 0.1:
+        A[0, 0] += 1.0
+    return A, rng.uniform(-1.0, 1.0, dim)
+
+
+@pytest.mark.parametrize("name,scale,tol", [("C1", 2, 1e-11), ("C2", 2, 1e-11),
+                                            ("C3", 4, 1e-11), ("C4", 4, 1e-9)])
+def test_linear_exactness_matches_oracle(engine, oracle, name, scale, tol):
+    """SPEC.md:265-274 on the GPU: with the bit-exact navs / volumes the
+    affine-flux residual equals the oracle's bit for bit; the fast path and
+    the constant-flux balance meet the SPEC tolerances."""
+    m = meshgen.baseline_config(name, scale)
+    D = m.dim
+    engine.set_mesh(m)
+    engine.build_edges()
+    engine.navs(DF, EXACT)
+    engine.volumes(EDGE)
+    e, _ = oracle.build_edges(m)
+    n, v = engine.get_navs(), engine.get_volumes()
+    A, b = _affine(D, 11)
+    for AA, bb in ((A, b), (np.eye(D) / D, np.zeros(D))):
+        g = engine.check_linear_exactness(AA, bb)
+        assert g == oracle.check_linear_exactness(m, e, n, v, AA, bb)
+        assert g <= tol
+    gc = engine.check_linear_exactness(np.zeros((D, D)), b)
+    oc = oracle.check_linear_exactness(m, e, n, v, np.zeros((D, D)), b)
+    assert gc <= 1e-13 and abs(gc - oc) <= 1e-15
+    engine.navs(DF, GATHER)
+    engine.volumes(EDGE)
+    assert engine.check_linear_exactness(A, b) <= tol
+    with pytest.raises(Exception):
+        engine.check_linear_exactness(np.diag([1.0, -1.0] + [0.0] * (D - 2)), b)
+
+
+def test_linear_exactness_full_size():
+    """C5 at full size (SPEC invariant: exactness <= 1e-11)."""
+    from paper_2502_00778_b200 import Engine
+    m = meshgen.baseline_config("C5")
+    eng = Engine(0)
+    try:
+        eng.set_mesh(m)
+        eng.build_edges()
+        eng.navs(DF, GATHER)
+        eng.volumes(EDGE)
+        A, b = _affine(3, 5)
+        assert eng.check_linear_exactness(A, b) <= 1e-11
+        assert eng.check_linear_exactness(np.eye(3) / 3, np.zeros(3)) <= 1e-11
+        assert eng.check_linear_exactness(np.zeros((3, 3)), b) <= 1e-13
+        eng.corrupt_nav(int(m.num_elements() // 3), 1e-3)
+        assert eng.check_linear_exactness(A, b) > 1e-6
+    finally:
+        eng.close()

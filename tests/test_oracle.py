@@ -222,3 +222,42 @@ def test_threaded_oracle_is_bitwise_serial(oracle, mesh_fn, threads):
         oracle.plan_free(plan)
     np.testing.assert_array_equal(nt, nd)
     np.testing.assert_array_equal(vt, ve)
+
+
+def _affine(dim, seed):
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1.0, 1.0, (dim, dim))
+    if abs(np.trace(A)) < 0.1:
+        A[0, 0] += 1.0
+    return A, rng.uniform(-1.0, 1.0, dim)
+
+
+@pytest.mark.parametrize("mesh_fn,tol", [
+    (lambda: meshgen.tri_square(32, amp=0.2, seed=42), 1e-11),   # SPEC.md:271 example 2
+    (lambda: meshgen.tet_cube(10, amp=0.15), 1e-11),
+    # BL grid (dz0 = 1e-5, z up to 53): |F||n| / (V tr) ~ 1e5, so rounding
+    # alone reaches ~1e-10 (tolerances are configuration)
+    (lambda: meshgen.baseline_config("C4", 16), 1e-9),
+])
+def test_linear_exactness_spec_examples(oracle, mesh_fn, tol):
+    """F = x/D gives Res_j/V_j = 1 at interior nodes; a seeded
+    random affine flux gives <= 1e-11; a constant flux balances to <= 1e-13
+    at all nodes with the boundary closure; trace(A) = 0 is rejected."""
+    m = mesh_fn()
+    D = m.dim
+    e, o = oracle.build_edges(m)
+    n = oracle.navs_dualfree(m, e, o)
+    v = oracle.volumes_edge(m, e, n)
+    assert oracle.check_linear_exactness(m, e, n, v, np.eye(D) / D, np.zeros(D)) <= tol
+    A, b = _affine(D, 7)
+    assert oracle.check_linear_exactness(m, e, n, v, A, b) <= tol
+    assert oracle.check_linear_exactness(m, e, n, v, np.zeros((D, D)), b) <= 1e-13
+    with pytest.raises(ValueError):
+        oracle.check_linear_exactness(m, e, n, v, np.diag([1.0, -1.0] + [0.0] * (D - 2)), b)
+    # a corrupted nav of an interior edge breaks exactness
+    isb = np.zeros(m.num_nodes(), bool)
+    isb[m.boundary] = True
+    q = int(np.nonzero(~isb[e[:, 0]] & ~isb[e[:, 1]])[0][0])
+    n2 = n.copy()
+    n2[D * q:D * q + D] += 1e-3
+    assert oracle.check_linear_exactness(m, e, n2, v, A, b) > 1e3 * tol
