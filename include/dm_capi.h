@@ -83,6 +83,20 @@ int dm_set_mesh(dm_ctx* ctx, int dim, const double* coords, int64_t n_nodes,
 int dm_set_coords(dm_ctx* ctx, const double* coords);
 int dm_set_coords_device(dm_ctx* ctx, const double* d_coords);
 
+/* Device-side SPEC meshgen: the grids of
+ * include/dm_meshgen.h generated straight into the context (bitwise the same
+ * coordinates, elements and boundary as the host generator), replacing the
+ * current mesh like dm_set_mesh.  z_nodes: host array of nz+1 values or NULL.
+ * dm_gen_permute relabels the context's mesh as dmg_permute does. */
+int dm_gen_tri_square(dm_ctx* ctx, int n, uint64_t diag_seed, double amp, uint64_t seed);
+int dm_gen_tet_box(dm_ctx* ctx, int nx, int ny, int nz, const double* z_nodes, int jitter_mode,
+                   double amp, uint64_t seed);
+int dm_gen_permute(dm_ctx* ctx, uint64_t node_seed, uint64_t elem_seed);
+/* The context's mesh back to the host (any pointer may be NULL), and its sizes. */
+int dm_get_mesh(dm_ctx* ctx, double* coords, int32_t* elements, int32_t* boundary);
+int dm_mesh_sizes(dm_ctx* ctx, int* dim, int64_t* n_nodes, int64_t* n_elements,
+                  int64_t* n_boundary);
+
 /* Edge extraction: ref build_edges, proj/src/mesh.cpp:256-285.  Also builds
  * the element-to-local-edge map e2l[e*L+l] (local order mesh.cpp:17,263-265)
  * and the edge-to-element CSR incidence (ascending element ids per edge). */

@@ -56,6 +56,12 @@ CAPI = {
     "dm_set_mesh": (C.c_int, [P, C.c_int, DP, i64, I32P, i64, I32P, i64]),
     "dm_set_coords": (C.c_int, [P, DP]),
     "dm_set_coords_device": (C.c_int, [P, P]),
+    "dm_gen_tri_square": (C.c_int, [P, C.c_int, C.c_uint64, C.c_double, C.c_uint64]),
+    "dm_gen_tet_box": (C.c_int, [P, C.c_int, C.c_int, C.c_int, DP, C.c_int, C.c_double,
+                                 C.c_uint64]),
+    "dm_gen_permute": (C.c_int, [P, C.c_uint64, C.c_uint64]),
+    "dm_get_mesh": (C.c_int, [P, DP, I32P, I32P]),
+    "dm_mesh_sizes": (C.c_int, [P, C.POINTER(C.c_int), I64P, I64P, I64P]),
     "dm_build_edges": (C.c_int, [P, I64P]),
     "dm_get_edges": (C.c_int, [P, I32P, U64P]),
     "dm_get_e2l": (C.c_int, [P, I32P]),

@@ -66,6 +66,24 @@ class Mesh:
 
 
 @dataclass
+class MeshShape:
+    """Sizes of a mesh that lives only on the device (dm_gen_*)."""
+    dim: int
+    n_nodes: int
+    n_elements: int
+    n_boundary: int
+
+    def num_nodes(self) -> int:
+        return self.n_nodes
+
+    def num_elements(self) -> int:
+        return self.n_elements
+
+    def num_boundary(self) -> int:
+        return self.n_boundary
+
+
+@dataclass
 class EdgeList:
     """ref mesh.hpp:48-56."""
     edges: np.ndarray          # (n_edges, 2) int32, (min, max), lexicographic
@@ -132,6 +150,40 @@ class Engine:
                                        mesh.num_boundary()), "dm_set_mesh")
         self.mesh = mesh
         self.n_edges = 0
+
+    # device-side meshgen (dm_gen_*): the mesh lives only on the device; the
+    # engine keeps a size-only stand-in, get_mesh() copies it back
+    def _adopt_device_mesh(self):
+        d, nv, ne, nb = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._ck(self._lib.dm_mesh_sizes(self._c, C.byref(d), C.byref(nv), C.byref(ne),
+                                         C.byref(nb)), "dm_mesh_sizes")
+        self.mesh = MeshShape(d.value, nv.value, ne.value, nb.value)
+        self.n_edges = 0
+
+    def gen_tri_square(self, n: int, diag_seed: int = 0, amp: float = 0.0, seed: int = 42):
+        self._ck(self._lib.dm_gen_tri_square(self._c, n, diag_seed, amp, seed),
+                 "dm_gen_tri_square")
+        self._adopt_device_mesh()
+
+    def gen_tet_box(self, nx: int, ny: int, nz: int, z_nodes=None, jitter_mode: int = 0,
+                    amp: float = 0.0, seed: int = 42):
+        z = None if z_nodes is None else np.ascontiguousarray(z_nodes, np.float64)
+        self._ck(self._lib.dm_gen_tet_box(self._c, nx, ny, nz, ptr(z, C.c_double), jitter_mode,
+                                          amp, seed), "dm_gen_tet_box")
+        self._adopt_device_mesh()
+
+    def gen_permute(self, node_seed: int, elem_seed: int):
+        self._ck(self._lib.dm_gen_permute(self._c, node_seed, elem_seed), "dm_gen_permute")
+        self._adopt_device_mesh()
+
+    def get_mesh(self) -> Mesh:
+        s = self.mesh
+        x = np.empty(s.dim * s.num_nodes(), np.float64)
+        el = np.empty((s.dim + 1) * s.num_elements(), np.int32)
+        bd = np.empty(s.dim * s.num_boundary(), np.int32)
+        self._ck(self._lib.dm_get_mesh(self._c, ptr(x, C.c_double), ptr(el, C.c_int32),
+                                       ptr(bd, C.c_int32)), "dm_get_mesh")
+        return Mesh(s.dim, x, el, bd)
 
     def set_coords(self, coords: np.ndarray):
         coords = np.ascontiguousarray(coords, np.float64)

@@ -101,3 +101,24 @@ def baseline_config(name: str, scale: int = 1) -> Mesh:
     if name == "C5":
         return tet_cube(256 // scale, amp=0.15)
     raise KeyError(name)
+
+
+def baseline_config_device(engine, name: str, scale: int = 1) -> None:
+    """The same grids as baseline_config, generated on the engine's device
+    (dm_gen_*, bitwise identical); the mesh stays on the GPU."""
+    if name == "C1":
+        engine.gen_tri_square(256 // scale, SEED_DIAG, 0.2, SEED_JITTER)
+    elif name == "C2":
+        engine.gen_tet_box(64 // scale, 64 // scale, 64 // scale, None, 0, 0.15, SEED_JITTER)
+    elif name == "C3":
+        n = 160 // scale
+        engine.gen_tet_box(n, n, n, None, 0, 0.15, SEED_JITTER)
+        engine.gen_permute(SEED_NODES, SEED_ELEMS)
+    elif name == "C4":
+        n, nz = 128 // scale, 256 // scale
+        engine.gen_tet_box(n, n, nz, bl_z(nz, 1e-5, 1.05), 1, 0.1, SEED_JITTER)
+    elif name == "C5":
+        n = 256 // scale
+        engine.gen_tet_box(n, n, n, None, 0, 0.15, SEED_JITTER)
+    else:
+        raise KeyError(name)
