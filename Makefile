@@ -30,7 +30,11 @@ build/host_api.o: $(CSRC)/host_api.cpp include/dualmesh/mesh.hpp include/dualmes
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(LIBDIR)/libdualmesh.so: $(CU_OBJS) build/host_api.o
+build/io.o: $(CSRC)/io.cpp include/dualmesh/io.hpp include/dualmesh/mesh.hpp include/dualmesh/metrics.hpp include/dm_capi.h
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libdualmesh.so: $(CU_OBJS) build/host_api.o build/io.o
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -o $@ $^
 

@@ -180,6 +180,27 @@ int64_t dm_kernel_launches(const dm_ctx* ctx);
  * [4] max tile node count (ring path), [5] failure flag of the ring build,
  * [6] edge-volume pass walks nodes in Morton order (1) or id order (0). */
 int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
+/* SPEC cli_io file formats, host only (no device needed).
+ * MeshFile: dm_mesh_file_read parses `path` (call with NULL arrays for the
+ * sizes first); ids come back 0-based; *has_boundary = 0 when the file has no
+ * boundary section (derive it with dm_derive_boundary).  Parse errors return
+ * DM_ERR_INVALID_ARG with "path:line: what" in err (syntax, count mismatch,
+ * invalid index).  dm_mesh_file_write writes 1-based ids and 17-significant-
+ * digit coordinates (lossless).  MetricsFile: JSON with 1-based edges, navs,
+ * volumes and provenance (algorithm names, dm_mesh_checksum = FNV-1a 64 of the
+ * mesh arrays); deterministic bytes. */
+int dm_mesh_file_read(const char* path, int* dim, int64_t* n_nodes, int64_t* n_elements,
+                      int64_t* n_boundary, int* has_boundary, double* coords, int32_t* elements,
+                      int32_t* boundary, char* err, int64_t err_len);
+int dm_mesh_file_write(const char* path, int dim, const double* coords, int64_t n_nodes,
+                       const int32_t* elements, int64_t n_elements, const int32_t* boundary,
+                       int64_t n_boundary);
+uint64_t dm_mesh_checksum(int dim, const double* coords, int64_t n_nodes, const int32_t* elements,
+                          int64_t n_elements, const int32_t* boundary, int64_t n_boundary);
+int dm_metrics_file_write(const char* path, int dim, const int32_t* edges, int64_t n_edges,
+                          const double* navs, const double* volumes, int64_t n_nodes,
+                          int nav_algo, int vol_algo, uint64_t mesh_checksum);
+
 /* Pinned host memory for end-to-end transfers. */
 int dm_host_alloc(size_t bytes, void** ptr);
 int dm_host_free(void* ptr);

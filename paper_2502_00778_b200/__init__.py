@@ -9,7 +9,7 @@ tests and the bench; the native library is ``lib/libdualmesh.so``.
 from .mesh import (DualMeshError, EdgeAbsent, EdgeList, Engine, Mesh, MeshEdgeMismatch,
                    boundary_node_mask, build_edges, default_engine, derive_boundary_faces,
                    element_volume, max_element_volume, max_face_area, total_volume)
-from . import meshgen, metrics
+from . import fileio, meshgen, metrics
 
 __all__ = [
     "DualMeshError", "EdgeAbsent", "EdgeList", "Engine", "Mesh", "MeshEdgeMismatch",

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "dualmesh/mesh.hpp"
+#include "dualmesh/io.hpp"
 #include "dualmesh/metrics.hpp"
 
 namespace {
@@ -99,6 +100,24 @@ int probe_linear_exactness(int dim, const double* x, int64_t nv, const int32_t* 
     *residual = dualmesh::check_linear_exactness(m, r.edges, r.navs, r.volumes, AA, ff);
     return 0;
   } catch (const std::invalid_argument&) {
+    return -1;
+  } catch (const std::exception&) {
+    return -2;
+  }
+}
+
+// dualmesh::read_mesh -> write_mesh, and compute_metrics -> write_metrics, through
+// the C++ API (io.hpp).  Returns the boundary count read (derived when the file
+// has no boundary section), -1 on a parse error, -2 on other errors.
+int64_t probe_io(const char* in_path, const char* mesh_out, const char* metrics_out) {
+  try {
+    auto m = dualmesh::read_mesh(in_path);
+    dualmesh::write_mesh(m, mesh_out);
+    auto r = dualmesh::compute_metrics(m, dualmesh::NavAlgo::dualfree, dualmesh::VolAlgo::edge);
+    dualmesh::write_metrics(metrics_out, m, r.edges, r.navs, r.volumes,
+                            dualmesh::NavAlgo::dualfree, dualmesh::VolAlgo::edge);
+    return static_cast<int64_t>(m.num_boundary());
+  } catch (const std::runtime_error&) {
     return -1;
   } catch (const std::exception&) {
     return -2;

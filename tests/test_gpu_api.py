@@ -34,6 +34,8 @@ def probe():
                                           D, D, D]
     lib.probe_linear_exactness.restype = C.c_int
     lib.probe_linear_exactness.argtypes = [C.c_int, D, I64, I32, I64, I32, I64, D, D, D]
+    lib.probe_io.restype = I64
+    lib.probe_io.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p]
     lib.probe_mismatch.restype = C.c_int
     lib.probe_mismatch.argtypes = [C.c_int, D, I64, I32, I64]
     lib.probe_element_volume.restype = C.c_double
@@ -169,3 +171,26 @@ def test_linear_exactness_cpp_api(probe, oracle, name, scale):
     assert probe.probe_linear_exactness(*_a(m), p(m.boundary, C.c_int32), m.num_boundary(),
                                         p(np.ascontiguousarray(bad), C.c_double),
                                         p(f, C.c_double), C.byref(r)) == -1
+
+
+def test_file_io_cpp_api(probe, tmp_path):
+    """io.hpp: read_mesh derives a missing boundary, write_mesh round-trips,
+    write_metrics writes the SPEC MetricsFile; parse errors throw."""
+    import json
+    from paper_2502_00778_b200 import fileio
+    c = meshgen.tet_cube(4, amp=0.15)
+    src = tmp_path / "in.dm"
+    fileio.write_mesh(Mesh(3, c.coords, c.elements), src)
+    src.write_text(src.read_text().replace("boundary 0\n", ""))
+    out, met = tmp_path / "out.dm", tmp_path / "m.json"
+    nb = probe.probe_io(str(src).encode(), str(out).encode(), str(met).encode())
+    assert nb == c.num_boundary()
+    r = fileio.read_mesh(out)
+    np.testing.assert_array_equal(r.coords, c.coords)
+    np.testing.assert_array_equal(r.elements, c.elements)
+    np.testing.assert_array_equal(r.boundary, RefMesh(r).derive_boundary())
+    d = json.loads(met.read_text())
+    assert d["provenance"]["mesh_checksum"] == f"fnv1a64:{fileio.mesh_checksum(r):016x}"
+    bad = tmp_path / "bad.dm"
+    bad.write_text("dualmesh v1\ndim 2\nnodes 1\n0 0\nelements 1\n1 1 2\n")
+    assert probe.probe_io(str(bad).encode(), str(out).encode(), str(met).encode()) == -1
