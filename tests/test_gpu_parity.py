@@ -270,3 +270,59 @@ def test_linear_exactness_full_size():
         assert eng.check_linear_exactness(A, b) > 1e-6
     finally:
         eng.close()
+
+
+def _fan_mesh(n):
+    """n tets around the edge (0,0,0)-(0,0,1): an edge with n > kRingMax (24)
+    incidences pushes the ring plan to its fallback."""
+    th = 2 * np.pi * np.arange(n) / n
+    ring = np.stack([np.cos(th), np.sin(th), np.full(n, 0.5)], 1)
+    x = np.concatenate([[[0, 0, 0], [0, 0, 1]], ring]).ravel()
+    el = []
+    for i in range(n):
+        t = [0, 1, 2 + i, 2 + (i + 1) % n]
+        p = x.reshape(-1, 3)[t]
+        if np.linalg.det(np.stack([p[1] - p[0], p[2] - p[0], p[3] - p[0]])) < 0:
+            t[2], t[3] = t[3], t[2]
+        el += t
+    return Mesh(3, x, np.array(el, np.int32))
+
+
+@pytest.mark.parametrize("n", [12, 30])
+def test_fan_fallback(engine, oracle, n):
+    m0 = _fan_mesh(n)
+    engine.set_mesh(m0)
+    m = Mesh(3, m0.coords, m0.elements, engine.derive_boundary())
+    engine.set_mesh(m)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    info = engine.plan_info()
+    assert info["ring_ok"] == (n <= 24)
+    e, o = oracle.build_edges(m)
+    want = oracle.navs_dualfree(m, e, o)
+    assert per_vector_rel(engine.get_navs(), want, 3) <= 1e-12
+    engine.volumes(EDGE)
+    np.testing.assert_array_equal(engine.get_volumes(), oracle.volumes_edge(m, e, engine.get_navs()))
+
+
+def test_local_order_rotations(engine, oracle):
+    """Elements stored with even permutations of their local order (still
+    positively oriented): the ring orientation bits follow the local order."""
+    m = meshgen.baseline_config("C2", 4)
+    rng = np.random.default_rng(9)
+    even = np.array([[0, 1, 2, 3], [1, 2, 0, 3], [2, 0, 1, 3], [0, 2, 3, 1], [0, 3, 1, 2],
+                     [1, 0, 3, 2], [2, 3, 0, 1], [3, 2, 1, 0], [1, 3, 2, 0], [2, 1, 3, 0],
+                     [3, 0, 2, 1], [3, 1, 0, 2]])
+    el = m.elements.reshape(-1, 4)
+    pick = even[rng.integers(0, len(even), el.shape[0])]
+    el2 = np.take_along_axis(el, pick, axis=1)
+    m2 = Mesh(3, m.coords, el2, m.boundary)
+    engine.set_mesh(m2)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    assert engine.plan_info()["ring_ok"]
+    e, o = oracle.build_edges(m2)
+    want = oracle.navs_dualfree(m2, e, o)
+    assert per_vector_rel(engine.get_navs(), want, 3) <= 1e-12
+    engine.navs(DF, EXACT)
+    np.testing.assert_array_equal(engine.get_navs(), want)
