@@ -326,3 +326,41 @@ def test_local_order_rotations(engine, oracle):
     assert per_vector_rel(engine.get_navs(), want, 3) <= 1e-12
     engine.navs(DF, EXACT)
     np.testing.assert_array_equal(engine.get_navs(), want)
+
+
+def test_isolated_nodes_and_inverted_element(engine, oracle):
+    """Unused nodes get zero volume and do not disturb the ring plan; an
+    inverted element makes a ring inconsistently oriented, which sends the
+    plan to its bit-exact fallback (results still equal the oracle)."""
+    m = meshgen.tet_cube(5, amp=0.15)
+    extra = np.array([[2.0, 2.0, 2.0], [-1.0, 0.5, 0.5]])
+    mi = Mesh(3, np.concatenate([m.coords, extra.ravel()]), m.elements, m.boundary)
+    engine.set_mesh(mi)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    assert engine.plan_info()["ring_ok"]
+    e, o = oracle.build_edges(mi)
+    want = oracle.navs_dualfree(mi, e, o)
+    assert per_vector_rel(engine.get_navs(), want, 3) <= 1e-12
+    engine.volumes(EDGE)
+    v = engine.get_volumes()
+    assert v[-1] == 0.0 and v[-2] == 0.0
+    np.testing.assert_array_equal(v, oracle.volumes_edge(mi, e, engine.get_navs()))
+    el = m.elements.reshape(-1, 4).copy()
+    el[17] = el[17][[0, 2, 1, 3]]
+    mv = Mesh(3, m.coords, el, m.boundary)
+    engine.set_mesh(mv)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    assert not engine.plan_info()["ring_ok"]
+    e, o = oracle.build_edges(mv)
+    np.testing.assert_array_equal(engine.get_navs(), oracle.navs_dualfree(mv, e, o))
+
+
+def test_empty_mesh(engine):
+    for dim in (2, 3):
+        engine.set_mesh(Mesh(dim, np.zeros(0), np.zeros(0, np.int32)))
+        assert engine.build_edges() == 0
+        engine.navs(DF, GATHER)
+        engine.volumes(EDGE)
+        assert engine.get_navs().size == 0 and engine.get_volumes().size == 0
