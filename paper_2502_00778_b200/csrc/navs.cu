@@ -572,7 +572,8 @@ __global__ void __launch_bounds__(kEB, MINB)
       // scale pass; boundary edges get their facet terms (and s) from
       // k_ring_boundary, launched right after on the same stream
       edge_tail_values<3, kDualFree>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
-      if (!(FAKE & 2) || s == -12345.0) svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
+      if (!(FAKE & 2) || s == -12345.0)
+        svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
     }
     if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) store_nav_row(navs, e, nv);
     __syncthreads();  // buffer b is refilled next iteration
