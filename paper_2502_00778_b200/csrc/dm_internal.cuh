@@ -91,7 +91,8 @@ struct dm_ctx {
   dm::i64 ring_max_nodes = 0, ring_fail = 0;
   dm::DevBuf<int32_t> tnodes;      // kTileNodeCap per tile (rings.cu)
   dm::DevBuf<dm::u32> tnode_cnt;
-  dm::DevBuf<uint16_t> rcodes;     // lane-transposed warp blocks (rings.cu)
+  dm::DevBuf<uint8_t> rcodes;      // lane-transposed warp blocks (rings.cu), bytes
+  int code_width = 2;              // 1: 8-bit slots + per-lane header, 2: 16-bit words
   dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU | nbnd << 16, bptr}, offsets
   dm::DevBuf<int32_t> eperm;       // tile position p -> edge id (Morton origin order)
   dm::DevBuf<int32_t> morder;      // Morton rank -> node id

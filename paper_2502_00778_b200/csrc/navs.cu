@@ -365,7 +365,8 @@ __global__ void __launch_bounds__(kEB, MINB)
 // The terms of an edge are summed unsigned and the edge's common orientation
 // applied once.  Tiles with more than CAP nodes or kPipeCodeCap codes are
 // evaluated straight from global memory (same arithmetic, same order).
-constexpr int kPipeCodeCap = 4096;
+constexpr int kPipeCodeCap = 4096;  // 16-bit codes per buffer
+constexpr int kPipeCodeBytes = 2 * kPipeCodeCap;
 extern __shared__ __align__(128) unsigned char dm_smem[];
 
 template <int CAP>
@@ -388,7 +389,7 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
                                            const int (&ids)[CAP / kEB],
                                            const double2* __restrict__ mxy,
                                            const double* __restrict__ mz,
-                                           const uint16_t* __restrict__ rcodes,
+                                           const uint8_t* __restrict__ rcodes,
                                            const int4* __restrict__ meta) {
   const int t = threadIdx.x;
   const int nu = meta_nu(m);
@@ -402,10 +403,10 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
       }
     }
   }
-  if (m.y <= kPipeCodeCap) {
-    // code blocks are warp-aligned (multiples of 32 codes): 16-byte pieces
+  if (m.y <= kPipeCodeBytes) {
+    // code blocks are multiples of 32 bytes: 16-byte pieces
     const uint4* src = reinterpret_cast<const uint4*>(rcodes + m.x);
-    for (int w = t; w < m.y / 8; w += kEB) cp_async16(&S.cd[b][4 * w], src + w);
+    for (int w = t; w < m.y / 16; w += kEB) cp_async16(&S.cd[b][4 * w], src + w);
   }
   if (t == 0) cp_async16(&S.wo[b], meta + 2 * tile + 1);
 }
@@ -426,27 +427,46 @@ __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __
   }
 }
 
-// Walks one edge's ring; T(slot) returns the node record of a tile slot;
-// cd points at this lane's step-0 code, step s at cd[s * 32] (rings.cu
-// layout: word 0 = slot(j) | sign << 15, word 1 = slot(k) | n << 11,
-// word 2 = slot(m_0) | boundary << 15).  Returns the boundary bit.  x_j
-// is not needed by the walk; the caller reads it afterwards (fewer live
+// One lane's view of its warp block of ring codes (rings.cu): W == 2: 16-bit
+// words, step s at word s*32 + lane (word 0 = slot(j) | sign << 15, word 1 =
+// slot(k) | n << 11); W == 1: a header byte n | sign << 5 | boundary << 6 per
+// lane, then one slot byte per step at 32 + s*32 + lane.
+template <int W>
+struct RingCodes {
+  const uint8_t* __restrict__ blk;
+  int lane;
+  __device__ __forceinline__ unsigned raw(int s) const {
+    if constexpr (W == 2) return reinterpret_cast<const uint16_t*>(blk)[s * 32 + lane];
+    else return blk[32 + s * 32 + lane];
+  }
+  __device__ __forceinline__ unsigned slot(int s) const {
+    return W == 2 && s < 3 ? (raw(s) & 0x7ffu) : raw(s);
+  }
+  __device__ __forceinline__ int count() const {
+    if constexpr (W == 2) return static_cast<int>(raw(1) >> 11);
+    else return blk[lane] & 31;
+  }
+  __device__ __forceinline__ bool negative() const {
+    if constexpr (W == 2) return (raw(0) & 0x8000u) != 0;
+    else return (blk[lane] & 32) != 0;
+  }
+};
+
+// Walks one edge's ring; T(slot) returns the node record of a tile slot.
+// x_j is not needed by the walk; the caller reads it afterwards (fewer live
 // registers across the loop).
-template <int RU = 1, typename TabFn>
-__device__ __forceinline__ bool ring_walk(const TabFn& T, const uint16_t* __restrict__ cd,
-                                          double* acc, d4& xk) {
-  const unsigned w0 = cd[0];
-  const unsigned w1 = cd[32];
-  const unsigned w2 = cd[64];
-  const int n = static_cast<int>(w1 >> 11);
-  xk = T(w1 & 0x7ffu);
-  const d4 mp = T(w2 & 0x7ffu);
+template <int W, int RU = 1, typename TabFn>
+__device__ __forceinline__ void ring_walk(const TabFn& T, const RingCodes<W>& C, double* acc,
+                                          d4& xk) {
+  const int n = C.count();
+  xk = T(C.slot(1));
+  const d4 mp = T(C.slot(2));
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int i0 = 0; i0 < n; i0 += RU) {
     unsigned w[RU];
 #pragma unroll
-    for (int u = 0; u < RU; ++u) w[u] = i0 + u < n ? cd[(3 + i0 + u) * 32] : 0u;
+    for (int u = 0; u < RU; ++u) w[u] = i0 + u < n ? C.raw(3 + i0 + u) : 0u;
     d4 m[RU];
 #pragma unroll
     for (int u = 0; u < RU; ++u) m[u] = T(w[u]);
@@ -465,16 +485,15 @@ __device__ __forceinline__ bool ring_walk(const TabFn& T, const uint16_t* __rest
       }
     }
   }
-  const bool neg = (w0 & 0x8000u) != 0;
+  const bool neg = C.negative();
   acc[0] = neg ? -a0 : a0;
   acc[1] = neg ? -a1 : a1;
   acc[2] = neg ? -a2 : a2;
-  return (w2 & 0x8000u) != 0;
 }
 
-template <int CAP, int MINB, int RU = 1, int FAKE = 0>
+template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0>
 __global__ void __launch_bounds__(kEB, MINB)
-    k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint16_t* __restrict__ rcodes,
+    k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint8_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      const double2* __restrict__ mxy, const double* __restrict__ mz,
                      Coords<3> X, i64 ne, int ntiles, bool pos_s, double* __restrict__ navs,
@@ -524,13 +543,12 @@ __global__ void __launch_bounds__(kEB, MINB)
     const bool valid = p < ne;
     double acc[3] = {0.0, 0.0, 0.0};
     d4 xj{}, xk{};
-    bool bflag = false;
     if (valid) {
       const int warp = t >> 5;
       const unsigned wo = (reinterpret_cast<const unsigned*>(&S.wo[b])[warp >> 1] >>
                            (16 * (warp & 1))) & 0xffffu;
       const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
-      if (meta_nu(m) <= CAP && m.y <= kPipeCodeCap) {
+      if (meta_nu(m) <= CAP && m.y <= kPipeCodeBytes) {
         const double2* xy = S.xy[b];
         const double* zz = S.z[b];
         auto T = [&](unsigned i) -> d4 {
@@ -542,14 +560,14 @@ __global__ void __launch_bounds__(kEB, MINB)
           r.z = zz[i];
           return r;
         };
-        const uint16_t* cd = reinterpret_cast<const uint16_t*>(S.cd[b]) + wo + lane;
+        const RingCodes<W> C{reinterpret_cast<const uint8_t*>(S.cd[b]) + wo, lane};
         if (FAKE & 8) {
-          xk = T(cd[32] & 0x7ffu);
+          xk = T(C.slot(1));
           acc[0] = xk.x;
         } else {
-          bflag = ring_walk<RU>(T, cd, acc, xk);
+          ring_walk<W, RU>(T, C, acc, xk);
         }
-        xj = T(cd[0] & 0x7ffu);
+        xj = T(C.slot(0));
       } else {
         auto T = [&](unsigned i) -> d4 {
           const int r = __ldg(tn + i);
@@ -560,14 +578,13 @@ __global__ void __launch_bounds__(kEB, MINB)
           q.z = __ldg(mz + r);
           return q;
         };
-        const uint16_t* cd = rcodes + m.x + wo + lane;
-        bflag = ring_walk(T, cd, acc, xk);
-        xj = T(cd[0] & 0x7ffu);
+        const RingCodes<W> C{rcodes + m.x + wo, lane};
+        ring_walk<W>(T, C, acc, xk);
+        xj = T(C.slot(0));
       }
     }
     double nv[3] = {0.0, 0.0, 0.0};
     double s = 0.0;
-    (void)bflag;
     if (valid) {
       // scale pass; boundary edges get their facet terms (and s) from
       // k_ring_boundary, launched right after on the same stream
@@ -852,24 +869,25 @@ int launch_navs(dm_ctx* c, int variant) {
         return DM_OK;
       };
       int st = DM_OK;
-      switch (c->gather_cfg) {
-        case 7: st = launch(k_navs_ring_pipe<512, 3, 2>, sizeof(PipeSmem<512>)); break;
-        case 8: st = launch(k_navs_ring_pipe<768, 3>, sizeof(PipeSmem<768>)); break;
-        case 9: st = launch(k_navs_ring_pipe<256, 3>, sizeof(PipeSmem<256>)); break;
-        case 10: st = launch(k_navs_ring_pipe<1024, 2>, sizeof(PipeSmem<1024>)); break;
-        case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1>, sizeof(PipeSmem<256>)); break;
-        case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 2>, sizeof(PipeSmem<256>)); break;
-        case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 4>, sizeof(PipeSmem<256>)); break;
-        case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 8>, sizeof(PipeSmem<256>)); break;
-        case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 6>, sizeof(PipeSmem<256>)); break;
-        case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 14>, sizeof(PipeSmem<256>)); break;
-        case 11: st = launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>)); break;
-        case 12: st = launch(k_navs_ring_pipe<256, 4>, sizeof(PipeSmem<256>)); break;
-        case 13: st = launch(k_navs_ring_pipe<512, 3>, sizeof(PipeSmem<512>)); break;
-        default:  // smallest table that holds every tile
-          st = c->ring_max_nodes <= 256 ? launch(k_navs_ring_pipe<256, 4>, sizeof(PipeSmem<256>))
-                                        : launch(k_navs_ring_pipe<512, 4>, sizeof(PipeSmem<512>));
-          break;
+      // the code width and the table size follow the plan (8-bit codes and a
+      // 256-node table when every tile fits, else 16-bit codes, 512 nodes);
+      // DUALMESH_GATHER_CFG 20-25 are the timing probes of the kernel
+      if (c->code_width == 1) {
+        switch (c->gather_cfg) {
+          case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1>, sizeof(PipeSmem<256>)); break;
+          case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2>, sizeof(PipeSmem<256>)); break;
+          case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 4>, sizeof(PipeSmem<256>)); break;
+          case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8>, sizeof(PipeSmem<256>)); break;
+          case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6>, sizeof(PipeSmem<256>)); break;
+          case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14>, sizeof(PipeSmem<256>)); break;
+          default: st = launch(k_navs_ring_pipe<256, 4, 1>, sizeof(PipeSmem<256>)); break;
+        }
+      } else {
+        switch (c->gather_cfg) {
+          case 13: st = launch(k_navs_ring_pipe<512, 3, 2>, sizeof(PipeSmem<512>)); break;
+          case 10: st = launch(k_navs_ring_pipe<1024, 2, 2>, sizeof(PipeSmem<1024>)); break;
+          default: st = launch(k_navs_ring_pipe<512, 4, 2>, sizeof(PipeSmem<512>)); break;
+        }
       }
       if (st) return st;
     }

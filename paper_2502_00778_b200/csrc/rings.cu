@@ -34,6 +34,9 @@
 //                  [slot(j) | s<<15, slot(k) | n<<11, slot(m_0) | b<<15,
 //                   slot(m_1), ..., slot(m_n)]  (slots into the tile list;
 //                                                b: edge has boundary facets)
+//                or, when every tile table holds <= 256 nodes, n+3 bytes of
+//                slots plus a per-lane header byte n | s<<5 | b<<6 at the
+//                start of the warp block (half the code bytes to stream)
 //                stored lane-transposed per warp of 32 consecutive positions:
 //                the warp block holds S_w = max(n+3) steps x 32 lanes, entry
 //                (step, lane) at wstart[w] + step*32 + lane, so the 32 lanes
@@ -168,13 +171,14 @@ __device__ __forceinline__ int perm_sign(int a0, int a1, int a2, int b0, int b1,
   return x1 == b1 ? 1 : -1;
 }
 
+template <int W>
 __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __restrict__ eperm,
                              const int32_t* __restrict__ inc_ptr,
                              const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
                              const int32_t* __restrict__ rank, const uint8_t* __restrict__ bmark,
                              const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt,
                              const u32* __restrict__ wstart, i64 ne,
-                             uint16_t* __restrict__ rcodes, int* __restrict__ flag) {
+                             uint8_t* __restrict__ rcodes, int* __restrict__ flag) {
   const i64 p = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= ne) return;
   const int e = eperm[p];
@@ -213,10 +217,18 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
       if (cnt == 1 && (start < 0 || v < start)) start = v;
     }
   if (start < 0) start = a[0];
-  // step s of this edge lives at out[s * 32]
-  uint16_t* out = rcodes + wstart[p >> 5] + (p & 31);
+  // step s of this edge lives at out[s * 32]; W == 1: one byte per step
+  // after a 32-byte header (n | sign << 5 | boundary << 6 per lane)
+  uint8_t* blk = rcodes + wstart[p >> 5];
+  uint16_t* out = reinterpret_cast<uint16_t*>(blk) + (p & 31);
+  uint8_t* out8 = blk + 32 + (p & 31);
+  auto put = [&](int step, unsigned v) {
+    if constexpr (W == 2) out[step * 32] = static_cast<uint16_t>(v);
+    else out8[step * 32] = static_cast<uint8_t>(v);
+  };
   int sg0 = 0;
-  out[2 * 32] = static_cast<uint16_t>(tslot(list, nl, rank[start]) | (bmark[e] ? 0x8000u : 0u));
+  const int s_start = tslot(list, nl, rank[start]);
+  put(2, W == 2 ? (s_start | (bmark[e] ? 0x8000u : 0u)) : s_start);
   unsigned used = 0;
   int cur = start;
   for (int step = 0; step < n; ++step) {
@@ -238,16 +250,24 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
       atomicOr(flag, 16);  // inconsistently oriented fan
       return;
     }
-    out[(3 + step) * 32] = static_cast<uint16_t>(tslot(list, nl, rank[nxt]));
+    put(3 + step, tslot(list, nl, rank[nxt]));
     cur = nxt;
   }
-  out[0] = static_cast<uint16_t>(tslot(list, nl, rank[j]) | (sg0 < 0 ? 0x8000u : 0u));
-  out[32] = static_cast<uint16_t>(tslot(list, nl, rank[k]) | n << 11);
+  const int sj = tslot(list, nl, rank[j]), sk = tslot(list, nl, rank[k]);
+  if constexpr (W == 2) {
+    put(0, sj | (sg0 < 0 ? 0x8000u : 0u));
+    put(1, sk | n << 11);
+  } else {
+    put(0, sj);
+    put(1, sk);
+    blk[p & 31] = static_cast<uint8_t>(n | (sg0 < 0 ? 32 : 0) | (bmark[e] ? 64 : 0));
+  }
 }
 
-// Codes per warp block: S_w * 32 with S_w = max over the warp's edges of n+3.
+// Bytes per warp block, S_w = max over the warp's edges of n+3 steps:
+// W == 2: S_w * 32 u16 codes; W == 1: a 32-byte header + S_w * 32 bytes.
 __global__ void k_ring_warpsize(const int32_t* __restrict__ eperm,
-                                const int32_t* __restrict__ inc_ptr, i64 ne, i64 nwarps,
+                                const int32_t* __restrict__ inc_ptr, i64 ne, i64 nwarps, int W,
                                 u32* __restrict__ wsize) {
   const i64 w = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (w >= nwarps) return;
@@ -256,11 +276,11 @@ __global__ void k_ring_warpsize(const int32_t* __restrict__ eperm,
     const int e = eperm[p];
     S = max(S, inc_ptr[e + 1] - inc_ptr[e] + 3);
   }
-  wsize[w] = static_cast<u32>(S * 32);
+  wsize[w] = static_cast<u32>(W == 2 ? S * 64 : (S + 1) * 32);
 }
 
-// meta[2t]   = {C0, NC, NU | nbnd << 16, bptr}
-// meta[2t+1] = eight u16 warp-block offsets relative to C0
+// meta[2t]   = {C0, NC, NU | nbnd << 16, bptr}  (C0, NC in bytes)
+// meta[2t+1] = eight u16 warp-block byte offsets relative to C0
 __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restrict__ tcnt,
                             const u32* __restrict__ tile_bptr, i64 nwarps, i64 ntiles,
                             int4* __restrict__ meta) {
@@ -286,6 +306,8 @@ __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restric
 // ---- Morton origin order and the edge permutation
 
 static_assert(kTileNodeCap <= 2048 && kRingMax < 32, "code word 1 packs slot(k) | n << 11");
+static_assert(kRingMax + 4 <= 64 && kTileEdges / 32 * 64 * (kRingMax + 4) < 65536,
+              "u16 warp-block byte offsets");
 
 // per-block partial bounding box of the coordinates: part[6 * block + {lo, hi}]
 __global__ void __launch_bounds__(256) k_bbox(const d4* __restrict__ x4, i64 nv,
@@ -623,18 +645,6 @@ int ensure_rings(dm_ctx* c) {
   // the overflow sets ring_ok = false)
   DM_CK(c, cudaMemsetAsync(c->tnode_cnt.p, 0, ntiles * sizeof(u32), c->stream));
   DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(2 * ntiles)));
-  DevBuf<u32> wstart;
-  DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
-  DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->eperm.p, c->inc_ptr.p, ne, nwarps, wstart.p);
-  int st = scan_exclusive(c, wstart.p, wstart.p, nwarps);
-  if (st) return st;
-  u32 ncodes = 0;
-  DM_CK(c, cudaMemcpyAsync(&ncodes, wstart.p + nwarps, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->stream));
-  DM_CK(c, cudaStreamSynchronize(c->stream));
-  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(ncodes) + 8));
-  DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, (static_cast<size_t>(ncodes) + 8) * sizeof(uint16_t),
-                           c->stream));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
   DevBuf<int32_t> rank;
@@ -648,9 +658,31 @@ int ensure_rings(dm_ctx* c) {
   DM_LAUNCH(c, k_tile_nodes, static_cast<unsigned>(ntiles), kTileEdges, 0, c->edges.p,
             c->eperm.p, c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, ne, c->tnodes.p,
             c->tnode_cnt.p, c->flag.p);
-  DM_LAUNCH(c, k_ring_codes, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p, c->inc_ptr.p,
-            c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p, wstart.p, ne,
-            c->rcodes.p, c->flag.p);
+  // 8-bit slot codes when every tile table fits 256 nodes, else 16-bit
+  int fl0[2] = {0, 0};
+  DM_CK(c, cudaMemcpyAsync(fl0, c->flag.p, sizeof(fl0), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  c->code_width = fl0[1] <= 256 ? 1 : 2;
+  DevBuf<u32> wstart;
+  DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
+  DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->eperm.p, c->inc_ptr.p, ne,
+            nwarps, c->code_width, wstart.p);
+  int st = scan_exclusive(c, wstart.p, wstart.p, nwarps);
+  if (st) return st;
+  u32 nbytes = 0;
+  DM_CK(c, cudaMemcpyAsync(&nbytes, wstart.p + nwarps, sizeof(u32), cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(nbytes) + 16));
+  DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, static_cast<size_t>(nbytes) + 16, c->stream));
+  if (c->code_width == 1)
+    DM_LAUNCH(c, k_ring_codes<1>, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p,
+              c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p,
+              wstart.p, ne, c->rcodes.p, c->flag.p);
+  else
+    DM_LAUNCH(c, k_ring_codes<2>, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p,
+              c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p,
+              wstart.p, ne, c->rcodes.p, c->flag.p);
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
             c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
   int fl[2] = {0, 0};
