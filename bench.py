@@ -60,7 +60,7 @@ def algorithmic_bytes(mesh, n_edges, n_bnd_nodes, n_bnd_edges):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -80,29 +80,50 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
 
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+    def _rows(self):
+        out = []
+        try:
+            lines = open(self.path).read().splitlines()
+        except OSError:
+            return out
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
+                t = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+                t += float("0." + parts[0].split(".")[1]) if "." in parts[0] else 0.0
+                out.append((t, float(parts[1]), float(parts[2]), parts[3:7]))
+            except (ValueError, IndexError):
                 continue
-            for nm, v in zip(names, parts[2:6]):
+        return out
+
+    def live(self) -> bool:
+        """True once nvidia-smi has written samples (it starts slowly)."""
+        return self.proc is not None and len(self._rows()) >= 2
+
+    def stop(self, t0=None, t1=None):
+        """Clock samples inside the host-time window [t0, t1] of the timed
+        region (all samples if the window caught none)."""
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = self._rows()
+        os.unlink(self.path)
+        inside = [r for r in rows if t0 is None or (t0 - 0.02 <= r[0] <= t1 + 0.02)]
+        sel = inside or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in sel:
+            for nm, v in zip(names, r[3]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        os.unlink(self.path)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median([r[1] for r in sel])) if sel else None,
+                "sm_max_mhz": max(r[2] for r in sel) if sel else None,
+                "reasons": sorted(reasons), "samples": len(sel),
+                "samples_in_timed_region": len(inside) if t0 is not None else None}
 
 
 def dist_setup(args):
@@ -239,6 +260,13 @@ def run_ours(args, world, rank, local, dist):
     clocks.start()
     for _ in range(args.warmup):
         step()
+    # keep warming up until nvidia-smi is producing samples, so the timed
+    # region is covered by clock samples (bounded wait)
+    t_wait = time.perf_counter()
+    while not clocks.live() and time.perf_counter() - t_wait < 5.0:
+        for _ in range(10):
+            step()
+        torch.cuda.synchronize()
     torch.cuda.synchronize()
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
@@ -246,13 +274,15 @@ def run_ours(args, world, rank, local, dist):
     barrier(dist)
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_t0 = time.time()
     start.record(stream)
     for k in range(K):
         step(evs[k])
     end.record(stream)
     torch.cuda.synchronize()
+    host_t1 = time.time()
     barrier(dist)
-    clk = clocks.stop()
+    clk = clocks.stop(host_t0, host_t1)
     launches = eng.launches() - launches0
     total_ms = start.elapsed_time(end)
     total_ms = max_over_ranks(dist, total_ms, device=torch.device("cuda", local))
