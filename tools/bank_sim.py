@@ -275,3 +275,106 @@ def color_rank_bits(u, nslots=256, key=lambda r: r % 16):
         slot[r] = c + 16 * used[c]
         used[c] += 1
     return slot
+
+
+def refine(rs, u, slot, nslots=256, sweeps=1, lanes=32):
+    """Min-conflict sweeps over nodes starting from an assignment `slot`
+    (colour = slot % 16): each node moves to the colour with the fewest
+    same-bank partners in the quarter (mod 8) and half (mod 16) groups it is
+    read in."""
+    cap = nslots // 16
+    col = {r: slot[r] % 16 for r in u}
+    used = [0] * 16
+    for r in u:
+        used[col[r]] += 1
+    memb = defaultdict(list)  # node -> list of (half members, quarter members)
+    for w0 in range(0, len(rs), lanes):
+        W = rs[w0:w0 + lanes]
+        S = max(len(s) for s in W)
+        for st in range(S):
+            r_ = [s[st] if st < len(s) else None for s in W]
+            for h in range(0, lanes, 16):
+                half = [x for x in r_[h:h + 16] if x is not None]
+                for q in (h, h + 8):
+                    quart = [x for x in r_[q:q + 8] if x is not None]
+                    for x in set(quart):
+                        memb[x].append((half, quart))
+    for _ in range(sweeps):
+        for v in u:
+            c16 = [0] * 16
+            c8 = [0] * 8
+            for half, quart in memb[v]:
+                for x in set(half):
+                    if x != v:
+                        c16[col[x]] += 1
+                for x in set(quart):
+                    if x != v:
+                        c8[col[x] % 8] += 1
+            used[col[v]] -= 1
+            best = min((c for c in range(16) if used[c] < cap),
+                       key=lambda c: (c16[c] + c8[c % 8], c != col[v]))
+            col[v] = best
+            used[best] += 1
+    nxt = [0] * 16
+    out = {}
+    for r in u:
+        c = col[r]
+        out[r] = c + 16 * nxt[c]
+        nxt[c] += 1
+    return out
+
+
+def refine_parallel(rs, u, slot, rounds=3, nslots=512, seed=0, lanes=32):
+    """Jacobi-style min-conflict rounds (what a CTA can do in parallel): every
+    node computes its best colour from the current colours; a node moves only
+    if it improves and no co-member that also wants to move has a higher
+    random priority.  Colour classes hold nslots / 16 slots."""
+    rng = np.random.default_rng(seed)
+    cap = nslots // 16
+    col = {r: slot[r] % 16 for r in u}
+    prio = {r: rng.random() for r in u}
+    memb = defaultdict(list)
+    for w0 in range(0, len(rs), lanes):
+        W = rs[w0:w0 + lanes]
+        S = max(len(s) for s in W)
+        for st in range(S):
+            r_ = [s[st] if st < len(s) else None for s in W]
+            for h in range(0, lanes, 16):
+                half = [x for x in r_[h:h + 16] if x is not None]
+                for q in (h, h + 8):
+                    quart = [x for x in r_[q:q + 8] if x is not None]
+                    for x in set(quart):
+                        memb[x].append((half, quart))
+    for _ in range(rounds):
+        used = [0] * 16
+        for r in u:
+            used[col[r]] += 1
+        want = {}
+        for v in u:
+            c16 = [0] * 16
+            c8 = [0] * 8
+            for half, quart in memb[v]:
+                for x in set(half):
+                    if x != v:
+                        c16[col[x]] += 1
+                for x in set(quart):
+                    if x != v:
+                        c8[col[x] % 8] += 1
+            cost = [c16[c] + c8[c % 8] for c in range(16)]
+            b = min(range(16), key=lambda c: (cost[c], c != col[v]))
+            if cost[b] < cost[col[v]]:
+                want[v] = b
+        for v, b in want.items():
+            rivals = {x for half, _ in memb[v] for x in half
+                      if x in want and x != v and want[x] % 8 == b % 8}
+            if all(prio[v] > prio[x] for x in rivals) and used[b] < cap:
+                used[col[v]] -= 1
+                used[b] += 1
+                col[v] = b
+    nxt = [0] * 16
+    out = {}
+    for r in u:
+        c = col[r]
+        out[r] = c + 16 * nxt[c]
+        nxt[c] += 1
+    return out
