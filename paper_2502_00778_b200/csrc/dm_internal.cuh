@@ -231,16 +231,6 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned b
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s), "r"(bytes)
                : "memory");
 }
-// Arrive on m once all of this thread's prior cp.async copies have landed
-// (the arrival is not pre-counted: the barrier's count includes it).
-__device__ __forceinline__ void cp_async_arrive(unsigned long long* m) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(s) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(m));
   unsigned ok = 0;
