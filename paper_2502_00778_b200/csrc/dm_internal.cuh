@@ -219,40 +219,6 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
-// mbarrier + TMA tile::gather4 (sm_100a): four arbitrary rows of a 2D
-// tensor map into 128 contiguous bytes of shared memory per instruction,
-// through the TMA engine instead of the LSU / L1 pipeline.
-__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  unsigned ok = 0;
-  while (!ok)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(s), "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map,
-                                            unsigned long long* m, int r0, int r1, int r2,
-                                            int r3) {
-  const unsigned sd = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  const unsigned sm = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(sd),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-      "r"(sm)
-      : "memory");
-}
 __device__ __forceinline__ int4 ld_i4(const int4* p) { return __ldg(p); }
 
 // Select el[i] for a runtime i in 0..3 without local-memory indexing.
