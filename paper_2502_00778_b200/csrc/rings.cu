@@ -64,93 +64,78 @@
 namespace dm {
 namespace {
 
-constexpr int kCand = 8192;  // candidate ids gathered per tile (before dedup)
+constexpr int kHash = 4096;  // open-addressing set of the tile's node ranks
+static_assert(kTileNodeCap <= kHash / 2, "hash set at most half full");
 
+// Per tile: the sorted unique Morton ranks of every node its edges touch (j,
+// k and the ring nodes).  Candidates go through a shared-memory hash set
+// (linear probing, atomicCAS), the unique ones are bitonic-sorted.  Tiles
+// with more than kTileNodeCap nodes set flag bit 2 and keep count 0.
 __global__ void __launch_bounds__(kTileEdges)
     k_tile_nodes(const int2* __restrict__ edges, const int32_t* __restrict__ eperm,
                  const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
                  const int32_t* __restrict__ el, const int32_t* __restrict__ rank, i64 ne,
                  int32_t* __restrict__ tnodes, u32* __restrict__ tcnt, int* __restrict__ flag) {
-  __shared__ int buf[kCand];
+  __shared__ int hs[kHash];
+  __shared__ int uq[2 * kTileNodeCap];
   __shared__ int s_n;
-  __shared__ int s_w[kTileEdges / 32 + 1];
   const int t = threadIdx.x;
-  const i64 p = static_cast<i64>(blockIdx.x) * kTileEdges + t;
+  for (int i = t; i < kHash; i += kTileEdges) hs[i] = -1;
   if (t == 0) s_n = 0;
   __syncthreads();
+  auto insert = [&](int v) {
+    unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 20;  // 12 bits
+    for (int probe = 0; probe < kHash; ++probe, h = (h + 1) & (kHash - 1)) {
+      const int old = atomicCAS(&hs[h], -1, v);
+      if (old == -1) {
+        const int pos = atomicAdd(&s_n, 1);
+        if (pos < 2 * kTileNodeCap) uq[pos] = v;
+        return;
+      }
+      if (old == v) return;
+    }
+  };
+  const i64 p = static_cast<i64>(blockIdx.x) * kTileEdges + t;
   if (p < ne) {
     const int e = eperm[p];
     const int2 jk = edges[e];
-    const int pb = inc_ptr[e], pe = inc_ptr[e + 1];
-    const int m = 2 + 2 * (pe - pb);
-    int w = atomicAdd(&s_n, m);
-    if (w + m <= kCand) {
-      buf[w++] = rank[jk.x];
-      buf[w++] = rank[jk.y];
-      for (int q = pb; q < pe; ++q) {
-        const int4 v = reinterpret_cast<const int4*>(el)[inc[q]];
-        const int vs[4] = {v.x, v.y, v.z, v.w};
-        for (int a = 0; a < 4; ++a)
-          if (vs[a] != jk.x && vs[a] != jk.y) buf[w++] = rank[vs[a]];
-      }
+    insert(rank[jk.x]);
+    insert(rank[jk.y]);
+    for (int q = inc_ptr[e]; q < inc_ptr[e + 1]; ++q) {
+      const int4 v = reinterpret_cast<const int4*>(el)[inc[q]];
+      const int vs[4] = {v.x, v.y, v.z, v.w};
+      for (int a = 0; a < 4; ++a)
+        if (vs[a] != jk.x && vs[a] != jk.y) insert(rank[vs[a]]);
     }
   }
   __syncthreads();
   const int n = s_n;
-  if (n > kCand) {
-    if (t == 0) atomicOr(flag, 1);
+  if (t == 0) atomicMax(flag + 1, n);
+  if (n > kTileNodeCap) {
+    if (t == 0) atomicOr(flag, 2);
     return;
   }
   int P = 2;
   while (P < n) P <<= 1;
-  for (int i = n + t; i < P; i += kTileEdges) buf[i] = 0x7fffffff;
+  for (int i = n + t; i < P; i += kTileEdges) uq[i] = 0x7fffffff;
   __syncthreads();
   for (int k = 2; k <= P; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = t; i < P; i += kTileEdges) {
         const int ixj = i ^ j;
         if (ixj > i) {
-          const int a = buf[i], b = buf[ixj];
+          const int a = uq[i], b = uq[ixj];
           if ((a > b) == ((i & k) == 0)) {
-            buf[i] = b;
-            buf[ixj] = a;
+            uq[i] = b;
+            uq[ixj] = a;
           }
         }
       }
       __syncthreads();
     }
-  // unique, in order: each thread owns a contiguous chunk
-  const int per = (n + kTileEdges - 1) / kTileEdges;
-  const int lo = t * per, hi = min(n, lo + per);
-  int mine = 0;
-  for (int i = lo; i < hi; ++i)
-    if (i == 0 || buf[i] != buf[i - 1]) ++mine;
-  // block exclusive scan of `mine`
-  const int lane = t & 31, warp = t >> 5;
-  int incl = warp_incl_scan(mine);
-  if (lane == 31) s_w[warp] = incl;
-  __syncthreads();
-  if (t == 0) {
-    int run = 0;
-    for (int w = 0; w < kTileEdges / 32; ++w) {
-      const int v = s_w[w];
-      s_w[w] = run;
-      run += v;
-    }
-    s_w[kTileEdges / 32] = run;
-  }
-  __syncthreads();
-  int pos = s_w[warp] + incl - mine;
-  const int total = s_w[kTileEdges / 32];
-  if (t == 0) atomicMax(flag + 1, total);
-  if (total > kTileNodeCap) {
-    if (t == 0) atomicOr(flag, 2);
-    return;
-  }
   int32_t* out = tnodes + static_cast<i64>(blockIdx.x) * kTileNodeCap;
-  for (int i = lo; i < hi; ++i)
-    if (i == 0 || buf[i] != buf[i - 1]) out[pos++] = buf[i];
-  if (t == 0) tcnt[blockIdx.x] = static_cast<u32>(total);
+  for (int i = t; i < n; i += kTileEdges) out[i] = uq[i];
+  if (t == 0) tcnt[blockIdx.x] = static_cast<u32>(n);
 }
 
 __device__ __forceinline__ int tslot(const int32_t* list, int n, int v) {
