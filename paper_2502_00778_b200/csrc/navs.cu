@@ -491,7 +491,66 @@ __device__ __forceinline__ void ring_walk(const TabFn& T, const RingCodes<W>& C,
   acc[2] = neg ? -a2 : a2;
 }
 
-template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0>
+// Traditional median-dual terms along the
+// same ring: element i = {j, k, m_i, m_i+1} contributes
+//   c_i = (E_i - m) x (F_i - m) + (F_i+1 - m) x (E_i - m),  negated if
+//   c_i . (x_k - x_j) < 0,
+// with m the edge midpoint, E_i the element centroid and F_i the centroid of
+// the face {j, m_i, k}; each face centroid is shared by consecutive elements,
+// so an incidence again needs one new node.  Which of the two faces is "L"
+// does not matter (swapping them negates c exactly and the sign rule undoes
+// it).  The centroids are summed from S = x_j + x_k (= 2m exactly) instead of
+// in local order, so results are within rounding of the serial loop (<= 1e-12
+// per edge vector), not bitwise; x_j / x_k are re-read by the caller.
+template <int W, typename TabFn>
+__device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W>& C, double* acc) {
+  const int n = C.count();
+  double mx, my, mz, ex, ey, ez;
+  {
+    const d4 xj = T(C.slot(0)), xk = T(C.slot(1));
+    mx = (xj.x + xk.x) * 0.5;
+    my = (xj.y + xk.y) * 0.5;
+    mz = (xj.z + xk.z) * 0.5;
+    ex = xk.x - xj.x;
+    ey = xk.y - xj.y;
+    ez = xk.z - xj.z;
+  }
+  d4 mp = T(C.slot(2));
+  double fx = (2.0 * mx + mp.x) * (1.0 / 3.0) - mx;
+  double fy = (2.0 * my + mp.y) * (1.0 / 3.0) - my;
+  double fz = (2.0 * mz + mp.z) * (1.0 / 3.0) - mz;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const d4 m = T(C.raw(3 + i));
+    const double gx = (2.0 * mx + m.x) * (1.0 / 3.0) - mx;
+    const double gy = (2.0 * my + m.y) * (1.0 / 3.0) - my;
+    const double gz = (2.0 * mz + m.z) * (1.0 / 3.0) - mz;
+    const double cx = (2.0 * mx + mp.x + m.x) * 0.25 - mx;
+    const double cy = (2.0 * my + mp.y + m.y) * 0.25 - my;
+    const double cz = (2.0 * mz + mp.z + m.z) * 0.25 - mz;
+    double p0, p1, p2, q0, q1, q2;
+    cross3(cx, cy, cz, fx, fy, fz, p0, p1, p2);
+    cross3(gx, gy, gz, cx, cy, cz, q0, q1, q2);
+    double c0 = p0 + q0, c1 = p1 + q1, c2 = p2 + q2;
+    if (c0 * ex + c1 * ey + c2 * ez < 0.0) {
+      c0 = -c0;
+      c1 = -c1;
+      c2 = -c2;
+    }
+    a0 += c0;
+    a1 += c1;
+    a2 += c2;
+    mp = m;
+    fx = gx;
+    fy = gy;
+    fz = gz;
+  }
+  acc[0] = a0;
+  acc[1] = a1;
+  acc[2] = a2;
+}
+
+template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint8_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
@@ -561,13 +620,19 @@ __global__ void __launch_bounds__(kEB, MINB)
           return r;
         };
         const RingCodes<W> C{reinterpret_cast<const uint8_t*>(S.cd[b]) + wo, lane};
-        if (FAKE & 8) {
+        if constexpr (ALGO == kTraditional) {
+          ring_walk_trad<W>(T, C, acc);
           xk = T(C.slot(1));
-          acc[0] = xk.x;
+          xj = T(C.slot(0));
         } else {
-          ring_walk<W, RU>(T, C, acc, xk);
+          if (FAKE & 8) {
+            xk = T(C.slot(1));
+            acc[0] = xk.x;
+          } else {
+            ring_walk<W, RU>(T, C, acc, xk);
+          }
+          xj = T(C.slot(0));
         }
-        xj = T(C.slot(0));
       } else {
         auto T = [&](unsigned i) -> d4 {
           const int r = __ldg(tn + i);
@@ -579,7 +644,12 @@ __global__ void __launch_bounds__(kEB, MINB)
           return q;
         };
         const RingCodes<W> C{rcodes + m.x + wo, lane};
-        ring_walk<W>(T, C, acc, xk);
+        if constexpr (ALGO == kTraditional) {
+          ring_walk_trad<W>(T, C, acc);
+          xk = T(C.slot(1));
+        } else {
+          ring_walk<W>(T, C, acc, xk);
+        }
         xj = T(C.slot(0));
       }
     }
@@ -588,7 +658,7 @@ __global__ void __launch_bounds__(kEB, MINB)
     if (valid) {
       // scale pass; boundary edges get their facet terms (and s) from
       // k_ring_boundary, launched right after on the same stream
-      edge_tail_values<3, kDualFree>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
+      edge_tail_values<3, ALGO>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
       if (!(FAKE & 2) || s == -12345.0)
         svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
     }
@@ -853,7 +923,7 @@ int launch_navs(dm_ctx* c, int variant) {
               c->svals.p);
     tmark(c, 1);
     tmark(c, 2);
-  } else if (variant == DM_VARIANT_GATHER && D == 3 && ALGO == kDualFree && c->ring_ok) {
+  } else if (variant == DM_VARIANT_GATHER && D == 3 && c->ring_ok) {
     tmark(c, 0);
     if constexpr (D == 3) {
       auto launch = [&](auto kern, int smem) -> int {
@@ -872,7 +942,11 @@ int launch_navs(dm_ctx* c, int variant) {
       // the code width and the table size follow the plan (8-bit codes and a
       // 256-node table when every tile fits, else 16-bit codes, 512 nodes);
       // DUALMESH_GATHER_CFG 20-25 are the timing probes of the kernel
-      if (c->code_width == 1) {
+      if (ALGO == kTraditional) {  // ~30 live doubles in the walk: 2 CTAs/SM, no spills
+        st = c->code_width == 1
+                 ? launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional>, sizeof(PipeSmem<256>))
+                 : launch(k_navs_ring_pipe<512, 2, 2, 1, 0, kTraditional>, sizeof(PipeSmem<512>));
+      } else if (c->code_width == 1) {
         switch (c->gather_cfg) {
           case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1>, sizeof(PipeSmem<256>)); break;
           case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2>, sizeof(PipeSmem<256>)); break;
@@ -892,7 +966,7 @@ int launch_navs(dm_ctx* c, int variant) {
       if (st) return st;
     }
     tmark(c, 1);
-    if constexpr (D == 3) {
+    if constexpr (D == 3 && ALGO == kDualFree) {
       if (c->n_bedge > 0) {
         DM_CK(c, c->bterms.ensure(static_cast<size_t>(3 * c->nB)));
         DM_LAUNCH(c, k_facet_terms, grid_for(c->nB, 256), 256, 0, X, c->bnd.p, c->nB,
@@ -956,7 +1030,7 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
     return fail(c, DM_ERR_INVALID_ARG, "unknown nav variant");
   int st = ensure_bedge(c);
   if (st) return st;
-  if (variant == DM_VARIANT_GATHER && algo == DM_NAV_DUALFREE) {
+  if (variant == DM_VARIANT_GATHER) {
     st = ensure_rings(c);
     if (st) return st;
   }
@@ -975,8 +1049,7 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
                                  : launch_navs<2, kTraditional>(c, variant);
   }
   if (st) return st;
-  c->svals_pos = variant == DM_VARIANT_GATHER && c->dim == 3 && algo == DM_NAV_DUALFREE &&
-                 c->ring_ok && c->vol_by_rank;
+  c->svals_pos = variant == DM_VARIANT_GATHER && c->dim == 3 && c->ring_ok && c->vol_by_rank;
   c->have_navs = true;
   c->navs_algo = algo;
   c->have_vols = false;

@@ -42,8 +42,12 @@ def run_all(eng, mesh):
     out["navs_faces"] = eng.get_navs()
     eng.navs(DF, ELEMV)
     out["navs_elem"] = eng.get_navs()
-    eng.navs(TR, GATHER)
+    eng.navs(TR, EXACT)  # face-list kernel: bitwise the serial loop
     out["navs_traditional"] = eng.get_navs()
+    eng.navs(TR, GATHER)  # ring walk: <= 1e-12, deterministic
+    out["navs_trad_fast"] = eng.get_navs()
+    eng.navs(TR, GATHER)
+    out["navs_trad_fast2"] = eng.get_navs()
     eng.navs(DF, SCATTER)
     out["navs_scatter"] = eng.get_navs()
     eng.navs(DF, GATHER)  # default fast path (ring walk in 3D)
@@ -62,6 +66,8 @@ def check_fast(g, want_navs, want_vol, dim):
     assert np.abs(g["vol_fast"] - want_vol).max() <= 1e-12 * np.abs(want_vol).max()
     np.testing.assert_array_equal(g["navs_faces"], want_navs)
     np.testing.assert_array_equal(g["navs_elem"], want_navs)
+    np.testing.assert_array_equal(g["navs_trad_fast"], g["navs_trad_fast2"])
+    assert per_vector_rel(g["navs_trad_fast"], g["navs_traditional"], dim) <= 1e-12
 
 
 def test_fixtures_bit_exact(engine, fixtures, oracle):
