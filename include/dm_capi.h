@@ -178,7 +178,8 @@ int64_t dm_kernel_launches(const dm_ctx* ctx);
 /* Which element-loop kernels the plan enables: info[0] ring path built,
  * [1] ring path usable, [2] row tables built, [3] row tables usable,
  * [4] max tile node count (ring path), [5] failure flag of the ring build,
- * [6] edge-volume pass walks nodes in Morton order (1) or id order (0). */
+ * [6] edge-volume pass walks nodes in Morton order (1) or id order (0),
+ * [7] tile tables recoloured against bank conflicts (env DUALMESH_PLAN_COLOR=1). */
 int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
 /* SPEC cli_io file formats, host only (no device needed).
  * MeshFile: dm_mesh_file_read parses `path` (call with NULL arrays for the

@@ -336,6 +336,7 @@ int dm_plan_info(dm_ctx* c, int64_t info[8]) {
   info[4] = c->ring_max_nodes;
   info[5] = c->ring_fail;
   info[6] = c->vol_by_rank;
+  info[7] = c->plan_colored;
   return DM_OK;
 }
 

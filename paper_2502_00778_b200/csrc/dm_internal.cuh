@@ -93,6 +93,7 @@ struct dm_ctx {
   dm::DevBuf<dm::u32> tnode_cnt;
   dm::DevBuf<uint8_t> rcodes;      // lane-transposed warp blocks (rings.cu), bytes
   int code_width = 2;              // 1: 8-bit slots + per-lane header, 2: 16-bit words
+  bool plan_colored = false;       // tile tables recoloured against bank conflicts
   dm::DevBuf<int4> ring_meta;      // per tile {C0, NC, NU | nbnd << 16, bptr}, offsets
   dm::DevBuf<int32_t> eperm;       // tile position p -> edge id (Morton origin order)
   dm::DevBuf<int32_t> morder;      // Morton rank -> node id

@@ -397,7 +397,7 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
 #pragma unroll
     for (int u = 0; u < CAP / kEB; ++u) {
       const int i = t + u * kEB;
-      if (i < nu) {
+      if (i < nu && ids[u] >= 0) {  // recoloured tables have holes (rings.cu)
         cp_async16(&S.xy[b][i], mxy + ids[u]);
         cp_async8(&S.z[b][i], mz + ids[u]);
       }

@@ -350,7 +350,8 @@ class Engine:
         return {"rings_built": bool(info[0]), "ring_ok": bool(info[1]),
                 "tables_built": bool(info[2]), "table_ok": bool(info[3]),
                 "ring_max_tile_nodes": int(info[4]), "ring_fail_bits": int(info[5]),
-                "volume_order": "morton" if info[6] else "node"}
+                "volume_order": "morton" if info[6] else "node",
+                "colored": bool(info[7])}
 
     def launches(self) -> int:
         return int(self._lib.dm_kernel_launches(self._c))

@@ -400,3 +400,26 @@ def test_deforming_grid_reuses_plan(engine, oracle, name, scale):
     engine.metrics_host(p(np.ascontiguousarray(x2)), DF, GATHER, EDGE, p(navs), p(vols))
     np.testing.assert_array_equal(navs, got)
     np.testing.assert_array_equal(vols, engine.get_volumes())
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C3", 4), ("C5", 2)])
+def test_colored_plan_same_bits(name, scale, monkeypatch):
+    """The opt-in bank-conflict colouring only relabels table slots: navs
+    and volumes are bitwise those of the uncoloured plan."""
+    from paper_2502_00778_b200 import Engine
+    m = meshgen.baseline_config(name, scale)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("DUALMESH_PLAN_COLOR", flag)
+        eng = Engine(0)
+        try:
+            eng.set_mesh(m)
+            eng.build_edges()
+            eng.navs(DF, GATHER)
+            eng.volumes(EDGE)
+            assert eng.plan_info()["colored"] == (flag == "1")
+            out.append((eng.get_navs(), eng.get_volumes()))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
