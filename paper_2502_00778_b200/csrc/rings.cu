@@ -485,6 +485,13 @@ __global__ void __launch_bounds__(kTileEdges)
   }
 }
 
+__global__ void k_sum_u32(const u32* __restrict__ x, i64 n, unsigned long long* __restrict__ out) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long v = i < n ? x[i] : 0ull;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
 // ---- Morton origin order and the edge permutation
 
 static_assert(kTileNodeCap <= 2048 && kRingMax < 32, "code word 1 packs slot(k) | n << 11");
@@ -849,6 +856,22 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
   DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->eperm.p, c->inc_ptr.p, ne,
             nwarps, c->code_width, wstart.p);
+  // code offsets are 32-bit: check the exact total before the u32 scan
+  {
+    DevBuf<unsigned long long> tot;
+    DM_CK(c, tot.ensure(1));
+    DM_CK(c, cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), c->stream));
+    DM_LAUNCH(c, k_sum_u32, grid_for(nwarps, 256), 256, 0, wstart.p, nwarps, tot.p);
+    unsigned long long h = 0;
+    DM_CK(c, cudaMemcpyAsync(&h, tot.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    DM_CK(c, cudaStreamSynchronize(c->stream));
+    if (h + 16 >= (1ull << 32)) {  // plan too large for 32-bit offsets: bit-exact path
+      c->ring_fail = 32;
+      c->ring_ok = false;
+      c->have_rings = true;
+      return DM_OK;
+    }
+  }
   int st = scan_exclusive(c, wstart.p, wstart.p, nwarps);
   if (st) return st;
   u32 nbytes = 0;
