@@ -865,7 +865,7 @@ int ensure_rings(dm_ctx* c) {
     unsigned long long h = 0;
     DM_CK(c, cudaMemcpyAsync(&h, tot.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     DM_CK(c, cudaStreamSynchronize(c->stream));
-    if (h + 16 >= (1ull << 32)) {  // plan too large for 32-bit offsets: bit-exact path
+    if (h + 16 >= (1ull << 31)) {  // offsets live in int4 metadata: bit-exact path beyond 2 GB
       c->ring_fail = 32;
       c->ring_ok = false;
       c->have_rings = true;
