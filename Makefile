@@ -43,7 +43,7 @@ $(LIBDIR)/libdm_meshgen.so: $(CSRC)/meshgen.cpp include/dm_meshgen.h
 	$(CXX) $(CXXFLAGS) -O3 -shared -o $@ $<
 
 # test infrastructure: extern "C" probe over the C++ drop-in API
-tests/cpp/_build/libapi_probe.so: tests/cpp/api_probe.cpp $(LIBDIR)/libdualmesh.so include/dualmesh/mesh.hpp
+tests/cpp/_build/libapi_probe.so: tests/cpp/api_probe.cpp $(LIBDIR)/libdualmesh.so include/dualmesh/mesh.hpp include/dualmesh/metrics.hpp include/dualmesh/io.hpp
 	@mkdir -p tests/cpp/_build
 	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -ldualmesh -Wl,-rpath,'$$ORIGIN/../../../$(LIBDIR)'
 
