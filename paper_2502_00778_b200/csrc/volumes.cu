@@ -17,7 +17,7 @@ namespace {
 // acc += s[idx(q)] for q in [b, e), in order; the loads of each batch of
 // kB terms are issued before any add (memory-level parallelism on a
 // latency-bound gather; the fold order is unchanged).
-constexpr int kB = 8;
+constexpr int kB = 6;
 template <typename Idx>
 __device__ __forceinline__ double fold_terms(double acc, u32 b, u32 e, const Idx& idx,
                                              const double* __restrict__ s) {
@@ -33,7 +33,7 @@ __device__ __forceinline__ double fold_terms(double acc, u32 b, u32 e, const Idx
 }
 
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 8)
     k_vol_edge(const u32* __restrict__ in_ptr, const int32_t* __restrict__ in_list,
                const u32* __restrict__ os, const double* __restrict__ svals, i64 nv,
                double* __restrict__ V) {
