@@ -301,9 +301,9 @@ __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restric
 // class has a higher priority (a fixed hash), capacity permitting.  Slots are
 // only a relabelling of the table, so results do not depend on it
 // (tools/bank_sim.py models 1.8-1.9x -> ~1.45x ideal wavefronts; measured on
-// C5: element loop 2.36 -> 2.24 ms, plan +0.6 s -- hence opt-in).
+// C5: shared-load conflict wavefronts 177 M -> 96 M, element loop 2.36 -> 2.24
+// ms, plan +0.19 s).
 constexpr int kColorRounds = 8;
-constexpr int kMembCap = kTileEdges * (kRingMax + 3);
 
 __device__ __forceinline__ unsigned color_prio(unsigned tile, unsigned v) {
   unsigned h = tile * 0x9E3779B1u ^ (v + 0x7F4A7C15u) * 0x85EBCA77u;
@@ -312,25 +312,30 @@ __device__ __forceinline__ unsigned color_prio(unsigned tile, unsigned v) {
   return h ^ (h >> 13);
 }
 
+// Warp-cooperative: each warp walks its own code block step by step; the 32
+// lanes of a step hold the nodes read together, so the colour histograms of a
+// half / quarter warp come from 16 ballots, duplicates of a lane's own node
+// are removed with __match_any_sync, and each lane adds its partner counts to
+// its node's cost row in shared memory.  A node that wants to move is blocked
+// by a higher-priority partner (same half warp) wanting the same mod-8 class
+// (__match_any_sync + __reduce_max_sync); capacity 16 slots per colour.
 __global__ void __launch_bounds__(kTileEdges)
-    k_tile_color(uint8_t* __restrict__ rcodes, int4* __restrict__ meta,
-                 int32_t* __restrict__ tnodes, int ntiles, i64 ne) {
-  __shared__ __align__(16) uint8_t cb[2 * 4096];  // the tile's code block
-  __shared__ uint16_t memb[kMembCap];             // (warp, step, lane) per access, by node
-  __shared__ int mptr[257], mfill[256];
-  __shared__ uint8_t col[256], want[256], slot_new[256];
+    k_tile_color_warp(uint8_t* __restrict__ rcodes, int4* __restrict__ meta,
+                      int32_t* __restrict__ tnodes, int ntiles, i64 ne) {
+  __shared__ __align__(16) uint8_t cb[2 * 4096];
+  __shared__ uint16_t cost[256][24];  // per node: 16 half-warp (mod 16) + 8 quarter (mod 8)
+  __shared__ uint8_t col[256], want[256], blocked[256], slot_new[256];
   __shared__ int ccount[16];
   __shared__ int wofs[kTileEdges / 32 + 1];
   __shared__ int32_t ids[256];
   const int tile = blockIdx.x;
   if (tile >= ntiles) return;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
   const int4 m = meta[2 * tile];
   const int nu = m.z & 0xffff, nbytes = m.y;
   if (nu > 256 || nbytes > static_cast<int>(sizeof(cb))) return;
   for (int i = t; i < nbytes / 16; i += kTileEdges)
     reinterpret_cast<uint4*>(cb)[i] = reinterpret_cast<const uint4*>(rcodes + m.x)[i];
-  // warp blocks of this tile (the last tile may have fewer than 8)
   const i64 left = ne - static_cast<i64>(tile) * kTileEdges;
   const int nw = static_cast<int>(left >= kTileEdges ? kTileEdges / 32 : (left + 31) / 32);
   if (t <= kTileEdges / 32) {
@@ -339,137 +344,105 @@ __global__ void __launch_bounds__(kTileEdges)
                            static_cast<unsigned>(wo.z), static_cast<unsigned>(wo.w)};
     wofs[t] = t < nw ? static_cast<int>((o[t >> 1] >> (16 * (t & 1))) & 0xffffu) : nbytes;
   }
-  mfill[t] = 0;
   if (t < 16) ccount[t] = 0;
   __syncthreads();
-  // accesses of this lane: steps 0 .. n+2 of warp block w
-  const int w = t >> 5, l = t & 31;
-  const bool has_block = wofs[w] < wofs[w + 1];
+  const bool has_block = w < nw;
+  const int S = has_block ? (wofs[w + 1] - wofs[w]) / 32 - 1 : 0;  // steps in this warp block
   const int nl = has_block ? (cb[wofs[w] + l] & 31) : -3;
-  auto code = [&](int ww, int st, int ll) -> int { return cb[wofs[ww] + 32 + st * 32 + ll]; };
-  for (int st = 0; st < nl + 3; ++st) atomicAdd(&mfill[code(w, st, l)], 1);
-  __syncthreads();
-  // padding steps (st >= n+3 of a lane) become 0xff: a co-member check is
-  // then one byte read (the padding is never read by the ring kernel)
-  if (has_block) {
-    const int S = (wofs[w + 1] - wofs[w]) / 32 - 1;
-    for (int st = nl + 3; st < S; ++st) cb[wofs[w] + 32 + st * 32 + l] = 0xff;
-  }
-  if (t == 0) {
-    int run = 0;
-    for (int v = 0; v < 256; ++v) {
-      mptr[v] = run;
-      run += mfill[v];
-    }
-    mptr[256] = run;
+  const uint8_t* blk = cb + wofs[w] + 32;
+  if (t < nu) {
+    col[t] = static_cast<uint8_t>(t & 15);
+    atomicAdd(&ccount[t & 15], 1);
   }
   __syncthreads();
-  mfill[t] = mptr[t];
-  __syncthreads();
-  for (int st = 0; st < nl + 3; ++st) {
-    const int v = code(w, st, l);
-    const int pos = atomicAdd(&mfill[v], 1);
-    if (pos < kMembCap) memb[pos] = static_cast<uint16_t>(w << 10 | st << 5 | l);
-  }
-  const int v = t;  // from here on, thread = node slot
-  if (v < nu) {
-    col[v] = static_cast<uint8_t>(v & 15);
-    atomicAdd(&ccount[v & 15], 1);
-  }
-  __syncthreads();
-  const unsigned pv = color_prio(tile, v);
+  const unsigned half = (l & 16) ? 0xffff0000u : 0x0000ffffu;
+  const unsigned quart = 0xffu << (l & 24);
   for (int round = 0; round < kColorRounds; ++round) {
-    // same-bank partner counts per colour, 8 bits each, in registers:
-    // c16 (half warp, mod 16) in h[0..3], c8 (quarter warp, mod 8) in g[0..1]
-    unsigned h[4] = {0u, 0u, 0u, 0u}, g[2] = {0u, 0u};
-    if (v < nu) {
-      for (int q = mptr[v]; q < mptr[v + 1]; ++q) {
-        const int a = memb[q], ww = a >> 10, st = (a >> 5) & 31, ll = a & 31;
-        const uint8_t* grp = cb + wofs[ww] + 32 + st * 32 + (ll & 16);
-        const int qq = ll & 8;
-        for (int l2 = 0; l2 < 16; ++l2) {
-          const int x = grp[l2];
-          if (x == 0xff || x == v) continue;
-          const int cx = col[x];
-          const unsigned inc = 1u << (8 * (cx & 3));
-          h[0] += (cx >> 2) == 0 ? inc : 0u;
-          h[1] += (cx >> 2) == 1 ? inc : 0u;
-          h[2] += (cx >> 2) == 2 ? inc : 0u;
-          h[3] += (cx >> 2) == 3 ? inc : 0u;
-          if ((l2 & 8) == qq) {
-            const unsigned i8 = 1u << (8 * (cx & 3));
-            g[0] += (cx & 4) == 0 ? i8 : 0u;
-            g[1] += (cx & 4) != 0 ? i8 : 0u;
-          }
+    for (int i = t; i < 256 * 24 / 2; i += kTileEdges) reinterpret_cast<uint32_t*>(cost)[i] = 0u;
+    __syncthreads();
+    // ---- partner histograms, step by step (warp-uniform loop)
+    for (int st = 0; st < S; ++st) {
+      const bool act = st < nl + 3;
+      const int x = act ? blk[st * 32 + l] : 256 + l;  // inactive lanes: unique dummies
+      const int cx = act ? col[x] : 31;
+      const unsigned same = __match_any_sync(0xffffffffu, x);
+      const unsigned others = ~same;
+      unsigned h16[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) h16[c] = __ballot_sync(0xffffffffu, cx == c);
+      if (act) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int n16 = __popc(h16[c] & half & others);
+          if (n16) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][c & ~1]),
+                             static_cast<unsigned>(n16) << (16 * (c & 1)));
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int n8 = __popc((h16[c] | h16[c + 8]) & quart & others);
+          if (n8) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][16 + (c & ~1)]),
+                            static_cast<unsigned>(n8) << (16 * (c & 1)));
         }
       }
-      auto cost = [&](int c) -> int {
-        const unsigned a16 = (c >> 2) == 0 ? h[0] : (c >> 2) == 1 ? h[1] : (c >> 2) == 2 ? h[2] : h[3];
-        const unsigned a8 = (c & 4) ? g[1] : g[0];
-        return static_cast<int>((a16 >> (8 * (c & 3))) & 255u) +
-               static_cast<int>((a8 >> (8 * (c & 3))) & 255u);
-      };
-      const int cur = col[v];
-      int best = cur, bc = cost(cur);
+    }
+    __syncthreads();
+    if (t < nu) {
+      const int cur = col[t];
+      int best = cur, bc = cost[t][cur] + cost[t][16 + (cur & 7)];
       for (int c = 0; c < 16; ++c) {
-        const int cc = cost(c);
+        const int cc = cost[t][c] + cost[t][16 + (c & 7)];
         if (cc < bc) {
           bc = cc;
           best = c;
         }
       }
-      want[v] = static_cast<uint8_t>(best != cur ? best : 0xff);
+      want[t] = static_cast<uint8_t>(best != cur ? best : 0xff);
+      blocked[t] = 0;
     }
-    const int any = __syncthreads_or(v < nu && want[v] != 0xff);
+    const int any = __syncthreads_or(t < nu && want[t] != 0xff);
     if (!any) break;
-    if (v < nu && want[v] != 0xff) {
-      const int b = want[v];
-      bool blocked = false;
-      for (int q = mptr[v]; q < mptr[v + 1] && !blocked; ++q) {
-        const int a = memb[q], ww = a >> 10, st = (a >> 5) & 31, ll = a & 31;
-        const uint8_t* grp = cb + wofs[ww] + 32 + st * 32 + (ll & 16);
-        for (int l2 = 0; l2 < 16; ++l2) {
-          const int x = grp[l2];
-          if (x == 0xff || x == v || want[x] == 0xff || (want[x] & 7) != (b & 7)) continue;
-          const unsigned px = color_prio(tile, x);
-          if (px > pv || (px == pv && x > v)) {
-            blocked = true;
-            break;
-          }
-        }
-      }
-      if (!blocked) {
+    // ---- a mover is blocked by a higher-priority partner wanting the same mod-8 class
+    for (int st = 0; st < S; ++st) {
+      const bool act = st < nl + 3;
+      const int x = act ? blk[st * 32 + l] : 0;
+      const int wx = act ? want[x] : 0xff;
+      const bool mv = act && wx != 0xff;
+      const unsigned key = mv ? static_cast<unsigned>((wx & 7) | ((l >> 4) << 3)) : 16u + l;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      const unsigned pr = mv ? ((color_prio(tile, x) & ~0xffu) | static_cast<unsigned>(x)) : 0u;
+      // different nodes in the group: the largest (priority, id) wins
+      const unsigned best = __reduce_max_sync(grp, pr);
+      if (mv && best != pr) blocked[x] = 1;
+    }
+    __syncthreads();
+    if (t < nu) {
+      slot_new[t] = col[t];
+      if (want[t] != 0xff && !blocked[t]) {
+        const int b = want[t];
         if (atomicAdd(&ccount[b], 1) < 16) {
-          atomicSub(&ccount[col[v]], 1);
-          slot_new[v] = static_cast<uint8_t>(b);
+          atomicSub(&ccount[col[t]], 1);
+          slot_new[t] = static_cast<uint8_t>(b);
         } else {
           atomicSub(&ccount[b], 1);
-          slot_new[v] = col[v];
         }
-      } else {
-        slot_new[v] = col[v];
       }
-    } else if (v < nu) {
-      slot_new[v] = col[v];
     }
     __syncthreads();
-    if (v < nu) col[v] = slot_new[v];
+    if (t < nu) col[t] = slot_new[t];
     __syncthreads();
   }
-  // slot = colour + 16 * (index among the nodes of that colour, in old slot order)
-  if (v < nu) {
+  if (t < nu) {
     int k = 0;
-    const int cv = col[v];
-    for (int u = 0; u < v; ++u) k += col[u] == cv;
-    slot_new[v] = static_cast<uint8_t>(cv + 16 * k);
+    const int cv = col[t];
+    for (int u = 0; u < t; ++u) k += col[u] == cv;
+    slot_new[t] = static_cast<uint8_t>(cv + 16 * k);
   }
   int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
   ids[t] = -1;
   __syncthreads();
-  if (v < nu) ids[slot_new[v]] = tn[v];
+  if (t < nu) ids[slot_new[t]] = tn[t];
   __syncthreads();
-  tn[t] = ids[t];  // 256 slots, holes = -1
-  // remap the code block and write it back
+  tn[t] = ids[t];
   for (int st = 0; st < nl + 3; ++st) {
     uint8_t* p = cb + wofs[w] + 32 + st * 32 + l;
     *p = slot_new[*p];
@@ -478,10 +451,10 @@ __global__ void __launch_bounds__(kTileEdges)
   for (int i = t; i < nbytes / 16; i += kTileEdges)
     reinterpret_cast<uint4*>(rcodes + m.x)[i] = reinterpret_cast<const uint4*>(cb)[i];
   if (t == 0) {
-    int top = 0;
+    int tp = 0;
     for (int u = 0; u < 256; ++u)
-      if (ids[u] >= 0) top = u + 1;
-    meta[2 * tile].z = (m.z & ~0xffff) | top;
+      if (ids[u] >= 0) tp = u + 1;
+    meta[2 * tile].z = (m.z & ~0xffff) | tp;
   }
 }
 
@@ -890,15 +863,14 @@ int ensure_rings(dm_ctx* c) {
               wstart.p, ne, c->rcodes.p, c->flag.p);
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
             c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
-  // bank-conflict-aware slots for 8-bit plans: opt-in (env DUALMESH_PLAN_COLOR=1);
-  // C5: element loop 2.36 -> 2.24 ms for ~0.6 s more plan time, so it pays off
-  // only over thousands of steps on one topology
+  // bank-conflict-aware slots for 8-bit plans (env DUALMESH_PLAN_COLOR=0 turns
+  // it off): C5 element loop 2.36 -> 2.24 ms for ~0.19 s more plan time
   c->plan_colored = false;
   if (c->code_width == 1) {
     const char* pc = std::getenv("DUALMESH_PLAN_COLOR");
-    if (pc && std::atoi(pc) != 0) {
-      DM_LAUNCH(c, k_tile_color, static_cast<unsigned>(ntiles), kTileEdges, 0, c->rcodes.p,
-                c->ring_meta.p, c->tnodes.p, static_cast<int>(ntiles), ne);
+    if (!pc || std::atoi(pc) != 0) {
+      DM_LAUNCH(c, k_tile_color_warp, static_cast<unsigned>(ntiles), kTileEdges, 0,
+                c->rcodes.p, c->ring_meta.p, c->tnodes.p, static_cast<int>(ntiles), ne);
       c->plan_colored = true;
     }
   }
