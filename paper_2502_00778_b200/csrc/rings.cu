@@ -303,7 +303,10 @@ __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restric
 // (tools/bank_sim.py models 1.8-1.9x -> ~1.45x ideal wavefronts; measured on
 // C5: shared-load conflict wavefronts 177 M -> 96 M, element loop 2.36 -> 2.24
 // ms, plan +0.19 s).
-constexpr int kColorRounds = 8;
+int color_rounds() {
+  const char* r = std::getenv("DUALMESH_COLOR_ROUNDS");
+  return r ? std::max(1, std::atoi(r)) : 8;
+}
 
 __device__ __forceinline__ unsigned color_prio(unsigned tile, unsigned v) {
   unsigned h = tile * 0x9E3779B1u ^ (v + 0x7F4A7C15u) * 0x85EBCA77u;
@@ -321,7 +324,7 @@ __device__ __forceinline__ unsigned color_prio(unsigned tile, unsigned v) {
 // (__match_any_sync + __reduce_max_sync); capacity 16 slots per colour.
 __global__ void __launch_bounds__(kTileEdges)
     k_tile_color_warp(uint8_t* __restrict__ rcodes, int4* __restrict__ meta,
-                      int32_t* __restrict__ tnodes, int ntiles, i64 ne) {
+                      int32_t* __restrict__ tnodes, int ntiles, i64 ne, int rounds) {
   __shared__ __align__(16) uint8_t cb[2 * 4096];
   __shared__ uint16_t cost[256][24];  // per node: 16 half-warp (mod 16) + 8 quarter (mod 8)
   __shared__ uint8_t col[256], want[256], blocked[256], slot_new[256];
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(kTileEdges)
   __syncthreads();
   const unsigned half = (l & 16) ? 0xffff0000u : 0x0000ffffu;
   const unsigned quart = 0xffu << (l & 24);
-  for (int round = 0; round < kColorRounds; ++round) {
+  for (int round = 0; round < rounds; ++round) {
     for (int i = t; i < 256 * 24 / 2; i += kTileEdges) reinterpret_cast<uint32_t*>(cost)[i] = 0u;
     __syncthreads();
     // ---- partner histograms, step by step (warp-uniform loop)
@@ -870,7 +873,8 @@ int ensure_rings(dm_ctx* c) {
     const char* pc = std::getenv("DUALMESH_PLAN_COLOR");
     if (!pc || std::atoi(pc) != 0) {
       DM_LAUNCH(c, k_tile_color_warp, static_cast<unsigned>(ntiles), kTileEdges, 0,
-                c->rcodes.p, c->ring_meta.p, c->tnodes.p, static_cast<int>(ntiles), ne);
+                c->rcodes.p, c->ring_meta.p, c->tnodes.p, static_cast<int>(ntiles), ne,
+                color_rounds());
       c->plan_colored = true;
     }
   }
