@@ -373,18 +373,25 @@ __global__ void __launch_bounds__(kTileEdges)
       unsigned h16[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) h16[c] = __ballot_sync(0xffffffffu, cx == c);
-      if (act) {
+      // one lane per (node, half) adds the half-warp counts, one per
+      // (node, quarter) the quarter counts: a node read by several lanes of a
+      // phase is one address (a broadcast), so it counts once
+      const unsigned me = 1u << l;
+      const bool lead16 = act && ((same & half) & (me - 1)) == 0;
+      const bool lead8 = act && ((same & quart) & (me - 1)) == 0;
+      if (lead16) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int n16 = __popc(h16[c] & half & others);
-          if (n16) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][c & ~1]),
-                             static_cast<unsigned>(n16) << (16 * (c & 1)));
+        for (int c = 0; c < 16; c += 2) {
+          const unsigned n0 = __popc(h16[c] & half & others), n1 = __popc(h16[c + 1] & half & others);
+          if (n0 | n1) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][c]), n0 | n1 << 16);
         }
+      }
+      if (lead8) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int n8 = __popc((h16[c] | h16[c + 8]) & quart & others);
-          if (n8) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][16 + (c & ~1)]),
-                            static_cast<unsigned>(n8) << (16 * (c & 1)));
+        for (int c = 0; c < 8; c += 2) {
+          const unsigned n0 = __popc((h16[c] | h16[c + 8]) & quart & others);
+          const unsigned n1 = __popc((h16[c + 1] | h16[c + 9]) & quart & others);
+          if (n0 | n1) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][16 + c]), n0 | n1 << 16);
         }
       }
     }
@@ -410,11 +417,24 @@ __global__ void __launch_bounds__(kTileEdges)
       const int x = act ? blk[st * 32 + l] : 0;
       const int wx = act ? want[x] : 0xff;
       const bool mv = act && wx != 0xff;
-      const unsigned key = mv ? static_cast<unsigned>((wx & 7) | ((l >> 4) << 3)) : 16u + l;
-      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      if (!__any_sync(0xffffffffu, mv)) continue;
       const unsigned pr = mv ? ((color_prio(tile, x) & ~0xffu) | static_cast<unsigned>(x)) : 0u;
-      // different nodes in the group: the largest (priority, id) wins
-      const unsigned best = __reduce_max_sync(grp, pr);
+      // per (mod-8 class, half warp): the largest (priority, id) among the
+      // movers wins (uniform-mask reductions, classes without movers skipped)
+      unsigned best = 0u;
+      const int mk = mv ? (wx & 7) : -1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const unsigned who = __ballot_sync(0xffffffffu, mk == k);
+        if (who & 0x0000ffffu) {
+          const unsigned b = __reduce_max_sync(0xffffffffu, (mk == k && l < 16) ? pr : 0u);
+          if (mk == k && l < 16) best = b;
+        }
+        if (who & 0xffff0000u) {
+          const unsigned b = __reduce_max_sync(0xffffffffu, (mk == k && l >= 16) ? pr : 0u);
+          if (mk == k && l >= 16) best = b;
+        }
+      }
       if (mv && best != pr) blocked[x] = 1;
     }
     __syncthreads();
@@ -434,11 +454,21 @@ __global__ void __launch_bounds__(kTileEdges)
     if (t < nu) col[t] = slot_new[t];
     __syncthreads();
   }
-  if (t < nu) {
-    int k = 0;
-    const int cv = col[t];
-    for (int u = 0; u < t; ++u) k += col[u] == cv;
-    slot_new[t] = static_cast<uint8_t>(cv + 16 * k);
+  // slot = colour + 16 * (rank among the nodes of that colour, in old order):
+  // per-warp colour counts from __match_any_sync, then a prefix over warps
+  __shared__ int wcnt[kTileEdges / 32][17];
+  {
+    const int cv = t < nu ? col[t] : 16;
+    const unsigned same = __match_any_sync(0xffffffffu, cv);
+    if (t < 17 * (kTileEdges / 32)) wcnt[t / 17][t % 17] = 0;
+    __syncthreads();
+    if ((same & ((1u << l) - 1)) == 0) wcnt[w][cv] = __popc(same);
+    __syncthreads();
+    if (t < nu) {
+      int k = __popc(same & ((1u << l) - 1));
+      for (int ww = 0; ww < w; ++ww) k += wcnt[ww][cv];
+      slot_new[t] = static_cast<uint8_t>(cv + 16 * k);
+    }
   }
   int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
   ids[t] = -1;
