@@ -78,3 +78,13 @@ def check_total_volume(mesh: Mesh, volumes: np.ndarray) -> float:
     eng.set_mesh(mesh)
     eng.put_volumes(volumes)
     return eng.check_total_volume()[0]
+
+
+def check_linear_exactness(mesh: Mesh, edges: EdgeList, navs: np.ndarray, volumes: np.ndarray,
+                           A, b) -> float:
+    """affine flux F(x) = A x + b (A: dim x dim); constant
+    flux when A == 0.  trace(A) == 0 with A != 0 raises."""
+    eng = _with_edges(mesh, edges)
+    eng.put_navs(navs)
+    eng.put_volumes(volumes)
+    return eng.check_linear_exactness(A, b)
