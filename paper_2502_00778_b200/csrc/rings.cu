@@ -301,8 +301,8 @@ __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restric
 // class has a higher priority (a fixed hash), capacity permitting.  Slots are
 // only a relabelling of the table, so results do not depend on it
 // (tools/bank_sim.py models 1.8-1.9x -> ~1.45x ideal wavefronts; measured on
-// C5: shared-load conflict wavefronts 177 M -> 96 M, element loop 2.36 -> 2.24
-// ms, plan +0.19 s).
+// C5: shared-load conflict wavefronts 177 M -> 97 M, element loop 2.36 -> 2.25
+// ms, plan +0.1 s).
 int color_rounds() {
   const char* r = std::getenv("DUALMESH_COLOR_ROUNDS");
   return r ? std::max(1, std::atoi(r)) : 8;
@@ -897,7 +897,7 @@ int ensure_rings(dm_ctx* c) {
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
             c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
   // bank-conflict-aware slots for 8-bit plans (env DUALMESH_PLAN_COLOR=0 turns
-  // it off): C5 element loop 2.36 -> 2.24 ms for ~0.19 s more plan time
+  // it off): C5 element loop 2.36 -> 2.25 ms for ~0.1 s more plan time
   c->plan_colored = false;
   if (c->code_width == 1) {
     const char* pc = std::getenv("DUALMESH_PLAN_COLOR");

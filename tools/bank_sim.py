@@ -378,3 +378,54 @@ def refine_parallel(rs, u, slot, rounds=3, nslots=512, seed=0, lanes=32):
         out[r] = c + 16 * nxt[c]
         nxt[c] += 1
     return out
+
+
+def wavefronts_copies(rs, slot, ncopy=2, lanes=32, xor=(0, 4, 2, 6)):
+    """Table with ncopy copies of every node (copy c of slot s at bank index
+    s ^ xor[c]); each access picks a copy greedily per half warp so that the
+    quarter (mod 8) and half (mod 16) phases see distinct banks where
+    possible (same node -> same copy, a broadcast)."""
+    wxy = wz = ixy = iz = 0
+    for w0 in range(0, len(rs), lanes):
+        W = rs[w0:w0 + lanes]
+        S = max(len(s) for s in W)
+        for st in range(S):
+            sl = [slot[s[st]] if st < len(s) else None for s in W]
+            phys = [None] * lanes
+            for h in range(0, lanes, 16):
+                chosen = {}
+                for lane in range(h, h + 16):
+                    v = sl[lane]
+                    if v is None:
+                        continue
+                    if v in chosen:
+                        phys[lane] = chosen[v]
+                        continue
+                    q0 = lane - lane % 8
+                    best = None
+                    for c in range(ncopy):
+                        p = (v ^ xor[c]) + 256 * c
+                        load16 = sum(1 for x in phys[h:h + 16] if x is not None and x % 16 == p % 16 and x != p)
+                        load8 = sum(1 for x in phys[q0:q0 + 8] if x is not None and x % 8 == p % 8 and x != p)
+                        key = (load8 + load16, c)
+                        if best is None or key < best[0]:
+                            best = (key, p)
+                    phys[lane] = best[1]
+                    chosen[v] = best[1]
+            for qd in range(0, lanes, 8):
+                g = defaultdict(set)
+                for x in phys[qd:qd + 8]:
+                    if x is not None:
+                        g[x % 8].add(x)
+                if g:
+                    wxy += max(len(c) for c in g.values())
+                    ixy += 1
+            for hf in range(0, lanes, 16):
+                g = defaultdict(set)
+                for x in phys[hf:hf + 16]:
+                    if x is not None:
+                        g[x % 16].add(x)
+                if g:
+                    wz += max(len(c) for c in g.values())
+                    iz += 1
+    return wxy, wz, ixy, iz
