@@ -74,13 +74,13 @@ __global__ void __launch_bounds__(256)
 }
 
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 8)
     k_vol_elem(const u32* __restrict__ ptr, const int32_t* __restrict__ n2e,
                const double* __restrict__ ve, i64 nv, double* __restrict__ V) {
   const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= nv) return;
-  double acc = 0.0;
-  for (u32 q = ptr[v]; q < ptr[v + 1]; ++q) acc += ve[__ldg(n2e + q)];
+  const double acc =
+      fold_terms(0.0, ptr[v], ptr[v + 1], [&](u32 q) { return __ldg(n2e + q); }, ve);
   V[v] = acc * (1.0 / static_cast<double>(D + 1));
 }
 
