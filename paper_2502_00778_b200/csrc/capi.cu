@@ -59,6 +59,12 @@ int dm_create(dm_ctx** out, int device) {
   auto* c = new dm_ctx;
   c->device = device;
   if (const char* g = std::getenv("DUALMESH_GATHER_CFG")) c->gather_cfg = std::atoi(g);
+  // configurations 20-29 are timing probes that skip work (invalid results):
+  // honoured only with DUALMESH_TIMING_PROBES=1
+  if (c->gather_cfg >= 20 && c->gather_cfg < 30) {
+    const char* pr = std::getenv("DUALMESH_TIMING_PROBES");
+    if (!pr || std::atoi(pr) != 1) c->gather_cfg = 0;
+  }
   int st = check_device(c);
   if (st == DM_OK) {
     cudaError_t e = cudaSetDevice(device);
