@@ -7,16 +7,16 @@
 //                          edge-based dual volumes, fused here
 //                          so K4 never re-reads navs.
 //
-// Variants (north_star (b)):
-//   GATHER (default): one CTA per 256-edge tile.  The tile's slice of the
-//       face-list incidence (ifl, edges.cu) is contiguous; every incidence
-//       (edge e, element E) carries the two nodes of E off the edge plus the
-//       local slots of j and k, so an incidence costs one streaming 8-byte
-//       load and two coordinate gathers -- no dependent connectivity load.
-//       Incidences are evaluated in parallel into shared memory, then each
-//       edge thread folds its own incidences in ascending element id, scales,
-//       adds its boundary terms in ascending facet id, and writes navs and s
-//       once.  That is the serial oracle's summation order: bitwise equal.
+// Variants (dm_navs(ctx, algo, variant)):
+//   GATHER (default, 3D): the ring walk over the Morton-tile plan of rings.cu
+//       (k_navs_ring_pipe): one new table node per incidence, persistent CTAs
+//       with a double-buffered cp.async pipeline; dual-free (K3 in
+//       k_facet_terms + k_ring_boundary) and traditional forms; <= 1e-12 of
+//       the serial loop, deterministic.
+//   GATHER_EXACT: row-table gather (k_navs_gather) summing in ascending
+//       element id -- bitwise the serial oracle; traditional: face list.
+//   GATHER_FACES: one thread per edge over the face-list incidence (ifl),
+//       ascending element id, bitwise (also 2D and the fallbacks).
 //   GATHER_ELEM: the same fold through the element-id CSR (inc) and a
 //       dependent connectivity gather per incidence (kept for comparison).
 //   SCATTER: one thread per element, fp64 atomics (REDG.E.ADD.F64) through
