@@ -179,7 +179,7 @@ int64_t dm_kernel_launches(const dm_ctx* ctx);
  * [1] ring path usable, [2] row tables built, [3] row tables usable,
  * [4] max tile node count (ring path), [5] failure bits of the ring build (2: a tile
  * touches > 1536 nodes, 4: an edge has > 24 incident elements, 8: non-manifold fan,
- * 16: inconsistently oriented fan, 32: ring codes beyond 2 GB),
+ * 16: inconsistently oriented fan, 32: ring codes beyond 64 GB),
  * [6] edge-volume pass walks nodes in Morton order (1) or id order (0),
  * [7] tile tables recoloured against bank conflicts (env DUALMESH_PLAN_COLOR=1). */
 int dm_plan_info(dm_ctx* ctx, int64_t info[8]);

@@ -405,7 +405,7 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
   }
   if (m.y <= kPipeCodeBytes) {
     // code blocks are multiples of 32 bytes: 16-byte pieces
-    const uint4* src = reinterpret_cast<const uint4*>(rcodes + m.x);
+    const uint4* src = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x));
     for (int w = t; w < m.y / 16; w += kEB) cp_async16(&S.cd[b][4 * w], src + w);
   }
   if (t == 0) cp_async16(&S.wo[b], meta + 2 * tile + 1);
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(kEB, MINB)
           q.z = __ldg(mz + r);
           return q;
         };
-        const RingCodes<W> C{rcodes + m.x + wo, lane};
+        const RingCodes<W> C{rcodes + 32 * static_cast<i64>(m.x) + wo, lane};
         if constexpr (ALGO == kTraditional) {
           ring_walk_trad<W>(T, C, acc);
           xk = T(C.slot(1));

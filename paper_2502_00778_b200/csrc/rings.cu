@@ -204,7 +204,7 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
   if (start < 0) start = a[0];
   // step s of this edge lives at out[s * 32]; W == 1: one byte per step
   // after a 32-byte header (n | sign << 5 | boundary << 6 per lane)
-  uint8_t* blk = rcodes + wstart[p >> 5];
+  uint8_t* blk = rcodes + static_cast<i64>(wstart[p >> 5]) * 32;
   uint16_t* out = reinterpret_cast<uint16_t*>(blk) + (p & 31);
   uint8_t* out8 = blk + 32 + (p & 31);
   auto put = [&](int step, unsigned v) {
@@ -249,8 +249,9 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
   }
 }
 
-// Bytes per warp block, S_w = max over the warp's edges of n+3 steps:
-// W == 2: S_w * 32 u16 codes; W == 1: a 32-byte header + S_w * 32 bytes.
+// Size of a warp block in 32-byte units, S_w = max over the warp's edges of
+// n+3 steps: W == 2: S_w * 32 u16 codes; W == 1: a 32-byte header + S_w * 32
+// bytes.
 __global__ void k_ring_warpsize(const int32_t* __restrict__ eperm,
                                 const int32_t* __restrict__ inc_ptr, i64 ne, i64 nwarps, int W,
                                 u32* __restrict__ wsize) {
@@ -261,10 +262,10 @@ __global__ void k_ring_warpsize(const int32_t* __restrict__ eperm,
     const int e = eperm[p];
     S = max(S, inc_ptr[e + 1] - inc_ptr[e] + 3);
   }
-  wsize[w] = static_cast<u32>(W == 2 ? S * 64 : (S + 1) * 32);
+  wsize[w] = static_cast<u32>(W == 2 ? 2 * S : S + 1);  // 32-byte units
 }
 
-// meta[2t]   = {C0, NC, NU | nbnd << 16, bptr}  (C0, NC in bytes)
+// meta[2t]   = {C0, NC, NU | nbnd << 16, bptr}  (C0 in 32-byte units, NC in bytes)
 // meta[2t+1] = eight u16 warp-block byte offsets relative to C0
 __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restrict__ tcnt,
                             const u32* __restrict__ tile_bptr, i64 nwarps, i64 ntiles,
@@ -273,13 +274,13 @@ __global__ void k_ring_meta(const u32* __restrict__ wstart, const u32* __restric
   if (t >= ntiles) return;
   const i64 w0 = t * (kTileEdges / 32);
   const i64 w1 = (w0 + kTileEdges / 32 < nwarps) ? w0 + kTileEdges / 32 : nwarps;
-  const u32 C0 = wstart[w0], C1 = wstart[w1];
+  const u32 C0 = wstart[w0], C1 = wstart[w1];  // 32-byte units
   const int nb = static_cast<int>(tile_bptr[t + 1] - tile_bptr[t]);  // <= 3 * 256
-  meta[2 * t] = make_int4(static_cast<int>(C0), static_cast<int>(C1 - C0),
+  meta[2 * t] = make_int4(static_cast<int>(C0), static_cast<int>(32 * (C1 - C0)),
                           static_cast<int>(tcnt[t]) | nb << 16, static_cast<int>(tile_bptr[t]));
   unsigned o[4] = {0u, 0u, 0u, 0u};
   for (i64 w = w0; w < w1; ++w) {
-    const u32 off = min(wstart[w] - C0, 0xffffu);
+    const u32 off = min(32 * (wstart[w] - C0), 0xffffu);
     const int q = static_cast<int>(w - w0);
     o[q >> 1] |= off << (16 * (q & 1));
   }
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(kTileEdges)
   const int nu = m.z & 0xffff, nbytes = m.y;
   if (nu > 256 || nbytes > static_cast<int>(sizeof(cb))) return;
   for (int i = t; i < nbytes / 16; i += kTileEdges)
-    reinterpret_cast<uint4*>(cb)[i] = reinterpret_cast<const uint4*>(rcodes + m.x)[i];
+    reinterpret_cast<uint4*>(cb)[i] = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x))[i];
   const i64 left = ne - static_cast<i64>(tile) * kTileEdges;
   const int nw = static_cast<int>(left >= kTileEdges ? kTileEdges / 32 : (left + 31) / 32);
   if (t <= kTileEdges / 32) {
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(kTileEdges)
   }
   __syncthreads();
   for (int i = t; i < nbytes / 16; i += kTileEdges)
-    reinterpret_cast<uint4*>(rcodes + m.x)[i] = reinterpret_cast<const uint4*>(cb)[i];
+    reinterpret_cast<uint4*>(rcodes + 32 * static_cast<i64>(m.x))[i] = reinterpret_cast<const uint4*>(cb)[i];
   if (t == 0) {
     int tp = 0;
     for (int u = 0; u < 256; ++u)
@@ -546,25 +547,26 @@ __device__ __forceinline__ u64 spread21(u64 v) {  // bit i -> bit 3i
   return v;
 }
 
-// Origin order key.  cell_shift == 0: the Morton key of the node's 21-bit
-// quantised position.  cell_shift > 0: the Morton key of its coarse cell
-// (position >> cell_shift) above the node id, i.e. cells in Z-order and the
+// Origin order key.  cells == 0: the Morton key of the node's 21-bit
+// quantised position.  cells > 0: the Morton key of its coarse cell (the
+// bounding cube split into cells^3, any cell count) above the node id, i.e.
+// cells in Z-order and the
 // nodes of a cell in id order -- for a numbering with runs of consecutive ids
 // along a row, a cell's rows become runs of consecutive origins, whose edge
 // ranges are adjacent in the edge list (coalesced output stores).
 __global__ void k_morton(const d4* __restrict__ x4, i64 nv, double lx, double ly, double lz,
-                         double sc, int cell_shift, u64* __restrict__ key,
+                         double sc, int cells, u64* __restrict__ key,
                          int32_t* __restrict__ id) {
   const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const d4 r = x4[v];
-  auto q = [&](double x, int sh) -> u64 {
+  auto q = [&](double x) -> u64 {
     const double f = x * sc;
-    return (f <= 0.0 ? 0ull : (f >= 2097151.0 ? 2097151ull : static_cast<u64>(f))) >> sh;
+    const u64 q21 = f <= 0.0 ? 0ull : (f >= 2097151.0 ? 2097151ull : static_cast<u64>(f));
+    return cells ? (q21 * static_cast<u64>(cells)) >> 21 : q21;
   };
-  const u64 m = spread21(q(r.x - lx, cell_shift)) | spread21(q(r.y - ly, cell_shift)) << 1 |
-                spread21(q(r.z - lz, cell_shift)) << 2;
-  key[v] = cell_shift ? (m << 32 | static_cast<u64>(v)) : m;
+  const u64 m = spread21(q(r.x - lx)) | spread21(q(r.y - ly)) << 1 | spread21(q(r.z - lz)) << 2;
+  key[v] = cells ? (m << 32 | static_cast<u64>(v)) : m;
   id[v] = static_cast<int32_t>(v);
 }
 
@@ -707,9 +709,9 @@ int build_edge_order(dm_ctx* c) {
   int32_t* i1p = c->morder.p;
   DevBuf<unsigned char> tmp;
   size_t tb = 0;
-  auto sort_nodes = [&](int cell_shift) -> int {
+  auto sort_nodes = [&](int cells) -> int {
     DM_LAUNCH(c, k_morton, grid_for(nv, 256), 256, 0, c->x4.p, nv, lo[0], lo[1], lo[2], sc,
-              cell_shift, k0.p, i0.p);
+              cells, k0.p, i0.p);
     size_t need = 0;
     DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, need, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
                                              c->stream));
@@ -737,15 +739,15 @@ int build_edge_order(dm_ctx* c) {
     DM_CK(c, cudaStreamSynchronize(c->stream));
     c->vol_by_rank = static_cast<double>(near) < 0.25 * static_cast<double>(nv);
   }
-  // cells of ~cell_nodes nodes (env DUALMESH_CELL_NODES, 0 = plain Morton
-  // always): 2^b cells per axis, b <= 10 so the key (3b + 32 bits) fits
+  // cells of ~cell_nodes nodes (env DUALMESH_CELL_NODES, 0 = plain Morton always)
   double cell_nodes = 64.0;
   if (const char* cn = std::getenv("DUALMESH_CELL_NODES")) cell_nodes = std::atof(cn);
   if (!c->vol_by_rank && cell_nodes > 0.0 && nv > 0) {
-    const double per_axis = std::cbrt(static_cast<double>(nv) / cell_nodes);
-    const int b = std::max(
-        1, std::min(10, static_cast<int>(std::lround(std::log2(std::max(per_axis, 2.0))))));
-    st = sort_nodes(21 - b);
+    // cells^3 cells of ~cell_nodes nodes on a cubic grid (at most 1024 per
+    // axis so the key, 3*10 + 32 bits, fits)
+    const int cells = static_cast<int>(std::max<long>(
+        1, std::min<long>(1024, std::lround(std::cbrt(static_cast<double>(nv) / cell_nodes)))));
+    st = sort_nodes(cells);
     if (st) return st;
   }
   // edge permutation: each origin's edge range appended whole, in that order
@@ -871,7 +873,7 @@ int ensure_rings(dm_ctx* c) {
     unsigned long long h = 0;
     DM_CK(c, cudaMemcpyAsync(&h, tot.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     DM_CK(c, cudaStreamSynchronize(c->stream));
-    if (h + 16 >= (1ull << 31)) {  // offsets live in int4 metadata: bit-exact path beyond 2 GB
+    if (h + 1 >= (1ull << 31)) {  // 32-byte units in int4 metadata: bit-exact path beyond 64 GB
       c->ring_fail = 32;
       c->ring_ok = false;
       c->have_rings = true;
@@ -880,12 +882,13 @@ int ensure_rings(dm_ctx* c) {
   }
   int st = scan_exclusive(c, wstart.p, wstart.p, nwarps);
   if (st) return st;
-  u32 nbytes = 0;
-  DM_CK(c, cudaMemcpyAsync(&nbytes, wstart.p + nwarps, sizeof(u32), cudaMemcpyDeviceToHost,
+  u32 nunits = 0;
+  DM_CK(c, cudaMemcpyAsync(&nunits, wstart.p + nwarps, sizeof(u32), cudaMemcpyDeviceToHost,
                            c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
-  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(nbytes) + 16));
-  DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, static_cast<size_t>(nbytes) + 16, c->stream));
+  const size_t nbytes = 32 * static_cast<size_t>(nunits);
+  DM_CK(c, c->rcodes.ensure(nbytes + 16));
+  DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, nbytes + 16, c->stream));
   if (c->code_width == 1)
     DM_LAUNCH(c, k_ring_codes<1>, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p,
               c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p,
