@@ -423,3 +423,26 @@ def test_colored_plan_same_bits(name, scale, monkeypatch):
             eng.close()
     np.testing.assert_array_equal(out[0][0], out[1][0])
     np.testing.assert_array_equal(out[0][1], out[1][1])
+
+
+def test_twice_c5_scale():
+    """A 320^3 Kuhn cube (196.6 M tets, 230 M edges; device-generated): the
+    ring plan (codes beyond 2 GB, coloured 256-node tables) and the SPEC
+    identities at twice the BASELINE size."""
+    from paper_2502_00778_b200 import Engine
+    eng = Engine(0)
+    try:
+        eng.gen_tet_box(320, 320, 320, None, 0, 0.15, 42)
+        assert eng.build_edges() == 230298560
+        eng.navs(DF, GATHER)
+        eng.volumes(EDGE)
+        info = eng.plan_info()
+        assert info["ring_ok"] and info["colored"]
+        r, ri = eng.check_closure()
+        assert r <= 1e-13 and ri <= 1e-13
+        rel, sv, _ = eng.check_total_volume()
+        assert rel <= 1e-12 and abs(sv - 1.0) <= 1e-12
+        A = np.array([[0.3, 0.1, 0.0], [0.0, 0.5, 0.2], [0.1, 0.0, 0.4]])
+        assert eng.check_linear_exactness(A, np.array([0.1, -0.2, 0.3])) <= 1e-11
+    finally:
+        eng.close()
