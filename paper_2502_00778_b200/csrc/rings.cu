@@ -570,6 +570,43 @@ __global__ void k_morton(const d4* __restrict__ x4, i64 nv, double lx, double ly
   id[v] = static_cast<int32_t>(v);
 }
 
+// Per-axis quantile cells: the cell index of a node along an axis is its rank
+// in that coordinate (sorted) scaled to `cells` -- equal node counts per slab,
+// so graded / stretched grids (boundary layers) get cells of ~cell_nodes
+// nodes like uniform ones.
+__global__ void k_axis_key(const d4* __restrict__ x4, i64 nv, int axis, u64* __restrict__ key,
+                           int32_t* __restrict__ id) {
+  const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const d4 r = x4[v];
+  const double x = axis == 0 ? r.x : (axis == 1 ? r.y : r.z);
+  const u64 b = static_cast<u64>(__double_as_longlong(x));
+  key[v] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // order-preserving
+  id[v] = static_cast<int32_t>(v);
+}
+
+__global__ void k_axis_cell(const int32_t* __restrict__ sorted, i64 nv, int axis, int cells,
+                            u32* __restrict__ cellpack) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= nv) return;
+  const u32 ci = static_cast<u32>((static_cast<u64>(r) * static_cast<u64>(cells)) /
+                                  static_cast<u64>(nv));
+  const int v = sorted[r];
+  if (axis == 0) cellpack[v] = ci;
+  else cellpack[v] |= ci << (10 * axis);
+}
+
+__global__ void k_cell_key(const u32* __restrict__ cellpack, i64 nv, u64* __restrict__ key,
+                           int32_t* __restrict__ id) {
+  const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const u32 c = cellpack[v];
+  const u64 m = spread21(c & 1023u) | spread21((c >> 10) & 1023u) << 1 |
+                spread21((c >> 20) & 1023u) << 2;
+  key[v] = m << 32 | static_cast<u64>(v);
+  id[v] = static_cast<int32_t>(v);
+}
+
 __global__ void k_origin_count(const int32_t* __restrict__ ord, const u32* __restrict__ os, i64 nv,
                                u32* __restrict__ cnt) {
   const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -709,9 +746,7 @@ int build_edge_order(dm_ctx* c) {
   int32_t* i1p = c->morder.p;
   DevBuf<unsigned char> tmp;
   size_t tb = 0;
-  auto sort_nodes = [&](int cells) -> int {
-    DM_LAUNCH(c, k_morton, grid_for(nv, 256), 256, 0, c->x4.p, nv, lo[0], lo[1], lo[2], sc,
-              cells, k0.p, i0.p);
+  auto radix = [&]() -> int {  // (k0, i0) -> sorted ids in i1p
     size_t need = 0;
     DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, need, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
                                              c->stream));
@@ -720,9 +755,14 @@ int build_edge_order(dm_ctx* c) {
       DM_CK(c, tmp.ensure(need));
       tb = need;
     }
-    DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, need, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
+    DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, need, k0.p, k1.p, i0.p, i1p, nv, 0, 64,
                                              c->stream));
     return DM_OK;
+  };
+  auto sort_nodes = [&](int cells) -> int {
+    DM_LAUNCH(c, k_morton, grid_for(nv, 256), 256, 0, c->x4.p, nv, lo[0], lo[1], lo[2], sc,
+              cells, k0.p, i0.p);
+    return radix();
   };
   int st = sort_nodes(0);
   if (st) return st;
@@ -747,8 +787,18 @@ int build_edge_order(dm_ctx* c) {
     // axis so the key, 3*10 + 32 bits, fits)
     const int cells = static_cast<int>(std::max<long>(
         1, std::min<long>(1024, std::lround(std::cbrt(static_cast<double>(nv) / cell_nodes)))));
-    st = sort_nodes(cells);
+    DevBuf<u32> cellpack;
+    DM_CK(c, cellpack.ensure(nv));
+    for (int axis = 0; axis < 3; ++axis) {
+      DM_LAUNCH(c, k_axis_key, grid_for(nv, 256), 256, 0, c->x4.p, nv, axis, k0.p, i0.p);
+      st = radix();
+      if (st) return st;
+      DM_LAUNCH(c, k_axis_cell, grid_for(nv, 256), 256, 0, i1p, nv, axis, cells, cellpack.p);
+    }
+    DM_LAUNCH(c, k_cell_key, grid_for(nv, 256), 256, 0, cellpack.p, nv, k0.p, i0.p);
+    st = radix();
     if (st) return st;
+    DM_CK(c, cudaStreamSynchronize(c->stream));  // cellpack dies here
   }
   // edge permutation: each origin's edge range appended whole, in that order
   u32* pstart = nullptr;
