@@ -127,6 +127,7 @@ struct dm_ctx {
   // generic scratch
   dm::DevBuf<dm::u32> cnt, fill;
   dm::DevBuf<dm::u64> tmp64;
+  dm::DevBuf<dm::u32> seg_big;  // segment_sort: ids of segments longer than a warp's
   dm::DevBuf<dm::u32> scan_tmp;
   dm::DevBuf<int> flag;
 
@@ -267,6 +268,10 @@ int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n);
 // Sort each segment [seg[s], seg[s+1]) of data ascending; segments up to
 // 4096 keys (larger ones set *flag = 1).  Keys are u32 or u64.
 int segment_sort_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg);
+// Keys unique within each segment (K1 payloads, boundary pairs); with ucnt,
+// ucnt[s] := number of distinct high words in segment s.
+int segment_sort_unique_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg, u32* ucnt);
+// u32 keys must be unique within each segment (edge / element ids).
 int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg);
 // (key, value) pairs sorted lexicographically within each segment.
 int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg);

@@ -8,7 +8,8 @@
 //               mesh.cpp:17 (3D) / mesh.cpp:263-265 (2D)
 //   bucket    : the origin j = min(a,b) of the pair (counting sort, atomics)
 //   payload   : (k << 32) | (e*L + l), k = max(a,b)
-//   per bucket: bitonic sort of the payloads -> (k, e*L+l) ascending
+//   per bucket: rank sort of the payloads -> (k, e*L+l) ascending, counting
+//               the distinct k on the way
 // The concatenated buckets are then sorted by (j, k, e) -- exactly the
 // lexicographic edge order of the reference with, per edge, its incident
 // elements in ascending id.  Atomic placement order is erased by the sort
@@ -68,22 +69,6 @@ __global__ void k_scatter(const int32_t* el, i64 nE, const u32* bstart, u32* fil
     const u32 pos = bstart[j] + atomicAdd(fill + j, 1u);
     out[pos] = (static_cast<u64>(static_cast<u32>(k)) << 32) | static_cast<u64>(e * L + l);
   }
-}
-
-// Warp per bucket: number of distinct k (= edges with origin j).
-__global__ void k_count_unique(const u64* items, const u32* bstart, i64 nv, u32* ucnt) {
-  const int lane = threadIdx.x & 31;
-  const i64 j = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (j >= nv) return;
-  const u32 b = bstart[j], n = bstart[j + 1] - b;
-  u32 total = 0;
-  for (u32 i0 = 0; i0 < n; i0 += 32) {
-    const u32 i = i0 + lane;
-    bool head = false;
-    if (i < n) head = (i == 0) || ((items[b + i] >> 32) != (items[b + i - 1] >> 32));
-    total += __popc(__ballot_sync(0xffffffffu, head));
-  }
-  if (lane == 0) ucnt[j] = total;
 }
 
 // Face-list incidence entry for element E seen from its local edge l:
@@ -177,11 +162,10 @@ int build_edges_impl(dm_ctx* c) {
   } else {
     DM_LAUNCH(c, k_scatter<2>, ge, 256, 0, c->elems.p, c->nE, c->cnt.p, c->fill.p, c->tmp64.p);
   }
-  st = segment_sort_u64(c, c->tmp64.p, c->cnt.p, nv);
+  // sort each bucket; fill := distinct k per bucket (edges per origin)
+  st = segment_sort_unique_u64(c, c->tmp64.p, c->cnt.p, nv, c->fill.p);
   if (st) return st;
-  // unique counts -> origin_start
   DM_CK(c, c->os.ensure(static_cast<size_t>(nv + 1)));
-  DM_LAUNCH(c, k_count_unique, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, nv, c->fill.p);
   st = scan_exclusive(c, c->fill.p, c->os.p, nv);
   if (st) return st;
   u32 ne32 = 0;
@@ -202,7 +186,8 @@ int build_edges_impl(dm_ctx* c) {
   }
   DM_LAUNCH(c, k_set_i32, 1, 1, 0, c->inc_ptr.p + c->ne, static_cast<int32_t>(M));
   DM_CK(c, cudaStreamSynchronize(c->stream));
-  c->tmp64.release();
+  // tmp64 stays allocated: re-extraction (remeshing loops) must not pay a
+  // cudaMalloc/cudaFree pair, which stalls the device for up to ~0.3 s
   c->have_edges = true;
   return DM_OK;
 }
@@ -388,7 +373,7 @@ int ensure_bedge(dm_ctx* c) {
     DM_LAUNCH(c, k_bedge_scatter<2>, grid_for(n, 256), 256, 0, c->bnd.p, c->nB, c->edges.p,
               c->os.p, nv, c->cnt.p, c->fill.p, c->bedge.p);
   }
-  st = segment_sort_u64(c, c->bedge.p, c->cnt.p, nv);
+  st = segment_sort_unique_u64(c, c->bedge.p, c->cnt.p, nv, nullptr);
   if (st) return st;
   // per-tile slices of the sorted (edge, facet) list, so no kernel searches it
   const i64 ntiles = (c->ne + kTileEdges - 1) / kTileEdges;

@@ -578,7 +578,8 @@ __global__ void __launch_bounds__(kEB, MINB)
     const int nxt = tile + G;
     // FAKE (timing probes only, results invalid): 1 conflict-free table
     // slots, 2 no stores, 4 no coordinate fill after the first two tiles,
-    // 8 no ring walk
+    // 8 no ring walk, 16 component-major navs stores, 32 one 32-byte row
+    // (navs, s) per edge
     if (nxt < ntiles) {
       if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false>(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
       else pipe_issue(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
@@ -659,10 +660,29 @@ __global__ void __launch_bounds__(kEB, MINB)
       // scale pass; boundary edges get their facet terms (and s) from
       // k_ring_boundary, launched right after on the same stream
       edge_tail_values<3, ALGO>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
-      if (!(FAKE & 2) || s == -12345.0)
+      if (!(FAKE & 34) || s == -12345.0)
         svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
     }
-    if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) store_nav_row(navs, e, nv);
+    if (FAKE & 32) {  // probe: one 32-byte (x, y, z, s) row per edge
+      if (valid) {
+        i64 r = 4 * static_cast<i64>(e);
+        if (r + 4 > 3 * ne) r -= 3 * ne - 4;
+        d4 q;
+        q.x = nv[0];
+        q.y = nv[1];
+        q.z = nv[2];
+        q.w = s;
+        *reinterpret_cast<d4*>(navs + (r & ~3ll)) = q;
+      }
+    } else if (FAKE & 16) {  // probe: component-major (SoA) navs stores
+      if (valid) {
+        navs[e] = nv[0];
+        navs[ne + e] = nv[1];
+        navs[2 * ne + e] = nv[2];
+      }
+    } else if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) {
+      store_nav_row(navs, e, nv);
+    }
     __syncthreads();  // buffer b is refilled next iteration
   }
   cp_async_wait<0>();
@@ -954,6 +974,9 @@ int launch_navs(dm_ctx* c, int variant) {
           case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8>, sizeof(PipeSmem<256>)); break;
           case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6>, sizeof(PipeSmem<256>)); break;
           case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14>, sizeof(PipeSmem<256>)); break;
+          case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16>, sizeof(PipeSmem<256>)); break;
+          case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3>, sizeof(PipeSmem<256>)); break;
+          case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32>, sizeof(PipeSmem<256>)); break;
           default: st = launch(k_navs_ring_pipe<256, 4, 1>, sizeof(PipeSmem<256>)); break;
         }
       } else {

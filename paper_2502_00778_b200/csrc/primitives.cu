@@ -110,32 +110,89 @@ __device__ void bitonic(K* buf, int P, int tid, int nthr) {
 constexpr int kWarpSeg = 128;
 constexpr int kBlockSeg = 4096;
 
-template <typename K>
+// Warp per segment of <= kWarpSeg keys: rank sort.  The segment is staged in
+// shared memory; each lane holds up to four keys and counts the keys below
+// each of them with broadcast reads (one wavefront per read, no bitonic
+// exchange traffic: 36 keys cost 36 broadcast loads instead of ~340
+// conflict-free exchange wavefronts); ties broken by position unless the
+// caller guarantees unique keys.  The sorted run is written back coalesced.
+// With `ucnt` (u64 keys only) the warp also counts distinct high words
+// (distinct k per origin bucket in K1) -- replacing a separate pass.
+template <typename K, bool kUnique, int R>
+__device__ __forceinline__ void rank_keys(const K* buf, int n, const K (&key)[4], int lane,
+                                          int (&cnt)[4]) {
+  for (int i = 0; i < n; i += 2) {  // buf[n] is padded with key_max
+    const K v0 = buf[i], v1 = buf[i + 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (kUnique) {
+        cnt[r] += (v0 < key[r]) + (v1 < key[r]);
+      } else {
+        const int me = lane + 32 * r;
+        cnt[r] += ((v0 < key[r]) | ((v0 == key[r]) & (i < me))) +
+                  ((v1 < key[r]) | ((v1 == key[r]) & (i + 1 < me)));
+      }
+    }
+  }
+}
+
+template <typename K, bool kUnique>
 __global__ void __launch_bounds__(256)
-    k_segsort_warp(K* data, const u32* seg, i64 nseg, u32* big, int* nbig) {
-  __shared__ K sbuf[8][kWarpSeg];
+    k_segsort_warp(K* data, const u32* seg, i64 nseg, u32* big, int* nbig, u32* ucnt) {
+  __shared__ __align__(16) K sbuf[8][kWarpSeg + 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 s = static_cast<i64>(blockIdx.x) * 8 + warp;
   if (s >= nseg) return;
   const u32 b = seg[s];
   const int n = static_cast<int>(seg[s + 1] - b);
-  if (n <= 1) return;
+  if (n <= 1) {
+    if (ucnt && lane == 0) ucnt[s] = static_cast<u32>(n);
+    return;
+  }
   if (n > kWarpSeg) {
     if (lane == 0) big[atomicAdd(nbig, 1)] = static_cast<u32>(s);
     return;
   }
-  int P = 2;
-  while (P < n) P <<= 1;
   K* buf = sbuf[warp];
-  for (int i = lane; i < P; i += 32) buf[i] = i < n ? data[b + i] : key_max<K>();
+  K key[4];
+  int cnt[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = lane + 32 * r;
+    key[r] = i < n ? data[b + i] : key_max<K>();
+    if (i < kWarpSeg + 2) buf[i] = key[r];
+  }
+  if (lane < 2) buf[kWarpSeg + lane] = key_max<K>();
   __syncwarp();
-  bitonic<K, true>(buf, P, lane, 32);
+  const int nr = (n + 31) >> 5;
+  if (nr == 1) rank_keys<K, kUnique, 1>(buf, n, key, lane, cnt);
+  else if (nr == 2) rank_keys<K, kUnique, 2>(buf, n, key, lane, cnt);
+  else if (nr == 3) rank_keys<K, kUnique, 3>(buf, n, key, lane, cnt);
+  else rank_keys<K, kUnique, 4>(buf, n, key, lane, cnt);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (lane + 32 * r < n) buf[cnt[r]] = key[r];
+  __syncwarp();
+  if constexpr (sizeof(K) == 8) {
+    if (ucnt) {
+      u32 heads = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = lane + 32 * r;
+        const bool h = i < n && (i == 0 || (buf[i] >> 32) != (buf[i - 1] >> 32));
+        heads += __popc(__ballot_sync(0xffffffffu, h));
+      }
+      if (lane == 0) ucnt[s] = heads;
+    }
+  }
   for (int i = lane; i < n; i += 32) data[b + i] = buf[i];
 }
 
 template <typename K>
 __global__ void __launch_bounds__(512)
-    k_segsort_block(K* data, const u32* seg, const u32* big, const int* nbig, int* flag) {
+    k_segsort_block(K* data, const u32* seg, const u32* big, const int* nbig, int* flag,
+                    u32* ucnt) {
   extern __shared__ unsigned char smem_raw[];
   K* buf = reinterpret_cast<K*>(smem_raw);
   const int count = *nbig;
@@ -153,25 +210,36 @@ __global__ void __launch_bounds__(512)
     __syncthreads();
     bitonic<K, false>(buf, P, threadIdx.x, blockDim.x);
     for (int i = threadIdx.x; i < n; i += blockDim.x) data[b + i] = buf[i];
+    if constexpr (sizeof(K) == 8) {
+      if (ucnt) {
+        int heads = 0;
+        for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+          const int i = i0 + threadIdx.x;
+          heads += __syncthreads_count(i < n && (i == 0 || (buf[i] >> 32) != (buf[i - 1] >> 32)));
+        }
+        if (threadIdx.x == 0) ucnt[s] = static_cast<u32>(heads);
+      }
+    }
     __syncthreads();
   }
 }
 
-template <typename K>
-int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg) {
+template <typename K, bool kUnique>
+int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg, u32* ucnt) {
   if (nseg <= 0) return DM_OK;
-  DevBuf<u32> big;
+  DevBuf<u32>& big = c->seg_big;  // persistent scratch (no free/malloc stalls)
   DM_CK(c, big.ensure(static_cast<size_t>(nseg)));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
   int* nbig = c->flag.p + 1;
-  DM_LAUNCH(c, k_segsort_warp<K>, grid_for(nseg, 8), 256, 0, data, seg, nseg, big.p, nbig);
+  DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg, big.p,
+            nbig, ucnt);
   const size_t smem = kBlockSeg * sizeof(K);
   DM_CK(c, cudaFuncSetAttribute(k_segsort_block<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  DM_LAUNCH(c, k_segsort_block<K>, 296, 512, smem, data, seg, big.p, nbig, c->flag.p);
+  DM_LAUNCH(c, k_segsort_block<K>, 296, 512, smem, data, seg, big.p, nbig, c->flag.p, ucnt);
   int f = 0;
-  int st = read_flag(c, &f);  // also keeps `big` alive until the sort finished
+  int st = read_flag(c, &f);
   if (st) return st;
   if (f) return fail(c, DM_ERR_UNSUPPORTED, "segment longer than 4096 keys (node valence too high)");
   return DM_OK;
@@ -264,7 +332,7 @@ __global__ void __launch_bounds__(512)
 
 int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg) {
   if (nseg <= 0) return DM_OK;
-  DevBuf<u32> big;
+  DevBuf<u32>& big = c->seg_big;  // persistent scratch (no free/malloc stalls)
   DM_CK(c, big.ensure(static_cast<size_t>(nseg)));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
@@ -294,10 +362,13 @@ int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n) {
 }
 
 int segment_sort_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg) {
-  return segment_sort<u64>(c, data, seg, nseg);
+  return segment_sort<u64, false>(c, data, seg, nseg, nullptr);
+}
+int segment_sort_unique_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg, u32* ucnt) {
+  return segment_sort<u64, true>(c, data, seg, nseg, ucnt);
 }
 int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg) {
-  return segment_sort<u32>(c, data, seg, nseg);
+  return segment_sort<u32, true>(c, data, seg, nseg, nullptr);
 }
 
 int read_flag(dm_ctx* c, int* value) {

@@ -61,6 +61,9 @@
 
 #include "dm_internal.cuh"
 
+#include <chrono>
+#include <cstdio>
+
 namespace dm {
 namespace {
 
@@ -702,6 +705,28 @@ __global__ void k_morton_coords(const d4* __restrict__ x4, const int32_t* __rest
   z[r] = p.z;
 }
 
+// Host phase timer of the plan (env DUALMESH_PLAN_TIMING=1): synchronises the
+// stream at each mark and prints the wall time since the previous one.
+struct PlanClock {
+  dm_ctx* c;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PlanClock(dm_ctx* ctx) : c(ctx) {
+    const char* e = std::getenv("DUALMESH_PLAN_TIMING");
+    on = e && std::atoi(e) == 1;
+    if (on) cudaStreamSynchronize(c->stream);
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(c->stream);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[plan] %-22s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 int bits_for(u64 v) {
   int b = 1;
   while (b < 64 && (v >> b)) ++b;
@@ -710,6 +735,7 @@ int bits_for(u64 v) {
 
 // eperm (Morton origin order), bedge_p and its per-tile slices.
 int build_edge_order(dm_ctx* c) {
+  PlanClock clk(c);
   const i64 nv = c->nv, ne = c->ne, nb = c->n_bedge;
   const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
   // bounding box
@@ -730,6 +756,7 @@ int build_edge_order(dm_ctx* c) {
   double ext = std::max(hi[0] - lo[0], std::max(hi[1] - lo[1], hi[2] - lo[2]));
   if (!(ext > 0.0) || !std::isfinite(ext)) ext = 1.0;
   const double sc = 2097151.0 / ext;
+  clk.mark("bbox");
   // Origin order.  First the plain Morton order of the nodes; if the node
   // numbering turns out to be spatially coherent (many id-consecutive nodes
   // within 8 Morton ranks), re-sort by (Morton key of a ~64-node cell, node
@@ -766,6 +793,7 @@ int build_edge_order(dm_ctx* c) {
   };
   int st = sort_nodes(0);
   if (st) return st;
+  clk.mark("morton sort");
   {
     DevBuf<int32_t> rk;
     DevBuf<u32> cnt;
@@ -779,6 +807,7 @@ int build_edge_order(dm_ctx* c) {
     DM_CK(c, cudaStreamSynchronize(c->stream));
     c->vol_by_rank = static_cast<double>(near) < 0.25 * static_cast<double>(nv);
   }
+  clk.mark("locality");
   // cells of ~cell_nodes nodes (env DUALMESH_CELL_NODES, 0 = plain Morton always)
   double cell_nodes = 64.0;
   if (const char* cn = std::getenv("DUALMESH_CELL_NODES")) cell_nodes = std::atof(cn);
@@ -800,6 +829,7 @@ int build_edge_order(dm_ctx* c) {
     if (st) return st;
     DM_CK(c, cudaStreamSynchronize(c->stream));  // cellpack dies here
   }
+  clk.mark("quantile cells");
   // edge permutation: each origin's edge range appended whole, in that order
   u32* pstart = nullptr;
   DevBuf<int32_t> pinv;
@@ -812,6 +842,7 @@ int build_edge_order(dm_ctx* c) {
   if (st) return st;
   DM_LAUNCH(c, k_eperm, grid_for(nv, 256), 256, 0, i1p, c->os.p, pstart, nv, c->eperm.p,
             pinv.p);
+  clk.mark("eperm");
   // Edge-volume terms (vol_by_rank decided above): for a spatially coherent
   // numbering the edge-id order is already local, so s goes to svals[e] and
   // the id-order volume pass reads it coalesced; otherwise s stays in position
@@ -828,6 +859,7 @@ int build_edge_order(dm_ctx* c) {
               c->rin_ptr.p, nv, c->rin_list.p);
   }
 
+  clk.mark("rank incoming");
   // boundary (edge, facet) list re-keyed by position
   DM_CK(c, c->bedge_p.ensure(nb > 0 ? nb : 1));
   DM_CK(c, c->tile_bptr_p.ensure(ntiles + 1));
@@ -862,6 +894,7 @@ int build_edge_order(dm_ctx* c) {
     c->n_bseg = ns;
   }
   DM_CK(c, cudaStreamSynchronize(c->stream));  // scratch buffers die here
+  clk.mark("boundary lists");
   return DM_OK;
 }
 
@@ -869,8 +902,10 @@ int build_edge_order(dm_ctx* c) {
 
 int ensure_rings(dm_ctx* c) {
   if (c->have_rings) return DM_OK;
+  PlanClock clk(c);
   int st0 = ensure_bedge(c);  // tile_bptr feeds the ring metadata
   if (st0) return st0;
+  clk.mark("boundary edges");
   if (c->dim != 3) {
     c->ring_ok = false;
     c->have_rings = true;
@@ -886,6 +921,7 @@ int ensure_rings(dm_ctx* c) {
   }
   int st1 = build_edge_order(c);
   if (st1) return st1;
+  clk.mark("edge order (total)");
   DM_CK(c, c->tnodes.ensure(static_cast<size_t>(ntiles * kTileNodeCap)));
   DM_CK(c, c->tnode_cnt.ensure(static_cast<size_t>(ntiles)));
   // tiles that overflow the caps keep count 0 (their codes are never used:
@@ -910,6 +946,7 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, cudaMemcpyAsync(fl0, c->flag.p, sizeof(fl0), cudaMemcpyDeviceToHost, c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
   c->code_width = fl0[1] <= 256 ? 1 : 2;
+  clk.mark("tile nodes");
   DevBuf<u32> wstart;
   DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
   DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->eperm.p, c->inc_ptr.p, ne,
@@ -937,6 +974,7 @@ int ensure_rings(dm_ctx* c) {
                            c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
   const size_t nbytes = 32 * static_cast<size_t>(nunits);
+  clk.mark("code offsets");
   DM_CK(c, c->rcodes.ensure(nbytes + 16));
   DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, nbytes + 16, c->stream));
   if (c->code_width == 1)
@@ -949,6 +987,7 @@ int ensure_rings(dm_ctx* c) {
               wstart.p, ne, c->rcodes.p, c->flag.p);
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
             c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
+  clk.mark("ring codes");
   // bank-conflict-aware slots for 8-bit plans (env DUALMESH_PLAN_COLOR=0 turns
   // it off): C5 element loop 2.36 -> 2.25 ms for ~0.1 s more plan time
   c->plan_colored = false;
@@ -968,7 +1007,10 @@ int ensure_rings(dm_ctx* c) {
   c->ring_max_nodes = fl[1];
   c->ring_ok = (fl[0] == 0);
   c->have_rings = true;
-  return c->ring_ok ? refresh_ring_coords(c) : DM_OK;
+  clk.mark("colouring");
+  const int st2 = c->ring_ok ? refresh_ring_coords(c) : DM_OK;
+  clk.mark("coords");
+  return st2;
 }
 
 int refresh_ring_coords(dm_ctx* c) {
