@@ -229,6 +229,11 @@ def run_ours(args, world, rank, local, dist):
     ne = eng.build_edges()
     ev1.record(stream)
     torch.cuda.synchronize()
+    edges_ms_first = ev0.elapsed_time(ev1)  # includes the buffers' cudaMalloc
+    ev0.record(stream)
+    ne = eng.build_edges()  # steady state (re-extraction, buffers resident)
+    ev1.record(stream)
+    torch.cuda.synchronize()
     edges_ms = ev0.elapsed_time(ev1)
     variant = _lib.DM_VARIANT_SCATTER if args.variant == "scatter" else _lib.DM_VARIANT_GATHER
     DF, TR, EDGE = _lib.DM_NAV_DUALFREE, _lib.DM_NAV_TRADITIONAL, _lib.DM_VOL_EDGE
@@ -337,17 +342,29 @@ def run_ours(args, world, rank, local, dist):
         dp = lambda p: C.cast(p, C.POINTER(C.c_double))  # noqa: E731
         for _ in range(2):
             eng.metrics_host(dp(hp[0]), DF, variant, EDGE, dp(hp[1]), dp(hp[2]))
+        # one synchronous step (copy-in, kernels, copy-out back to back)
+        barrier(dist)
+        t0 = time.perf_counter()
+        eng.metrics_host(dp(hp[0]), DF, variant, EDGE, dp(hp[1]), dp(hp[2]))
+        t_sync = time.perf_counter() - t0
+        # the pipelined loop: every step still copies its coordinates in and
+        # its navs + volumes out; step i+1's copy-in and kernels overlap step
+        # i's copy-out (full-duplex PCIe, two device output buffers)
         barrier(dist)
         t0 = time.perf_counter()
         ke = max(3, K // 2)
         for _ in range(ke):
-            eng.metrics_host(dp(hp[0]), DF, variant, EDGE, dp(hp[1]), dp(hp[2]))
+            eng.metrics_host_async(dp(hp[0]), DF, variant, EDGE, dp(hp[1]), dp(hp[2]))
+        eng.sync()
         t_e2e = (time.perf_counter() - t0) / ke
         t_e2e = max_over_ranks(dist, t_e2e, device=torch.device("cuda", local))
+        t_sync = max_over_ranks(dist, t_sync, device=torch.device("cuda", local))
         e2e = {"value": world * mesh.num_elements() / t_e2e, "unit": "tets/s",
                "h2d_bytes_per_step": nb_c, "d2h_bytes_per_step": nb_n + nb_v,
-               "ms_per_step": t_e2e * 1e3,
-               "api": "dm_metrics_host (include/dm_capi.h), pinned host buffers"}
+               "ms_per_step": t_e2e * 1e3, "steps": ke,
+               "ms_single_synchronous_step": t_sync * 1e3,
+               "api": "dm_metrics_host_async x steps + dm_sync (include/dm_capi.h), pinned "
+                      "host buffers; wall clock from the first call to the final sync"}
         for p in hp:
             _lib.capi().dm_host_free(p)
 
@@ -400,7 +417,8 @@ def run_ours(args, world, rank, local, dist):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
-            "extra": {"edges_ms": edges_ms, "plan_ms_first_call": plan_ms,
+            "extra": {"edges_ms": edges_ms, "edges_ms_first_call": edges_ms_first,
+                      "plan_ms_first_call": plan_ms,
                       "plan": eng.plan_info(), "edges_bytes": B["edges"],
                       "edges_GBps": B["edges"] / (edges_ms / 1e3) / 1e9,
                       "traditional_ms_per_step": trad_ms,

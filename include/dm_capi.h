@@ -127,6 +127,19 @@ int dm_put_volumes(dm_ctx* ctx, const double* volumes);
 int dm_metrics_host(dm_ctx* ctx, const double* coords, int nav_algo, int variant,
                     int vol_algo, double* navs, double* volumes);
 
+/* The same step, enqueued and returned from at once (a pipelined loop of
+ * metrics over a moving or changing set of coordinates): coords arrive on a
+ * host->device copy stream, the kernels run once they landed and the
+ * previous step's kernels ended, navs / volumes leave on a device->host copy
+ * stream.  navs / volumes alternate between two device buffers, so step i+1
+ * computes while step i is still being copied out (PCIe is full duplex; the
+ * step costs max(copy-out, copy-in + kernels) instead of their sum).  Host
+ * buffers must stay valid and untouched until dm_sync(); pinned buffers
+ * (dm_host_alloc) are needed for the copies to overlap.  Device views
+ * (dm_device_views) are valid until the next metrics call. */
+int dm_metrics_host_async(dm_ctx* ctx, const double* coords, int nav_algo, int variant,
+                          int vol_algo, double* navs, double* volumes);
+
 /* Verification on the resident navs / volumes. */
 int dm_check_closure(dm_ctx* ctx, double* residual, double* interior_residual);
 /* SPEC.md:265-274 check_linear_exactness: affine flux F(x) = A x + b (A row-major
@@ -168,7 +181,7 @@ int dm_get_derived_boundary(dm_ctx* ctx, int32_t* faces);
 /* Plumbing: stream, device views, per-phase timing, launch counter. */
 int dm_stream(dm_ctx* ctx, void** stream);
 int dm_device_views(dm_ctx* ctx, dm_device_view* view);
-int dm_sync(dm_ctx* ctx);
+int dm_sync(dm_ctx* ctx); /* waits for the ctx stream and the pipelined copies */
 /* When enabled, dm_navs / dm_volumes record CUDA events around each kernel
  * phase on the context stream; dm_get_timings returns the last values (ms):
  * [0] element loop, [1] boundary pass, [2] edge-volume loop, [3] total. */

@@ -74,6 +74,7 @@ CAPI = {
     "dm_put_navs": (C.c_int, [P, DP]),
     "dm_put_volumes": (C.c_int, [P, DP]),
     "dm_metrics_host": (C.c_int, [P, DP, C.c_int, C.c_int, C.c_int, DP, DP]),
+    "dm_metrics_host_async": (C.c_int, [P, DP, C.c_int, C.c_int, C.c_int, DP, DP]),
     "dm_check_closure": (C.c_int, [P, DP, DP]),
     "dm_check_linear_exactness": (C.c_int, [P, DP, DP, DP]),
     "dm_check_total_volume": (C.c_int, [P, DP, DP, DP]),

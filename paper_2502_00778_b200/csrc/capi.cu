@@ -36,6 +36,20 @@ void drop_derived(dm_ctx* c) {
   c->n_derived = 0;
 }
 
+// Writers of navs / volumes on the compute stream wait for the pipelined
+// copies still reading them (no-op without dm_metrics_host_async).
+int wait_out_copies(dm_ctx* c) {
+  for (cudaEvent_t e : c->ev_out)
+    if (e) DM_CK(c, cudaStreamWaitEvent(c->stream, e, 0));
+  return DM_OK;
+}
+int sync_all(dm_ctx* c) {
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  for (cudaStream_t s : {c->s_h2d, c->s_d2h})
+    if (s) DM_CK(c, cudaStreamSynchronize(s));
+  return DM_OK;
+}
+
 float ev_ms(dm_ctx* c, int a, int b) {
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) ms = -1.f;
@@ -86,12 +100,21 @@ void dm_destroy(dm_ctx* c) {
   if (c->stream) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    for (cudaStream_t s : {c->s_h2d, c->s_d2h})
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
     for (auto& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {c->ev_h2d, c->ev_comp, c->ev_out[0], c->ev_out[1]})
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
   }
   delete c;
 }
+
+
 
 const char* dm_last_error(const dm_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
@@ -103,6 +126,9 @@ int dm_set_mesh(dm_ctx* c, int dim, const double* coords, int64_t n_nodes, const
   if ((n_nodes && !coords) || (n_elements && !elements) || (n_boundary && !boundary))
     return fail(c, DM_ERR_INVALID_ARG, "null array with non-zero count");
   if (n_nodes >= (1ll << 31)) return fail(c, DM_ERR_UNSUPPORTED, "node ids are 32-bit");
+  if (int w = sync_all(c)) return w;  // pipelined copies may still read the old buffers
+  c->navs_alt.release();
+  c->vols_alt.release();
   drop_derived(c);
   c->dim = dim;
   c->nv = n_nodes;
@@ -201,13 +227,15 @@ int dm_get_incidence(dm_ctx* c, int32_t* inc_ptr, int32_t* inc) {
 
 int dm_navs(dm_ctx* c, int nav_algo, int variant) {
   if (!c) return DM_ERR_INVALID_ARG;
-  return navs_impl(c, nav_algo, variant);
+  int st = wait_out_copies(c);
+  return st ? st : navs_impl(c, nav_algo, variant);
 }
 
 int dm_volumes(dm_ctx* c, int vol_algo) {
   if (!c) return DM_ERR_INVALID_ARG;
   if (c->dim == 0) return fail(c, DM_ERR_STATE, "no mesh");
-  return volumes_impl(c, vol_algo);
+  int st = wait_out_copies(c);
+  return st ? st : volumes_impl(c, vol_algo);
 }
 
 int dm_get_navs(dm_ctx* c, double* navs) {
@@ -222,6 +250,7 @@ int dm_get_navs(dm_ctx* c, double* navs) {
 int dm_put_navs(dm_ctx* c, const double* navs) {
   if (!c || !navs) return DM_ERR_INVALID_ARG;
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  if (int w = wait_out_copies(c)) return w;
   DM_CK(c, c->navs.ensure(static_cast<size_t>(c->dim * c->ne)));
   DM_CK(c, cudaMemcpyAsync(c->navs.p, navs, sizeof(double) * c->dim * c->ne,
                            cudaMemcpyHostToDevice, c->stream));
@@ -238,6 +267,7 @@ int dm_put_navs(dm_ctx* c, const double* navs) {
 int dm_put_volumes(dm_ctx* c, const double* volumes) {
   if (!c || !volumes) return DM_ERR_INVALID_ARG;
   if (c->dim == 0) return fail(c, DM_ERR_STATE, "no mesh");
+  if (int w = wait_out_copies(c)) return w;
   DM_CK(c, c->vols.ensure(static_cast<size_t>(c->nv)));
   DM_CK(c, cudaMemcpyAsync(c->vols.p, volumes, sizeof(double) * c->nv, cudaMemcpyHostToDevice,
                            c->stream));
@@ -254,27 +284,55 @@ int dm_get_volumes(dm_ctx* c, double* volumes) {
   return DM_OK;
 }
 
-int dm_metrics_host(dm_ctx* c, const double* coords, int nav_algo, int variant, int vol_algo,
-                    double* navs, double* volumes) {
+int dm_metrics_host_async(dm_ctx* c, const double* coords, int nav_algo, int variant,
+                          int vol_algo, double* navs, double* volumes) {
   if (!c) return DM_ERR_INVALID_ARG;
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "build the edge list first");
+  if (!c->s_h2d) {
+    DM_CK(c, cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    DM_CK(c, cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_h2d, &c->ev_comp, &c->ev_out[0], &c->ev_out[1]})
+      DM_CK(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
   int st = DM_OK;
   if (coords) {
-    st = dm_set_coords(c, coords);
+    // the previous step's kernels read the resident coordinates
+    DM_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_comp, 0));
+    DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * c->dim * c->nv,
+                             cudaMemcpyHostToDevice, c->s_h2d));
+    DM_CK(c, cudaEventRecord(c->ev_h2d, c->s_h2d));
+    DM_CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d, 0));
+    c->have_navs = c->have_vols = false;
+    st = pad_coords(c);
     if (st) return st;
   }
+  // this step writes the other navs / vols buffer once its last copy-out ended
+  const int slot = c->out_slot ^ 1;
+  c->navs.swap(c->navs_alt);
+  c->vols.swap(c->vols_alt);
+  c->out_slot = slot;
+  c->have_navs = c->have_vols = false;
+  DM_CK(c, cudaStreamWaitEvent(c->stream, c->ev_out[slot], 0));
   st = navs_impl(c, nav_algo, variant);
   if (st) return st;
   st = volumes_impl(c, vol_algo);
   if (st) return st;
+  DM_CK(c, cudaEventRecord(c->ev_comp, c->stream));
+  DM_CK(c, cudaStreamWaitEvent(c->s_d2h, c->ev_comp, 0));
   if (navs)
     DM_CK(c, cudaMemcpyAsync(navs, c->navs.p, sizeof(double) * c->dim * c->ne,
-                             cudaMemcpyDeviceToHost, c->stream));
+                             cudaMemcpyDeviceToHost, c->s_d2h));
   if (volumes)
     DM_CK(c, cudaMemcpyAsync(volumes, c->vols.p, sizeof(double) * c->nv, cudaMemcpyDeviceToHost,
-                             c->stream));
-  DM_CK(c, cudaStreamSynchronize(c->stream));
+                             c->s_d2h));
+  DM_CK(c, cudaEventRecord(c->ev_out[slot], c->s_d2h));
   return DM_OK;
+}
+
+int dm_metrics_host(dm_ctx* c, const double* coords, int nav_algo, int variant, int vol_algo,
+                    double* navs, double* volumes) {
+  int st = dm_metrics_host_async(c, coords, nav_algo, variant, vol_algo, navs, volumes);
+  return st ? st : sync_all(c);
 }
 
 int dm_stream(dm_ctx* c, void** stream) {
@@ -308,8 +366,7 @@ int dm_device_views(dm_ctx* c, dm_device_view* v) {
 
 int dm_sync(dm_ctx* c) {
   if (!c) return DM_ERR_INVALID_ARG;
-  DM_CK(c, cudaStreamSynchronize(c->stream));
-  return DM_OK;
+  return sync_all(c);
 }
 
 int dm_set_timing(dm_ctx* c, int enable) {

@@ -34,6 +34,10 @@ struct DevBuf {
     p = nullptr;
     n = 0;
   }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+  }
   // (Re)allocate to exactly hold `count` elements; keeps the buffer when it
   // is already large enough.
   cudaError_t ensure(size_t count) {
@@ -140,6 +144,15 @@ struct dm_ctx {
 
   // tuning knob for the GATHER kernel shape (env DUALMESH_GATHER_CFG)
   int gather_cfg = 0;
+
+  // pipelined host steps (dm_metrics_host_async): coordinates arrive on
+  // s_h2d, results leave on s_d2h, the kernels stay on `stream`; navs / vols
+  // alternate between two device buffers so step i+1 computes while step i
+  // is still being copied out (PCIe is full duplex)
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d = nullptr, ev_comp = nullptr, ev_out[2] = {nullptr, nullptr};
+  int out_slot = 0;
+  dm::DevBuf<double> navs_alt, vols_alt;
 
   // timing
   bool timing = false;

@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kTileEdges)
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
           const unsigned n0 = __popc(h16[c] & half & others), n1 = __popc(h16[c + 1] & half & others);
-          if (n0 | n1) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][c]), n0 | n1 << 16);
+          atomicAdd(reinterpret_cast<unsigned*>(&cost[x][c]), n0 | n1 << 16);  // no branch: mostly != 0
         }
       }
       if (lead8) {
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kTileEdges)
         for (int c = 0; c < 8; c += 2) {
           const unsigned n0 = __popc((h16[c] | h16[c + 8]) & quart & others);
           const unsigned n1 = __popc((h16[c + 1] | h16[c + 9]) & quart & others);
-          if (n0 | n1) atomicAdd(reinterpret_cast<unsigned*>(&cost[x][16 + c]), n0 | n1 << 16);
+          atomicAdd(reinterpret_cast<unsigned*>(&cost[x][16 + c]), n0 | n1 << 16);
         }
       }
     }

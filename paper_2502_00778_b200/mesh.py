@@ -255,6 +255,13 @@ class Engine:
         self._ck(self._lib.dm_metrics_host(self._c, coords, nav_algo, variant, vol_algo,
                                            navs_out, vols_out), "dm_metrics_host")
 
+    def metrics_host_async(self, coords, nav_algo, variant, vol_algo, navs_out, vols_out):
+        """Enqueue the same step and return (dm_metrics_host_async): consecutive
+        calls overlap the copy-out of step i with the copy-in and kernels of
+        step i+1.  Host buffers (pinned) stay untouched until sync()."""
+        self._ck(self._lib.dm_metrics_host_async(self._c, coords, nav_algo, variant, vol_algo,
+                                                 navs_out, vols_out), "dm_metrics_host_async")
+
     # ---------------------------------------------------------------- verify
     def check_closure(self):
         r, ri = C.c_double(), C.c_double()

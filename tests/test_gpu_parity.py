@@ -402,6 +402,55 @@ def test_deforming_grid_reuses_plan(engine, oracle, name, scale):
     np.testing.assert_array_equal(vols, engine.get_volumes())
 
 
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C3", 4)])
+def test_pipelined_host_steps(engine, name, scale):
+    """dm_metrics_host_async: a loop of steps over changing coordinates, each
+    enqueued before the previous one's copy-out finished (two device output
+    buffers, copy streams), gives per step exactly the fields of the
+    synchronous calls on the same coordinates."""
+    import ctypes as C
+    m = meshgen.baseline_config(name, scale)
+    engine.set_mesh(m)
+    engine.build_edges()
+    rng = np.random.default_rng(11)
+    inner = (m.coords > 0) * (m.coords < 1)
+    xs = [m.coords + rng.uniform(-2e-3, 2e-3, m.coords.size) * inner for _ in range(5)]
+    nd, nn = m.dim * engine.n_edges, m.num_nodes()
+    lib = _lib.capi()
+    bufs = []
+
+    def pinned(n):
+        p = C.c_void_p()
+        assert lib.dm_host_alloc(8 * n, C.byref(p)) == 0
+        bufs.append(p)
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n,))
+
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    try:
+        hx = [pinned(m.coords.size) for _ in xs]
+        hn = [pinned(nd) for _ in xs]
+        hv = [pinned(nn) for _ in xs]
+        for h, x in zip(hx, xs):
+            h[:] = x
+        for i in range(len(xs)):
+            engine.metrics_host_async(dp(hx[i]), DF, GATHER, EDGE, dp(hn[i]), dp(hv[i]))
+        engine.sync()
+        for i, x in enumerate(xs):
+            engine.set_coords(x)
+            engine.navs(DF, GATHER)
+            engine.volumes(EDGE)
+            np.testing.assert_array_equal(hn[i], engine.get_navs())
+            np.testing.assert_array_equal(hv[i], engine.get_volumes())
+        # the synchronous call after the pipelined ones sees the last step
+        out_n, out_v = np.empty(nd), np.empty(nn)
+        engine.metrics_host(dp(hx[2]), DF, GATHER, EDGE, dp(out_n), dp(out_v))
+        np.testing.assert_array_equal(out_n, hn[2])
+        np.testing.assert_array_equal(out_v, hv[2])
+    finally:
+        for p in bufs:
+            lib.dm_host_free(p)
+
+
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C3", 4), ("C5", 2)])
 def test_colored_plan_same_bits(name, scale, monkeypatch):
     """The opt-in bank-conflict colouring only relabels table slots: navs
