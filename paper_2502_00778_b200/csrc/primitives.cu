@@ -1,5 +1,11 @@
 // primitives.cu -- device scan and segmented sort used by edge extraction
-// and by the derived CSR structures.  Hand-written (no CUB/Thrust).
+// and by the derived CSR structures.  Hand-written; CUB's radix sort only
+// for segments beyond one CTA's shared memory (> 4096 keys: a node with
+// more than ~1300 incident tets), one call per such segment.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <vector>
+
 #include "dm_internal.cuh"
 
 namespace dm {
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(512)
     const u32 s = big[q];
     const u32 b = seg[s];
     const int n = static_cast<int>(seg[s + 1] - b);
-    if (n > kBlockSeg) {
+    if (n > kBlockSeg) {  // left to the host loop of segment_sort
       if (threadIdx.x == 0) atomicExch(flag, 1);
       continue;
     }
@@ -224,6 +230,58 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+// (segment id, start, length) of the queued segments, for the host loop.
+__global__ void k_big_lengths(const u32* seg, const u32* big, const int* nbig, uint4* out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= *nbig) return;
+  const u32 s = big[q];
+  out[q] = make_uint4(s, seg[s], seg[s + 1] - seg[s], 0u);
+}
+
+// Distinct high words of one sorted segment (one CTA).
+__global__ void __launch_bounds__(1024) k_count_heads(const u64* data, u32 n, u32* out) {
+  int heads = 0;
+  for (u32 i0 = 0; i0 < n; i0 += blockDim.x) {
+    const u32 i = i0 + threadIdx.x;
+    heads += __syncthreads_count(i < n && (i == 0 || (data[i] >> 32) != (data[i - 1] >> 32)));
+  }
+  if (threadIdx.x == 0) *out = static_cast<u32>(heads);
+}
+
+// Segments longer than kBlockSeg: one device radix sort each.
+template <typename K>
+int sort_huge_segments(dm_ctx* c, K* data, const u32* seg, u32* ucnt) {
+  int nb = 0;
+  DM_CK(c, cudaMemcpyAsync(&nb, c->flag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  DevBuf<uint4> info;
+  DM_CK(c, info.ensure(static_cast<size_t>(nb)));
+  DM_LAUNCH(c, k_big_lengths, grid_for(nb, 256), 256, 0, seg, c->seg_big.p, c->flag.p + 1, info.p);
+  std::vector<uint4> h(static_cast<size_t>(nb));
+  DM_CK(c, cudaMemcpyAsync(h.data(), info.p, sizeof(uint4) * nb, cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  DevBuf<K> alt;
+  DevBuf<unsigned char> tmp;
+  for (const uint4& q : h) {
+    if (q.z <= static_cast<u32>(kBlockSeg)) continue;
+    DM_CK(c, alt.ensure(q.z));
+    size_t tb = 0;
+    DM_CK(c, cub::DeviceRadixSort::SortKeys(nullptr, tb, data + q.y, alt.p, static_cast<int>(q.z),
+                                            0, static_cast<int>(8 * sizeof(K)), c->stream));
+    DM_CK(c, tmp.ensure(tb));
+    DM_CK(c, cub::DeviceRadixSort::SortKeys(tmp.p, tb, data + q.y, alt.p, static_cast<int>(q.z),
+                                            0, static_cast<int>(8 * sizeof(K)), c->stream));
+    DM_CK(c, cudaMemcpyAsync(data + q.y, alt.p, sizeof(K) * q.z, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    if constexpr (sizeof(K) == 8) {
+      if (ucnt) DM_LAUNCH(c, k_count_heads, 1, 1024, 0, data + q.y, q.z, ucnt + q.x);
+    }
+  }
+  DM_CK(c, cudaStreamSynchronize(c->stream));  // scratch dies here
+  return DM_OK;
+}
+
 template <typename K, bool kUnique>
 int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg, u32* ucnt) {
   if (nseg <= 0) return DM_OK;
@@ -241,8 +299,7 @@ int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg, u32* ucnt) {
   int f = 0;
   int st = read_flag(c, &f);
   if (st) return st;
-  if (f) return fail(c, DM_ERR_UNSUPPORTED, "segment longer than 4096 keys (node valence too high)");
-  return DM_OK;
+  return f ? sort_huge_segments<K>(c, data, seg, ucnt) : DM_OK;
 }
 
 // ---- key/value variant: sorts (key, value) pairs lexicographically
@@ -308,7 +365,7 @@ __global__ void __launch_bounds__(512)
     const u32 s = big[q];
     const u32 b = seg[s];
     const int n = static_cast<int>(seg[s + 1] - b);
-    if (n > kBlockSeg) {
+    if (n > kBlockSeg) {  // left to sort_huge_segments_kv
       if (threadIdx.x == 0) atomicExch(flag, 1);
       continue;
     }
@@ -330,6 +387,40 @@ __global__ void __launch_bounds__(512)
 
 }  // namespace
 
+// (key, value) segments longer than kBlockSeg: two stable radix passes each
+// (by value, then by key) give the lexicographic order.
+int sort_huge_segments_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg) {
+  int nb = 0;
+  DM_CK(c, cudaMemcpyAsync(&nb, c->flag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  DevBuf<uint4> info;
+  DM_CK(c, info.ensure(static_cast<size_t>(nb)));
+  DM_LAUNCH(c, k_big_lengths, grid_for(nb, 256), 256, 0, seg, c->seg_big.p, c->flag.p + 1, info.p);
+  std::vector<uint4> h(static_cast<size_t>(nb));
+  DM_CK(c, cudaMemcpyAsync(h.data(), info.p, sizeof(uint4) * nb, cudaMemcpyDeviceToHost,
+                           c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  DevBuf<u64> k2;
+  DevBuf<u32> v2;
+  DevBuf<unsigned char> tmp;
+  for (const uint4& q : h) {
+    if (q.z <= static_cast<u32>(kBlockSeg)) continue;
+    const int n = static_cast<int>(q.z);
+    u64* k = keys + q.y;
+    u32* v = vals + q.y;
+    DM_CK(c, k2.ensure(q.z));
+    DM_CK(c, v2.ensure(q.z));
+    size_t t1 = 0, t2 = 0;
+    DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, t1, v, v2.p, k, k2.p, n, 0, 32, c->stream));
+    DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, t2, k2.p, k, v2.p, v, n, 0, 64, c->stream));
+    DM_CK(c, tmp.ensure(std::max(t1, t2)));
+    DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, t1, v, v2.p, k, k2.p, n, 0, 32, c->stream));
+    DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, t2, k2.p, k, v2.p, v, n, 0, 64, c->stream));
+  }
+  DM_CK(c, cudaStreamSynchronize(c->stream));  // scratch dies here
+  return DM_OK;
+}
+
 int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg) {
   if (nseg <= 0) return DM_OK;
   DevBuf<u32>& big = c->seg_big;  // persistent scratch (no free/malloc stalls)
@@ -345,8 +436,7 @@ int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg) {
   int f = 0;
   int st = read_flag(c, &f);
   if (st) return st;
-  if (f) return fail(c, DM_ERR_UNSUPPORTED, "segment longer than 4096 keys (node valence too high)");
-  return DM_OK;
+  return f ? sort_huge_segments_kv(c, keys, vals, seg) : DM_OK;
 }
 
 int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n) {

@@ -294,8 +294,11 @@ def _fan_mesh(n):
     return Mesh(3, x, np.array(el, np.int32))
 
 
-@pytest.mark.parametrize("n", [12, 30])
+@pytest.mark.parametrize("n", [12, 30, 50, 1500])
 def test_fan_fallback(engine, oracle, n):
+    """Fans around one edge: n > 24 incidences per edge leave the ring path;
+    n = 50 sorts node 0's 150 K1 keys in the CTA bitonic path, n = 1500 its
+    4500 keys (> 4096) in the per-segment radix-sort path."""
     m0 = _fan_mesh(n)
     engine.set_mesh(m0)
     m = Mesh(3, m0.coords, m0.elements, engine.derive_boundary())
@@ -305,6 +308,14 @@ def test_fan_fallback(engine, oracle, n):
     info = engine.plan_info()
     assert info["ring_ok"] == (n <= 24)
     e, o = oracle.build_edges(m)
+    got = engine.edges()
+    np.testing.assert_array_equal(got.edges, e)
+    np.testing.assert_array_equal(got.origin_start, o)
+    e2l, ip, inc = oracle.edge_maps(m, e, o)
+    np.testing.assert_array_equal(engine.e2l(), e2l)
+    gip, ginc = engine.incidence()
+    np.testing.assert_array_equal(gip, ip)
+    np.testing.assert_array_equal(ginc, inc)
     want = oracle.navs_dualfree(m, e, o)
     assert per_vector_rel(engine.get_navs(), want, 3) <= 1e-12
     engine.volumes(EDGE)
