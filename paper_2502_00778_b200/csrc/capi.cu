@@ -28,7 +28,8 @@ int check_device(dm_ctx* c) {
 }
 
 void drop_derived(dm_ctx* c) {
-  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_tables = c->have_rings = false;
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_ifl = c->have_tables =
+      c->have_rings = false;
   c->have_navs = c->have_vols = false;
   c->navs_algo = -1;
   c->ne = 0;

@@ -219,7 +219,7 @@ long long det3(const int* a, const int* b, const int* c, const int* d) {
 
 int begin_mesh(dm_ctx* c, int dim, i64 nv, i64 nE, i64 nB) {
   if (nv >= (1ll << 31)) return fail(c, DM_ERR_UNSUPPORTED, "node ids are 32-bit");
-  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_tables = c->have_rings =
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_ifl = c->have_tables = c->have_rings =
       false;
   c->have_navs = c->have_vols = false;
   c->navs_algo = -1;
@@ -339,7 +339,7 @@ extern "C" int dm_gen_permute(dm_ctx* c, uint64_t node_seed, uint64_t elem_seed)
     DM_LAUNCH(c, k_perm_rows, grid_for(nE, 256), 256, 0, tmp.p, dp.p, nE, npe, c->elems.p);
     DM_CK(c, cudaStreamSynchronize(c->stream));
   }
-  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_tables = c->have_rings =
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_ifl = c->have_tables = c->have_rings =
       false;
   c->have_navs = c->have_vols = false;
   c->ne = c->n_bedge = c->n_derived = 0;

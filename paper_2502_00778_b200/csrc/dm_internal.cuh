@@ -7,7 +7,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 #include <cstdio>
 #include <string>
@@ -21,6 +23,18 @@ using u64 = std::uint64_t;
 using i64 = std::int64_t;
 
 // ---------------------------------------------------------------- buffers
+// env DUALMESH_ALLOC_TRACE=1: print device allocations / frees slower than 2 ms
+inline void alloc_trace(const char* what, size_t bytes, std::chrono::steady_clock::time_point t0) {
+  static const bool on = [] {
+    const char* e = std::getenv("DUALMESH_ALLOC_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (!on) return;
+  const double ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (ms > 2.0) std::fprintf(stderr, "[alloc] %s %.1f MB %.2f ms\n", what, bytes / 1e6, ms);
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -30,7 +44,11 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      const auto t0 = std::chrono::steady_clock::now();
+      cudaFree(p);
+      alloc_trace("cudaFree", n * sizeof(T), t0);
+    }
     p = nullptr;
     n = 0;
   }
@@ -44,9 +62,88 @@ struct DevBuf {
     if (count <= n && p) return cudaSuccess;
     release();
     size_t bytes = (count ? count : 1) * sizeof(T);
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t st = cudaMalloc(reinterpret_cast<void**>(&p), bytes);
+    alloc_trace("cudaMalloc", bytes, t0);
     if (st == cudaSuccess) n = count;
     else p = nullptr;
+    return st;
+  }
+};
+
+// Scratch arena for the temporaries of the plan builders: a few large
+// device blocks reused across calls (a cold cudaMalloc / cudaFree costs
+// 2-60 ms each on a fresh process, and the ring plan needs ~15
+// temporaries).  Bump allocation, released by ArenaScope on exit; all users
+// run on the context stream, so reuse is stream-ordered.
+struct Arena {
+  struct Block {
+    char* p;
+    size_t size;
+  };
+  Block blocks[16] = {};
+  int nblocks = 0, cur = 0;
+  size_t off = 0;
+  Arena() = default;
+  Arena(const Arena&) = delete;
+  Arena& operator=(const Arena&) = delete;
+  ~Arena() {
+    for (int b = 0; b < nblocks; ++b) cudaFree(blocks[b].p);
+  }
+  cudaError_t take(size_t bytes, void** out, size_t min_block) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    while (cur < nblocks) {
+      if (off + bytes <= blocks[cur].size) {
+        *out = blocks[cur].p + off;
+        off += bytes;
+        return cudaSuccess;
+      }
+      ++cur;
+      off = 0;
+    }
+    if (nblocks == 16) return cudaErrorMemoryAllocation;
+    const size_t sz = bytes > min_block ? bytes : min_block;
+    const auto t0 = std::chrono::steady_clock::now();
+    char* p = nullptr;
+    cudaError_t st = cudaMalloc(reinterpret_cast<void**>(&p), sz);
+    alloc_trace("cudaMalloc(arena)", sz, t0);
+    if (st != cudaSuccess) return st;
+    blocks[nblocks++] = {p, sz};
+    cur = nblocks - 1;
+    off = bytes;
+    *out = p;
+    return cudaSuccess;
+  }
+};
+
+struct ArenaScope {
+  Arena& a;
+  int cur;
+  size_t off;
+  explicit ArenaScope(Arena& arena) : a(arena), cur(arena.cur), off(arena.off) {}
+  ~ArenaScope() {
+    a.cur = cur;
+    a.off = off;
+  }
+};
+
+// Arena-backed stand-in for a local DevBuf: same .p / .ensure() surface.
+template <typename T>
+struct ScratchBuf {
+  Arena& a;
+  size_t min_block;
+  T* p = nullptr;
+  size_t n = 0;
+  ScratchBuf(Arena& arena, size_t min_block_bytes) : a(arena), min_block(min_block_bytes) {}
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    void* q = nullptr;
+    cudaError_t st = a.take((count ? count : 1) * sizeof(T), &q, min_block);
+    if (st == cudaSuccess) {
+      p = static_cast<T*>(q);
+      n = count;
+    }
     return st;
   }
 };
@@ -77,7 +174,8 @@ struct dm_ctx {
   dm::DevBuf<int2> edges;
   dm::DevBuf<dm::u32> os;  // origin_start (32-bit on device)
   dm::DevBuf<int32_t> e2l, inc_ptr, inc;
-  dm::DevBuf<int2> ifl;  // face-list incidence, same order as inc (edges.cu make_ifl)
+  bool have_ifl = false;
+  dm::DevBuf<int2> ifl;  // face-list incidence, same order as inc (edges.cu, built on demand)
   // derived: incoming-edge CSR per node, boundary (edge,facet) pairs, node->element CSR
   bool have_in = false;
   dm::DevBuf<dm::u32> in_ptr;
@@ -132,6 +230,7 @@ struct dm_ctx {
   dm::DevBuf<dm::u32> cnt, fill;
   dm::DevBuf<dm::u64> tmp64;
   dm::DevBuf<dm::u32> seg_big;  // segment_sort: ids of segments longer than a warp's
+  dm::Arena arena;              // plan temporaries (rings.cu)
   dm::DevBuf<dm::u32> scan_tmp;
   dm::DevBuf<int> flag;
 
@@ -295,6 +394,7 @@ __global__ void k_tile_bptr(const u64* bedge, u32 n, i64 ne, i64 ntiles, u32* ti
 int ensure_incoming(dm_ctx* c);
 int ensure_bedge(dm_ctx* c);
 int ensure_n2e(dm_ctx* c);
+int ensure_ifl(dm_ctx* c);  // face-list incidence for the FACES / traditional fallbacks
 int ensure_tables(dm_ctx* c);
 int ensure_rings(dm_ctx* c);
 int build_edges_impl(dm_ctx* c);

@@ -94,11 +94,10 @@ __device__ __forceinline__ int2 make_ifl(const int32_t* el, int E, int l) {
   return make_int2(v[im] | (ij << 30), ik << 30);
 }
 
-// Warp per bucket: emit edges, inc_ptr, inc, e2l and the face-list incidence.
-template <int D, int L>
+// Warp per bucket: emit edges, inc_ptr, inc and e2l.
+template <int L>
 __global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 nv,
-                       const int32_t* el, int2* edges, int32_t* inc_ptr, int32_t* inc,
-                       int32_t* e2l, int2* ifl) {
+                       int2* edges, int32_t* inc_ptr, int32_t* inc, int32_t* e2l) {
   const int lane = threadIdx.x & 31;
   const i64 j = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (j >= nv) return;
@@ -124,9 +123,39 @@ __global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 n
       }
       inc[b + i] = static_cast<int32_t>(val / L);
       e2l[val] = id;
-      ifl[b + i] = make_ifl<D>(el, static_cast<int>(val / L), static_cast<int>(val % L));
     }
     id_base += __popc(hm);
+  }
+}
+
+// Face-list incidence, on demand (only the FACES / traditional fallbacks read
+// it): thread per edge over its incidence slice.  The local edge l of slot q
+// is recovered from the element's nodes -- the first local edge of element E
+// joining (j, k) after the one of the previous slot if that slot was E too --
+// so ifl[q] equals make_ifl(E, l) of the (E, l) item that K1 sorted into q.
+template <int D>
+__global__ void k_build_ifl(const int2* __restrict__ edges, const int32_t* __restrict__ inc_ptr,
+                            const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
+                            i64 ne, int2* __restrict__ ifl) {
+  constexpr int L = D == 3 ? 6 : 3;
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const int2 jk = edges[e];
+  int prevE = -1, prevl = -1;
+  for (int q = inc_ptr[e]; q < inc_ptr[e + 1]; ++q) {
+    const int E = inc[q];
+    int v[4];
+    load_elem<D>(el, E, v);
+    int l = E == prevE ? prevl + 1 : 0;
+    for (; l < L; ++l) {
+      int la, lb;
+      local_edge<D>(l, la, lb);
+      const int a = v[la], b = v[lb];
+      if ((a == jk.x && b == jk.y) || (a == jk.y && b == jk.x)) break;
+    }
+    ifl[q] = make_ifl<D>(el, E, l < L ? l : L - 1);
+    prevE = E;
+    prevl = l;
   }
 }
 
@@ -140,7 +169,8 @@ int build_edges_impl(dm_ctx* c) {
   const i64 M = static_cast<i64>(L) * c->nE;
   if (M >= (1ll << 31) || c->nv >= (1ll << 30))
     return fail(c, DM_ERR_UNSUPPORTED, "mesh exceeds the 32-bit item space of the device layout");
-  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_tables = c->have_rings = false;
+  c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_ifl = c->have_tables =
+      c->have_rings = false;
   c->have_navs = c->have_vols = false;
   const i64 nv = c->nv;
 
@@ -176,13 +206,12 @@ int build_edges_impl(dm_ctx* c) {
   DM_CK(c, c->inc_ptr.ensure(static_cast<size_t>(c->ne + 1)));
   DM_CK(c, c->inc.ensure(static_cast<size_t>(M)));
   DM_CK(c, c->e2l.ensure(static_cast<size_t>(M)));
-  DM_CK(c, c->ifl.ensure(static_cast<size_t>(M)));
   if (D == 3) {
-    DM_LAUNCH(c, (k_emit<3, 6>), grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p,
-              nv, c->elems.p, c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p, c->ifl.p);
+    DM_LAUNCH(c, k_emit<6>, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p, nv,
+              c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p);
   } else {
-    DM_LAUNCH(c, (k_emit<2, 3>), grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p,
-              nv, c->elems.p, c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p, c->ifl.p);
+    DM_LAUNCH(c, k_emit<3>, grid_for(nv * 32, 256), 256, 0, c->tmp64.p, c->cnt.p, c->os.p, nv,
+              c->edges.p, c->inc_ptr.p, c->inc.p, c->e2l.p);
   }
   DM_LAUNCH(c, k_set_i32, 1, 1, 0, c->inc_ptr.p + c->ne, static_cast<int32_t>(M));
   DM_CK(c, cudaStreamSynchronize(c->stream));
@@ -307,6 +336,21 @@ int ensure_incoming(dm_ctx* c) {
   st = segment_sort_u32(c, reinterpret_cast<u32*>(c->in_list.p), c->in_ptr.p, nv);
   if (st) return st;
   c->have_in = true;
+  return DM_OK;
+}
+
+int ensure_ifl(dm_ctx* c) {
+  if (c->have_ifl) return DM_OK;
+  if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
+  const i64 L = c->dim == 3 ? 6 : 3;
+  DM_CK(c, c->ifl.ensure(static_cast<size_t>(std::max<i64>(L * c->nE, 1))));
+  if (c->dim == 3)
+    DM_LAUNCH(c, k_build_ifl<3>, grid_for(c->ne, 256), 256, 0, c->edges.p, c->inc_ptr.p, c->inc.p,
+              c->elems.p, c->ne, c->ifl.p);
+  else
+    DM_LAUNCH(c, k_build_ifl<2>, grid_for(c->ne, 256), 256, 0, c->edges.p, c->inc_ptr.p, c->inc.p,
+              c->elems.p, c->ne, c->ifl.p);
+  c->have_ifl = true;
   return DM_OK;
 }
 

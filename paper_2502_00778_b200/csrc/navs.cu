@@ -1002,6 +1002,7 @@ int launch_navs(dm_ctx* c, int variant) {
     tmark(c, 2);
   } else if (variant == DM_VARIANT_GATHER_FACES || !c->table_ok || ALGO != kDualFree) {
     // face-list gather: traditional algorithm, meshes with node degree > 32
+    if (int sf = ensure_ifl(c)) return sf;
     tmark(c, 0);
 #define DM_FACES(U, MINB)                                                                     \
   DM_LAUNCH(c, (k_navs_faces<D, ALGO, U, MINB>), tiles, kEB, 0, c->edges.p, c->inc_ptr.p,      \

@@ -727,6 +727,13 @@ struct PlanClock {
   }
 };
 
+// First arena block: the plan's peak of temporaries in one allocation
+// (k0, k1, i0, rank-sort scratch, rk, cellpack ~ 40 B/node; pinv, bmark,
+// warp sizes ~ 6 B/edge).
+size_t arena_block(const dm_ctx* c) {
+  return static_cast<size_t>(48 * c->nv + 8 * c->ne + 12 * c->n_bedge) + (64u << 20);
+}
+
 int bits_for(u64 v) {
   int b = 1;
   while (b < 64 && (v >> b)) ++b;
@@ -740,7 +747,7 @@ int build_edge_order(dm_ctx* c) {
   const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
   // bounding box
   const int nblk = static_cast<int>(std::max<i64>(1, std::min<i64>(1024, (nv + 255) / 256)));
-  DevBuf<double> part;
+  ScratchBuf<double> part(c->arena, arena_block(c));
   DM_CK(c, part.ensure(6 * nblk));
   DM_LAUNCH(c, k_bbox, nblk, 256, 0, c->x4.p, nv, part.p);
   std::vector<double> hp(6 * nblk);
@@ -764,21 +771,20 @@ int build_edge_order(dm_ctx* c) {
   // output rows are mostly contiguous (C5: 2.51 -> 2.42 ms).  Without
   // coherence (randomly numbered grids) the plain order keeps the tables
   // small and s stays in position order for the volume pass (vol_by_rank).
-  DevBuf<u64> k0, k1;
-  DevBuf<int32_t> i0;
+  ScratchBuf<u64> k0(c->arena, arena_block(c)), k1(c->arena, arena_block(c));
+  ScratchBuf<int32_t> i0(c->arena, arena_block(c));
   DM_CK(c, k0.ensure(nv));
   DM_CK(c, k1.ensure(nv));
   DM_CK(c, i0.ensure(nv));
   DM_CK(c, c->morder.ensure(nv));
   int32_t* i1p = c->morder.p;
-  DevBuf<unsigned char> tmp;
+  ScratchBuf<unsigned char> tmp(c->arena, arena_block(c));
   size_t tb = 0;
   auto radix = [&]() -> int {  // (k0, i0) -> sorted ids in i1p
     size_t need = 0;
     DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, need, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
                                              c->stream));
     if (need > tb) {
-      DM_CK(c, cudaStreamSynchronize(c->stream));
       DM_CK(c, tmp.ensure(need));
       tb = need;
     }
@@ -795,8 +801,8 @@ int build_edge_order(dm_ctx* c) {
   if (st) return st;
   clk.mark("morton sort");
   {
-    DevBuf<int32_t> rk;
-    DevBuf<u32> cnt;
+    ScratchBuf<int32_t> rk(c->arena, arena_block(c));
+    ScratchBuf<u32> cnt(c->arena, arena_block(c));
     DM_CK(c, rk.ensure(nv));
     DM_CK(c, cnt.ensure(1));
     DM_CK(c, cudaMemsetAsync(cnt.p, 0, sizeof(u32), c->stream));
@@ -816,7 +822,7 @@ int build_edge_order(dm_ctx* c) {
     // axis so the key, 3*10 + 32 bits, fits)
     const int cells = static_cast<int>(std::max<long>(
         1, std::min<long>(1024, std::lround(std::cbrt(static_cast<double>(nv) / cell_nodes)))));
-    DevBuf<u32> cellpack;
+    ScratchBuf<u32> cellpack(c->arena, arena_block(c));
     DM_CK(c, cellpack.ensure(nv));
     for (int axis = 0; axis < 3; ++axis) {
       DM_LAUNCH(c, k_axis_key, grid_for(nv, 256), 256, 0, c->x4.p, nv, axis, k0.p, i0.p);
@@ -827,12 +833,11 @@ int build_edge_order(dm_ctx* c) {
     DM_LAUNCH(c, k_cell_key, grid_for(nv, 256), 256, 0, cellpack.p, nv, k0.p, i0.p);
     st = radix();
     if (st) return st;
-    DM_CK(c, cudaStreamSynchronize(c->stream));  // cellpack dies here
   }
   clk.mark("quantile cells");
   // edge permutation: each origin's edge range appended whole, in that order
   u32* pstart = nullptr;
-  DevBuf<int32_t> pinv;
+  ScratchBuf<int32_t> pinv(c->arena, arena_block(c));
   DM_CK(c, c->rpstart.ensure(nv + 1));
   pstart = c->rpstart.p;
   DM_CK(c, pinv.ensure(ne > 0 ? ne : 1));
@@ -864,7 +869,7 @@ int build_edge_order(dm_ctx* c) {
   DM_CK(c, c->bedge_p.ensure(nb > 0 ? nb : 1));
   DM_CK(c, c->tile_bptr_p.ensure(ntiles + 1));
   if (nb > 0) {
-    DevBuf<u64> bk;
+    ScratchBuf<u64> bk(c->arena, arena_block(c));
     DM_CK(c, bk.ensure(nb));
     DM_LAUNCH(c, k_bkey, grid_for(nb, 256), 256, 0, c->bedge.p, nb, pinv.p, bk.p);
     const int hb = 32 + bits_for(static_cast<u64>(ne));
@@ -879,7 +884,7 @@ int build_edge_order(dm_ctx* c) {
             static_cast<u32>(nb), ne, ntiles, c->tile_bptr_p.p);
   c->n_bseg = 0;
   if (nb > 0) {
-    DevBuf<u32> idx;
+    ScratchBuf<u32> idx(c->arena, arena_block(c));
     DM_CK(c, idx.ensure(nb + 1));
     DM_LAUNCH(c, k_bseg_flag, grid_for(nb, 256), 256, 0, c->bedge_p.p, nb, idx.p);
     st = scan_exclusive(c, idx.p, idx.p, nb);
@@ -893,7 +898,6 @@ int build_edge_order(dm_ctx* c) {
               c->edges.p, c->bseg.p, c->bseg_start.p);
     c->n_bseg = ns;
   }
-  DM_CK(c, cudaStreamSynchronize(c->stream));  // scratch buffers die here
   clk.mark("boundary lists");
   return DM_OK;
 }
@@ -902,6 +906,7 @@ int build_edge_order(dm_ctx* c) {
 
 int ensure_rings(dm_ctx* c) {
   if (c->have_rings) return DM_OK;
+  ArenaScope scratch(c->arena);  // temporaries of this plan are released on return
   PlanClock clk(c);
   int st0 = ensure_bedge(c);  // tile_bptr feeds the ring metadata
   if (st0) return st0;
@@ -930,8 +935,8 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(2 * ntiles)));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
-  DevBuf<int32_t> rank;
-  DevBuf<uint8_t> bmark;
+  ScratchBuf<int32_t> rank(c->arena, arena_block(c));
+  ScratchBuf<uint8_t> bmark(c->arena, arena_block(c));
   DM_CK(c, rank.ensure(c->nv));
   DM_CK(c, bmark.ensure(ne));
   DM_LAUNCH(c, k_rank, grid_for(c->nv, 256), 256, 0, c->morder.p, c->nv, rank.p);
@@ -947,13 +952,13 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, cudaStreamSynchronize(c->stream));
   c->code_width = fl0[1] <= 256 ? 1 : 2;
   clk.mark("tile nodes");
-  DevBuf<u32> wstart;
+  ScratchBuf<u32> wstart(c->arena, arena_block(c));
   DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));
   DM_LAUNCH(c, k_ring_warpsize, grid_for(nwarps, 256), 256, 0, c->eperm.p, c->inc_ptr.p, ne,
             nwarps, c->code_width, wstart.p);
   // code offsets are 32-bit: check the exact total before the u32 scan
   {
-    DevBuf<unsigned long long> tot;
+    ScratchBuf<unsigned long long> tot(c->arena, arena_block(c));
     DM_CK(c, tot.ensure(1));
     DM_CK(c, cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long), c->stream));
     DM_LAUNCH(c, k_sum_u32, grid_for(nwarps, 256), 256, 0, wstart.p, nwarps, tot.p);
