@@ -1000,8 +1000,12 @@ int launch_navs(dm_ctx* c, int variant) {
       }
     }
     tmark(c, 2);
-  } else if (variant == DM_VARIANT_GATHER_FACES || !c->table_ok || ALGO != kDualFree) {
-    // face-list gather: traditional algorithm, meshes with node degree > 32
+  } else if (variant == DM_VARIANT_GATHER_FACES || !c->table_ok || ALGO != kDualFree ||
+             (D == 2 && variant == DM_VARIANT_GATHER)) {
+    // face-list gather: traditional algorithm, meshes with node degree > 32,
+    // and the 2D default (<= 2 incidences per edge, one opposite node each:
+    // 2.5x the row-table kernel at 33.5 M triangles, and bitwise the serial
+    // order like it)
     if (int sf = ensure_ifl(c)) return sf;
     tmark(c, 0);
 #define DM_FACES(U, MINB)                                                                     \
@@ -1058,7 +1062,8 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
     st = ensure_rings(c);
     if (st) return st;
   }
-  if ((variant == DM_VARIANT_GATHER_EXACT || (variant == DM_VARIANT_GATHER && !c->ring_ok)) &&
+  if ((variant == DM_VARIANT_GATHER_EXACT ||
+       (variant == DM_VARIANT_GATHER && !c->ring_ok && c->dim == 3)) &&
       algo == DM_NAV_DUALFREE) {
     st = ensure_tables(c);
     if (st) return st;
