@@ -23,7 +23,7 @@ using u64 = std::uint64_t;
 using i64 = std::int64_t;
 
 // ---------------------------------------------------------------- buffers
-// env DUALMESH_ALLOC_TRACE=1: print device allocations / frees slower than 2 ms
+// env DUALMESH_ALLOC_TRACE=1: print driver allocations / frees slower than 2 ms
 inline void alloc_trace(const char* what, size_t bytes, std::chrono::steady_clock::time_point t0) {
   static const bool on = [] {
     const char* e = std::getenv("DUALMESH_ALLOC_TRACE");
@@ -35,6 +35,10 @@ inline void alloc_trace(const char* what, size_t bytes, std::chrono::steady_cloc
   if (ms > 2.0) std::fprintf(stderr, "[alloc] %s %.1f MB %.2f ms\n", what, bytes / 1e6, ms);
 }
 
+// devmem.cu: every device buffer is carved out of large pooled chunks.
+cudaError_t dev_alloc(void** out, size_t bytes);
+void dev_free(void* p);
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -44,11 +48,7 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (p) {
-      const auto t0 = std::chrono::steady_clock::now();
-      cudaFree(p);
-      alloc_trace("cudaFree", n * sizeof(T), t0);
-    }
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }
@@ -62,9 +62,7 @@ struct DevBuf {
     if (count <= n && p) return cudaSuccess;
     release();
     size_t bytes = (count ? count : 1) * sizeof(T);
-    const auto t0 = std::chrono::steady_clock::now();
-    cudaError_t st = cudaMalloc(reinterpret_cast<void**>(&p), bytes);
-    alloc_trace("cudaMalloc", bytes, t0);
+    cudaError_t st = dev_alloc(reinterpret_cast<void**>(&p), bytes);
     if (st == cudaSuccess) n = count;
     else p = nullptr;
     return st;
@@ -88,7 +86,7 @@ struct Arena {
   Arena(const Arena&) = delete;
   Arena& operator=(const Arena&) = delete;
   ~Arena() {
-    for (int b = 0; b < nblocks; ++b) cudaFree(blocks[b].p);
+    for (int b = 0; b < nblocks; ++b) dev_free(blocks[b].p);
   }
   cudaError_t take(size_t bytes, void** out, size_t min_block) {
     bytes = (bytes + 255) & ~size_t(255);
@@ -104,10 +102,8 @@ struct Arena {
     }
     if (nblocks == 16) return cudaErrorMemoryAllocation;
     const size_t sz = bytes > min_block ? bytes : min_block;
-    const auto t0 = std::chrono::steady_clock::now();
     char* p = nullptr;
-    cudaError_t st = cudaMalloc(reinterpret_cast<void**>(&p), sz);
-    alloc_trace("cudaMalloc(arena)", sz, t0);
+    cudaError_t st = dev_alloc(reinterpret_cast<void**>(&p), sz);
     if (st != cudaSuccess) return st;
     blocks[nblocks++] = {p, sz};
     cur = nblocks - 1;
