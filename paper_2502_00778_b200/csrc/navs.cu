@@ -195,8 +195,19 @@ __device__ __forceinline__ void store_navs_warp(const double* n, i64 wbase, i64 
 // Per-lane store of one 3D navs row (24 bytes at 24e): one 16-byte and one
 // 8-byte store, ordered by the row's 16-byte alignment (e even: xy | z,
 // e odd: x | yz).
+template <bool CS = false>
 __device__ __forceinline__ void store_nav_row(double* __restrict__ navs, i64 e, const double* n) {
   double* r = navs + 3 * e;
+  if constexpr (CS) {
+    if ((e & 1) == 0) {
+      st_cs2(r, n[0], n[1]);
+      st_cs(r + 2, n[2]);
+    } else {
+      st_cs(r, n[0]);
+      st_cs2(r + 1, n[1], n[2]);
+    }
+    return;
+  }
   if ((e & 1) == 0) {
     *reinterpret_cast<double2*>(r) = make_double2(n[0], n[1]);
     r[2] = n[2];
@@ -384,7 +395,7 @@ static_assert(sizeof(double) * 2 * 512 % 16 == 0 && (kPipeCodeCap / 2 + 4) % 4 =
 
 __device__ __forceinline__ int meta_nu(const int4& m) { return m.z & 0xffff; }
 
-template <int CAP, bool FILL = true>
+template <int CAP, bool FILL = true, int OPT = 0>
 __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, const int4& m,
                                            const int (&ids)[CAP / kEB],
                                            const double2* __restrict__ mxy,
@@ -398,7 +409,8 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
     for (int u = 0; u < CAP / kEB; ++u) {
       const int i = t + u * kEB;
       if (i < nu && ids[u] >= 0) {  // recoloured tables have holes (rings.cu)
-        cp_async16(&S.xy[b][i], mxy + ids[u]);
+        if (OPT & 1) cp_async16_cg(&S.xy[b][i], mxy + ids[u]);
+        else cp_async16(&S.xy[b][i], mxy + ids[u]);
         cp_async8(&S.z[b][i], mz + ids[u]);
       }
     }
@@ -406,7 +418,10 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
   if (m.y <= kPipeCodeBytes) {
     // code blocks are multiples of 32 bytes: 16-byte pieces
     const uint4* src = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x));
-    for (int w = t; w < m.y / 16; w += kEB) cp_async16(&S.cd[b][4 * w], src + w);
+    for (int w = t; w < m.y / 16; w += kEB) {
+      if (OPT & 1) cp_async16_cg(&S.cd[b][4 * w], src + w);
+      else cp_async16(&S.cd[b][4 * w], src + w);
+    }
   }
   if (t == 0) cp_async16(&S.wo[b], meta + 2 * tile + 1);
 }
@@ -414,16 +429,17 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
 // node ids and this thread's edge id of `tile` into registers (always the
 // full CAP window: the tile list has a fixed stride, so no dependency on the
 // tile's metadata).
-template <int NI>
+template <int NI, bool NA = false>
 __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __restrict__ tnodes,
                                          const int32_t* __restrict__ eperm, i64 ne,
                                          int (&ids)[NI], int& eid) {
   if (tile < ntiles) {
     const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
 #pragma unroll
-    for (int u = 0; u < NI; ++u) ids[u] = __ldg(tn + threadIdx.x + u * kEB);
+    for (int u = 0; u < NI; ++u)
+      ids[u] = NA ? ld_na(tn + threadIdx.x + u * kEB) : __ldg(tn + threadIdx.x + u * kEB);
     const i64 p = static_cast<i64>(tile) * kEB + threadIdx.x;
-    eid = p < ne ? __ldg(eperm + p) : 0;
+    eid = p < ne ? (NA ? ld_na(eperm + p) : __ldg(eperm + p)) : 0;
   }
 }
 
@@ -550,7 +566,13 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
   acc[2] = a2;
 }
 
-template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree>
+// OPT (valid results, all bitwise identical): 1 the (x, y) table and code
+// fill bypasses L1 (cp.async.cg: nothing a tile fills is re-read through
+// this SM's L1; C5 2.22 -> 2.17 ms), 2 streaming (evict-first) navs / s
+// stores (no change), 4 node ids / edge ids / metadata loaded with
+// L1::no_allocate (2.17 -> 2.19 ms)
+template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
+          int OPT = 1>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint8_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
@@ -567,12 +589,12 @@ __global__ void __launch_bounds__(kEB, MINB)
   int ids[CAP / kEB];
   int e_nxt = 0;
   int4 m_cur = __ldg(meta + 2 * tile);
-  pipe_ids(tile, ntiles, tnodes, eperm, ne, ids, e_nxt);
+  pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile, ntiles, tnodes, eperm, ne, ids, e_nxt);
   int e_cur = e_nxt;
-  pipe_issue(S, 0, tile, m_cur, ids, mxy, mz, rcodes, meta);
+  pipe_issue<CAP, true, OPT>(S, 0, tile, m_cur, ids, mxy, mz, rcodes, meta);
   cp_async_commit();
   int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
-  pipe_ids(tile + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
+  pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int b = it & 1;
     const int nxt = tile + G;
@@ -581,8 +603,8 @@ __global__ void __launch_bounds__(kEB, MINB)
     // 8 no ring walk, 16 component-major navs stores, 32 one 32-byte row
     // (navs, s) per edge
     if (nxt < ntiles) {
-      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false>(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
-      else pipe_issue(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
+      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
+      else pipe_issue<CAP, true, OPT>(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
     }
     cp_async_commit();
     const int4 m = m_cur;
@@ -594,8 +616,9 @@ __global__ void __launch_bounds__(kEB, MINB)
     asm volatile("" ::"r"(m.w));
     m_cur = m_nxt;
     e_cur = e_nxt;
-    m_nxt = nxt + G < ntiles ? __ldg(meta + 2 * (nxt + G)) : make_int4(0, 0, 0, 0);
-    pipe_ids(nxt + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
+    m_nxt = nxt + G < ntiles ? ((OPT & 4) ? ld_na4(meta + 2 * (nxt + G)) : __ldg(meta + 2 * (nxt + G)))
+                            : make_int4(0, 0, 0, 0);
+    pipe_ids<CAP / kEB, (OPT & 4) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
     cp_async_wait<1>();
     __syncthreads();
     // ---- evaluate tile `tile` from buffer b
@@ -660,8 +683,11 @@ __global__ void __launch_bounds__(kEB, MINB)
       // scale pass; boundary edges get their facet terms (and s) from
       // k_ring_boundary, launched right after on the same stream
       edge_tail_values<3, ALGO>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
-      if (!(FAKE & 34) || s == -12345.0)
-        svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
+      if (!(FAKE & 34) || s == -12345.0) {
+        double* sp = svals + (pos_s ? p : static_cast<i64>(e));  // rings.cu: vol_by_rank
+        if (OPT & 2) st_cs(sp, s);
+        else *sp = s;
+      }
     }
     if (FAKE & 32) {  // probe: one 32-byte (x, y, z, s) row per edge
       if (valid) {
@@ -681,7 +707,7 @@ __global__ void __launch_bounds__(kEB, MINB)
         navs[2 * ne + e] = nv[2];
       }
     } else if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) {
-      store_nav_row(navs, e, nv);
+      store_nav_row<(OPT & 2) != 0>(navs, e, nv);
     }
     __syncthreads();  // buffer b is refilled next iteration
   }
@@ -977,6 +1003,9 @@ int launch_navs(dm_ctx* c, int variant) {
           case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16>, sizeof(PipeSmem<256>)); break;
           case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3>, sizeof(PipeSmem<256>)); break;
           case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32>, sizeof(PipeSmem<256>)); break;
+          case 30: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 0>, sizeof(PipeSmem<256>)); break;
+          case 33: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 3>, sizeof(PipeSmem<256>)); break;
+          case 35: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 5>, sizeof(PipeSmem<256>)); break;
           default: st = launch(k_navs_ring_pipe<256, 4, 1>, sizeof(PipeSmem<256>)); break;
         }
       } else {
