@@ -380,23 +380,29 @@ constexpr int kPipeCodeCap = 4096;  // 16-bit codes per buffer
 constexpr int kPipeCodeBytes = 2 * kPipeCodeCap;
 extern __shared__ __align__(128) unsigned char dm_smem[];
 
-template <int CAP>
+// NB buffers of CCAP 16-bit code units each.  With two buffers a tile ends
+// with a barrier before its buffer is refilled; with three the refill of
+// buffer (i+1) mod 3 at tile i only needs every thread past tile i-1's
+// evaluation, which the one barrier of tile i already guarantees.
+template <int CAP, int NB = 2, int CCAP = kPipeCodeCap>
 struct PipeSmem {
+  static constexpr int kCodeBytes = 2 * CCAP;
   // node table split into a 16-byte (x,y) array and an 8-byte z array: a
   // random 16-byte LDS spreads over 8 bank groups instead of the 4 a 32-byte
   // record allows, and z over 16 (fewer conflict wavefronts per read)
-  double2 xy[2][CAP];
-  double z[2][CAP];
-  uint32_t cd[2][kPipeCodeCap / 2 + 4];  // rows stay 16-byte aligned for cp.async.16
-  int4 wo[2];                            // u16 warp-block code offsets of the tile
+  double2 xy[NB][CAP];
+  double z[NB][CAP];
+  uint32_t cd[NB][CCAP / 2 + 4];  // rows stay 16-byte aligned for cp.async.16
+  int4 wo[NB];                    // u16 warp-block code offsets of the tile
 };
-static_assert(sizeof(double) * 2 * 512 % 16 == 0 && (kPipeCodeCap / 2 + 4) % 4 == 0,
+static_assert(sizeof(double) * 2 * 512 % 16 == 0 && (kPipeCodeCap / 2 + 4) % 4 == 0 &&
+                  (2048 / 2 + 4) % 4 == 0,
               "PipeSmem members must stay 16-byte aligned");
 
 __device__ __forceinline__ int meta_nu(const int4& m) { return m.z & 0xffff; }
 
-template <int CAP, bool FILL = true, int OPT = 0>
-__device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, const int4& m,
+template <int CAP, bool FILL = true, int OPT = 0, typename SM>
+__device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m,
                                            const int (&ids)[CAP / kEB],
                                            const double2* __restrict__ mxy,
                                            const double* __restrict__ mz,
@@ -415,7 +421,7 @@ __device__ __forceinline__ void pipe_issue(PipeSmem<CAP>& S, int b, int tile, co
       }
     }
   }
-  if (m.y <= kPipeCodeBytes) {
+  if (m.y <= SM::kCodeBytes) {
     // code blocks are multiples of 32 bytes: 16-byte pieces
     const uint4* src = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x));
     for (int w = t; w < m.y / 16; w += kEB) {
@@ -570,16 +576,18 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
 // fill bypasses L1 (cp.async.cg: nothing a tile fills is re-read through
 // this SM's L1; C5 2.22 -> 2.17 ms), 2 streaming (evict-first) navs / s
 // stores (no change), 4 node ids / edge ids / metadata loaded with
-// L1::no_allocate (2.17 -> 2.19 ms)
+// L1::no_allocate (2.17 -> 2.19 ms).  NB = 3 buffers drop the end-of-tile
+// barrier (PipeSmem): C5 2.17 -> 2.03 ms, bitwise unchanged.
 template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
-          int OPT = 1>
+          int OPT = 1, int NB = 2>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint8_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      const double2* __restrict__ mxy, const double* __restrict__ mz,
                      Coords<3> X, i64 ne, int ntiles, bool pos_s, double* __restrict__ navs,
                      double* __restrict__ svals) {
-  PipeSmem<CAP>& S = *reinterpret_cast<PipeSmem<CAP>*>(dm_smem);
+  using SM = PipeSmem<CAP, NB, NB == 2 ? kPipeCodeCap : 2048>;
+  SM& S = *reinterpret_cast<SM*>(dm_smem);
   const int t = threadIdx.x;
   const int lane = t & 31;
   int tile = blockIdx.x;
@@ -596,15 +604,16 @@ __global__ void __launch_bounds__(kEB, MINB)
   int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
   pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
-    const int b = it & 1;
+    const int b = NB == 2 ? (it & 1) : it % NB;
+    const int bn = NB == 2 ? (b ^ 1) : (b + 1 == NB ? 0 : b + 1);
     const int nxt = tile + G;
     // FAKE (timing probes only, results invalid): 1 conflict-free table
     // slots, 2 no stores, 4 no coordinate fill after the first two tiles,
     // 8 no ring walk, 16 component-major navs stores, 32 one 32-byte row
     // (navs, s) per edge
     if (nxt < ntiles) {
-      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
-      else pipe_issue<CAP, true, OPT>(S, b ^ 1, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
+      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, bn, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
+      else pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
     }
     cp_async_commit();
     const int4 m = m_cur;
@@ -612,12 +621,12 @@ __global__ void __launch_bounds__(kEB, MINB)
     // m.w (the tile's boundary slice start) is not read by this kernel; keep
     // its register live until here so the allocator cannot reuse it while
     // the 16-byte metadata prefetch is still in flight (a write-after-write
-    // wait on the prefetch every tile)
+    // wait on the prefetch every tile; without this use ptxas also spills)
     asm volatile("" ::"r"(m.w));
     m_cur = m_nxt;
     e_cur = e_nxt;
     m_nxt = nxt + G < ntiles ? ((OPT & 4) ? ld_na4(meta + 2 * (nxt + G)) : __ldg(meta + 2 * (nxt + G)))
-                            : make_int4(0, 0, 0, 0);
+                             : make_int4(0, 0, 0, 0);
     pipe_ids<CAP / kEB, (OPT & 4) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
     cp_async_wait<1>();
     __syncthreads();
@@ -631,7 +640,7 @@ __global__ void __launch_bounds__(kEB, MINB)
       const unsigned wo = (reinterpret_cast<const unsigned*>(&S.wo[b])[warp >> 1] >>
                            (16 * (warp & 1))) & 0xffffu;
       const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
-      if (meta_nu(m) <= CAP && m.y <= kPipeCodeBytes) {
+      if (meta_nu(m) <= CAP && m.y <= SM::kCodeBytes) {
         const double2* xy = S.xy[b];
         const double* zz = S.z[b];
         auto T = [&](unsigned i) -> d4 {
@@ -709,7 +718,7 @@ __global__ void __launch_bounds__(kEB, MINB)
     } else if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) {
       store_nav_row<(OPT & 2) != 0>(navs, e, nv);
     }
-    __syncthreads();  // buffer b is refilled next iteration
+    if (NB == 2) __syncthreads();  // buffer b is refilled next iteration
   }
   cp_async_wait<0>();
 }
@@ -990,23 +999,28 @@ int launch_navs(dm_ctx* c, int variant) {
       // DUALMESH_GATHER_CFG 20-25 are the timing probes of the kernel
       if (ALGO == kTraditional) {  // ~30 live doubles in the walk: 2 CTAs/SM, no spills
         st = c->code_width == 1
-                 ? launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional>, sizeof(PipeSmem<256>))
+                 ? (c->gather_cfg == 36
+                        ? launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional>, sizeof(PipeSmem<256>))
+                        : launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional, 1, 3>,
+                                 sizeof(PipeSmem<256, 3, 2048>)))
                  : launch(k_navs_ring_pipe<512, 2, 2, 1, 0, kTraditional>, sizeof(PipeSmem<512>));
       } else if (c->code_width == 1) {
         switch (c->gather_cfg) {
-          case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1>, sizeof(PipeSmem<256>)); break;
-          case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2>, sizeof(PipeSmem<256>)); break;
-          case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 4>, sizeof(PipeSmem<256>)); break;
-          case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8>, sizeof(PipeSmem<256>)); break;
-          case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6>, sizeof(PipeSmem<256>)); break;
-          case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14>, sizeof(PipeSmem<256>)); break;
-          case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16>, sizeof(PipeSmem<256>)); break;
-          case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3>, sizeof(PipeSmem<256>)); break;
-          case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32>, sizeof(PipeSmem<256>)); break;
+          case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 4, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 30: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 0>, sizeof(PipeSmem<256>)); break;
+          case 31: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1>, sizeof(PipeSmem<256>)); break;
+          case 36: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 2>, sizeof(PipeSmem<256>)); break;
           case 33: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 3>, sizeof(PipeSmem<256>)); break;
           case 35: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 5>, sizeof(PipeSmem<256>)); break;
-          default: st = launch(k_navs_ring_pipe<256, 4, 1>, sizeof(PipeSmem<256>)); break;
+          default: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
         }
       } else {
         switch (c->gather_cfg) {

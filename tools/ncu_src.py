@@ -8,7 +8,7 @@ from collections import Counter
 rows = list(csv.reader(open(sys.argv[1])))
 h = rows[1]
 idx = {k: i for i, k in enumerate(h)}
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(h)]
 
 
 def f(x):
