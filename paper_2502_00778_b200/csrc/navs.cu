@@ -394,6 +394,7 @@ struct PipeSmem {
   double z[NB][CAP];
   uint32_t cd[NB][CCAP / 2 + 4];  // rows stay 16-byte aligned for cp.async.16
   int4 wo[NB];                    // u16 warp-block code offsets of the tile
+  uint64_t full[NB], empty[NB];   // mbarrier pipeline (OPT & 16)
 };
 static_assert(sizeof(double) * 2 * 512 % 16 == 0 && (kPipeCodeCap / 2 + 4) % 4 == 0 &&
                   (2048 / 2 + 4) % 4 == 0,
@@ -576,8 +577,9 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
 // fill bypasses L1 (cp.async.cg: nothing a tile fills is re-read through
 // this SM's L1; C5 2.22 -> 2.17 ms), 2 streaming (evict-first) navs / s
 // stores (no change), 4 node ids / edge ids / metadata loaded with
-// L1::no_allocate (2.17 -> 2.19 ms).  NB = 3 buffers drop the end-of-tile
-// barrier (PipeSmem): C5 2.17 -> 2.03 ms, bitwise unchanged.
+// L1::no_allocate (2.17 -> 2.19 ms), 16 mbarrier pipeline instead of the
+// tile barrier (NB = 3 only: 2.035 -> 2.015 ms).  NB = 3 buffers drop the
+// end-of-tile barrier (PipeSmem): C5 2.17 -> 2.035 ms.  All bitwise unchanged.
 template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
           int OPT = 1, int NB = 2>
 __global__ void __launch_bounds__(kEB, MINB)
@@ -593,6 +595,21 @@ __global__ void __launch_bounds__(kEB, MINB)
   int tile = blockIdx.x;
   if (tile >= ntiles) return;
   const int G = gridDim.x;
+  // OPT & 16: mbarrier pipeline (NB == 3) -- each thread's cp.async fills
+  // arrive on full[buffer]; each warp arrives on empty[buffer] after its
+  // evaluation; a warp waits only for the fill it reads and, before
+  // refilling a buffer, for every warp to be done with its previous use
+  constexpr bool MB = (OPT & 16) != 0;
+  static_assert(!MB || NB == 3, "the mbarrier pipeline uses three buffers");
+  if (MB) {
+    if (t == 0) {
+      for (int i = 0; i < NB; ++i) {
+        mbar_init(&S.full[i], kEB);
+        mbar_init(&S.empty[i], kEB / 32);
+      }
+    }
+    __syncthreads();
+  }
   // prologue: tile 0 -> buffer 0; ids / metadata of tile 1 into registers
   int ids[CAP / kEB];
   int e_nxt = 0;
@@ -600,7 +617,8 @@ __global__ void __launch_bounds__(kEB, MINB)
   pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile, ntiles, tnodes, eperm, ne, ids, e_nxt);
   int e_cur = e_nxt;
   pipe_issue<CAP, true, OPT>(S, 0, tile, m_cur, ids, mxy, mz, rcodes, meta);
-  cp_async_commit();
+  if (MB) cp_async_mbar_arrive(&S.full[0]);
+  else cp_async_commit();
   int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
   pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
@@ -612,10 +630,13 @@ __global__ void __launch_bounds__(kEB, MINB)
     // 8 no ring walk, 16 component-major navs stores, 32 one 32-byte row
     // (navs, s) per edge
     if (nxt < ntiles) {
+      // buffer bn's use (it + 1) / 3 waits for its previous use to be read
+      if (MB && it >= 2) mbar_wait(&S.empty[bn], static_cast<unsigned>((it + 1) / 3 - 1) & 1u);
       if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, bn, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
       else pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
+      if (MB) cp_async_mbar_arrive(&S.full[bn]);
     }
-    cp_async_commit();
+    if (!MB) cp_async_commit();
     const int4 m = m_cur;
     const int e = e_cur;
     // m.w (the tile's boundary slice start) is not read by this kernel; keep
@@ -628,8 +649,12 @@ __global__ void __launch_bounds__(kEB, MINB)
     m_nxt = nxt + G < ntiles ? ((OPT & 4) ? ld_na4(meta + 2 * (nxt + G)) : __ldg(meta + 2 * (nxt + G)))
                              : make_int4(0, 0, 0, 0);
     pipe_ids<CAP / kEB, (OPT & 4) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
-    cp_async_wait<1>();
-    __syncthreads();
+    if (MB) {
+      mbar_wait(&S.full[b], static_cast<unsigned>(it / 3) & 1u);
+    } else {
+      cp_async_wait<1>();
+      __syncthreads();
+    }
     // ---- evaluate tile `tile` from buffer b
     const i64 p = static_cast<i64>(tile) * kEB + t;
     const bool valid = p < ne;
@@ -719,6 +744,10 @@ __global__ void __launch_bounds__(kEB, MINB)
       store_nav_row<(OPT & 2) != 0>(navs, e, nv);
     }
     if (NB == 2) __syncthreads();  // buffer b is refilled next iteration
+    if (MB) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[b]);
+    }
   }
   cp_async_wait<0>();
 }
@@ -1018,9 +1047,10 @@ int launch_navs(dm_ctx* c, int variant) {
           case 30: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 0>, sizeof(PipeSmem<256>)); break;
           case 31: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1>, sizeof(PipeSmem<256>)); break;
           case 36: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 2>, sizeof(PipeSmem<256>)); break;
+          case 37: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 33: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 3>, sizeof(PipeSmem<256>)); break;
           case 35: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 5>, sizeof(PipeSmem<256>)); break;
-          default: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          default: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
         }
       } else {
         switch (c->gather_cfg) {
