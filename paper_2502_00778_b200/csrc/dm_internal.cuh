@@ -286,6 +286,12 @@ inline int fail(dm_ctx* c, int code, const std::string& msg) {
 constexpr int kTileEdges = 256;
 // Ring path (rings.cu): unique nodes per tile, incidences per edge.
 constexpr int kTileNodeCap = 1536;
+// 8-bit (256-node) plans keep, behind a tile's slot table in its tnodes row,
+// the tile's ranks in ascending order (kTileFillRanks, -1 padded) and their
+// recoloured slots as bytes (kTileFillSlots): the ring kernel's fill then
+// reads its sources in rank order (rings.cu k_tile_color_warp)
+constexpr int kTileFillRanks = 256;
+constexpr int kTileFillSlots = 512;
 constexpr int kRingMax = 24;
 
 inline unsigned grid_for(i64 n, int per_block) {

@@ -405,6 +405,7 @@ __device__ __forceinline__ int meta_nu(const int4& m) { return m.z & 0xffff; }
 template <int CAP, bool FILL = true, int OPT = 0, typename SM>
 __device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m,
                                            const int (&ids)[CAP / kEB],
+                                           const int (&sl)[CAP / kEB],
                                            const double2* __restrict__ mxy,
                                            const double* __restrict__ mz,
                                            const uint8_t* __restrict__ rcodes,
@@ -414,8 +415,10 @@ __device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m
   if (FILL && nu <= CAP) {
 #pragma unroll
     for (int u = 0; u < CAP / kEB; ++u) {
-      const int i = t + u * kEB;
-      if (i < nu && ids[u] >= 0) {  // recoloured tables have holes (rings.cu)
+      // OPT & 32: thread i copies the i-th smallest rank into its slot
+      // (coalesced sources); else slot i's rank (recoloured tables have holes)
+      const int i = (OPT & 32) ? sl[u] : t + u * kEB;
+      if (((OPT & 32) || i < nu) && ids[u] >= 0) {
         if (OPT & 1) cp_async16_cg(&S.xy[b][i], mxy + ids[u]);
         else cp_async16(&S.xy[b][i], mxy + ids[u]);
         cp_async8(&S.z[b][i], mz + ids[u]);
@@ -436,15 +439,21 @@ __device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m
 // node ids and this thread's edge id of `tile` into registers (always the
 // full CAP window: the tile list has a fixed stride, so no dependency on the
 // tile's metadata).
-template <int NI, bool NA = false>
+template <int NI, bool NA = false, bool SF = false>
 __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __restrict__ tnodes,
                                          const int32_t* __restrict__ eperm, i64 ne,
-                                         int (&ids)[NI], int& eid) {
+                                         int (&ids)[NI], int (&sl)[NI], int& eid) {
   if (tile < ntiles) {
     const int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
+    if constexpr (SF) {  // sorted fill list of a coloured 256-node table (rings.cu)
+      static_assert(NI == 1, "sorted fill lists hold 256 nodes");
+      ids[0] = __ldg(tn + kTileFillRanks + threadIdx.x);
+      sl[0] = __ldg(reinterpret_cast<const uint8_t*>(tn + kTileFillSlots) + threadIdx.x);
+    } else {
 #pragma unroll
-    for (int u = 0; u < NI; ++u)
-      ids[u] = NA ? ld_na(tn + threadIdx.x + u * kEB) : __ldg(tn + threadIdx.x + u * kEB);
+      for (int u = 0; u < NI; ++u)
+        ids[u] = NA ? ld_na(tn + threadIdx.x + u * kEB) : __ldg(tn + threadIdx.x + u * kEB);
+    }
     const i64 p = static_cast<i64>(tile) * kEB + threadIdx.x;
     eid = p < ne ? (NA ? ld_na(eperm + p) : __ldg(eperm + p)) : 0;
   }
@@ -578,7 +587,8 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
 // this SM's L1; C5 2.22 -> 2.17 ms), 2 streaming (evict-first) navs / s
 // stores (no change), 4 node ids / edge ids / metadata loaded with
 // L1::no_allocate (2.17 -> 2.19 ms), 16 mbarrier pipeline instead of the
-// tile barrier (NB = 3 only: 2.035 -> 2.015 ms).  NB = 3 buffers drop the
+// tile barrier (NB = 3 only: 2.035 -> 2.015 ms), 32 the table fill walks the
+// tile's rank-ordered fill list (coloured 256-node plans only).  NB = 3 buffers drop the
 // end-of-tile barrier (PipeSmem): C5 2.17 -> 2.035 ms.  All bitwise unchanged.
 template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
           int OPT = 1, int NB = 2>
@@ -611,16 +621,16 @@ __global__ void __launch_bounds__(kEB, MINB)
     __syncthreads();
   }
   // prologue: tile 0 -> buffer 0; ids / metadata of tile 1 into registers
-  int ids[CAP / kEB];
+  int ids[CAP / kEB], sl[CAP / kEB];
   int e_nxt = 0;
   int4 m_cur = __ldg(meta + 2 * tile);
-  pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile, ntiles, tnodes, eperm, ne, ids, e_nxt);
+  pipe_ids<CAP / kEB, (OPT & 4) != 0, (OPT & 32) != 0>(tile, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
   int e_cur = e_nxt;
-  pipe_issue<CAP, true, OPT>(S, 0, tile, m_cur, ids, mxy, mz, rcodes, meta);
+  pipe_issue<CAP, true, OPT>(S, 0, tile, m_cur, ids, sl, mxy, mz, rcodes, meta);
   if (MB) cp_async_mbar_arrive(&S.full[0]);
   else cp_async_commit();
   int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
-  pipe_ids<CAP / kEB, (OPT & 4) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
+  pipe_ids<CAP / kEB, (OPT & 4) != 0, (OPT & 32) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int b = NB == 2 ? (it & 1) : it % NB;
     const int bn = NB == 2 ? (b ^ 1) : (b + 1 == NB ? 0 : b + 1);
@@ -632,8 +642,8 @@ __global__ void __launch_bounds__(kEB, MINB)
     if (nxt < ntiles) {
       // buffer bn's use (it + 1) / 3 waits for its previous use to be read
       if (MB && it >= 2) mbar_wait(&S.empty[bn], static_cast<unsigned>((it + 1) / 3 - 1) & 1u);
-      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, bn, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
-      else pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, mxy, mz, rcodes, meta);
+      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
+      else pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
       if (MB) cp_async_mbar_arrive(&S.full[bn]);
     }
     if (!MB) cp_async_commit();
@@ -648,7 +658,7 @@ __global__ void __launch_bounds__(kEB, MINB)
     e_cur = e_nxt;
     m_nxt = nxt + G < ntiles ? ((OPT & 4) ? ld_na4(meta + 2 * (nxt + G)) : __ldg(meta + 2 * (nxt + G)))
                              : make_int4(0, 0, 0, 0);
-    pipe_ids<CAP / kEB, (OPT & 4) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, e_nxt);
+    pipe_ids<CAP / kEB, (OPT & 4) != 0, (OPT & 32) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
     if (MB) {
       mbar_wait(&S.full[b], static_cast<unsigned>(it / 3) & 1u);
     } else {
@@ -1030,27 +1040,32 @@ int launch_navs(dm_ctx* c, int variant) {
         st = c->code_width == 1
                  ? (c->gather_cfg == 36
                         ? launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional>, sizeof(PipeSmem<256>))
-                        : launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional, 1, 3>,
+                        : launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional, 17, 3>,
                                  sizeof(PipeSmem<256, 3, 2048>)))
                  : launch(k_navs_ring_pipe<512, 2, 2, 1, 0, kTraditional>, sizeof(PipeSmem<512>));
       } else if (c->code_width == 1) {
         switch (c->gather_cfg) {
-          case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 4, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 4, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 30: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 0>, sizeof(PipeSmem<256>)); break;
           case 31: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1>, sizeof(PipeSmem<256>)); break;
           case 36: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 2>, sizeof(PipeSmem<256>)); break;
           case 37: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 33: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 3>, sizeof(PipeSmem<256>)); break;
           case 35: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 5>, sizeof(PipeSmem<256>)); break;
-          default: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 38: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          default:  // coloured plans carry the rank-ordered fill list (OPT & 32)
+            st = c->plan_colored
+                     ? launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 3>, sizeof(PipeSmem<256, 3, 2048>))
+                     : launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>));
+            break;
         }
       } else {
         switch (c->gather_cfg) {

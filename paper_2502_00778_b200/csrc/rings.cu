@@ -340,7 +340,13 @@ __global__ void __launch_bounds__(kTileEdges)
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
   const int4 m = meta[2 * tile];
   const int nu = m.z & 0xffff, nbytes = m.y;
-  if (nu > 256 || nbytes > static_cast<int>(sizeof(cb))) return;
+  if (nu > 256) return;
+  int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
+  if (nbytes > static_cast<int>(sizeof(cb))) {  // not recoloured: identity fill list
+    tn[kTileFillRanks + t] = t < nu ? tn[t] : -1;
+    reinterpret_cast<uint8_t*>(tn + kTileFillSlots)[t] = static_cast<uint8_t>(t);
+    return;
+  }
   for (int i = t; i < nbytes / 16; i += kTileEdges)
     reinterpret_cast<uint4*>(cb)[i] = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x))[i];
   const i64 left = ne - static_cast<i64>(tile) * kTileEdges;
@@ -474,12 +480,14 @@ __global__ void __launch_bounds__(kTileEdges)
       slot_new[t] = static_cast<uint8_t>(cv + 16 * k);
     }
   }
-  int32_t* tn = tnodes + static_cast<i64>(tile) * kTileNodeCap;
   ids[t] = -1;
   __syncthreads();
-  if (t < nu) ids[slot_new[t]] = tn[t];
+  const int32_t rank_t = t < nu ? tn[t] : -1;  // old slot t = t-th smallest rank
+  if (t < nu) ids[slot_new[t]] = rank_t;
   __syncthreads();
   tn[t] = ids[t];
+  tn[kTileFillRanks + t] = rank_t;
+  reinterpret_cast<uint8_t*>(tn + kTileFillSlots)[t] = t < nu ? slot_new[t] : 0;
   for (int st = 0; st < nl + 3; ++st) {
     uint8_t* p = cb + wofs[w] + 32 + st * 32 + l;
     *p = slot_new[*p];
@@ -504,6 +512,8 @@ __global__ void k_sum_u32(const u32* __restrict__ x, i64 n, unsigned long long* 
 
 // ---- Morton origin order and the edge permutation
 
+static_assert(kTileFillSlots + 256 / 4 <= kTileNodeCap && kTileFillRanks + 256 <= kTileFillSlots,
+              "fill lists fit behind the 256-slot table");
 static_assert(kTileNodeCap <= 2048 && kRingMax < 32, "code word 1 packs slot(k) | n << 11");
 static_assert(kRingMax + 4 <= 64 && kTileEdges / 32 * 64 * (kRingMax + 4) < 65536,
               "u16 warp-block byte offsets");
