@@ -386,6 +386,7 @@ extern __shared__ __align__(128) unsigned char dm_smem[];
 // evaluation, which the one barrier of tile i already guarantees.
 template <int CAP, int NB = 2, int CCAP = kPipeCodeCap>
 struct PipeSmem {
+  static_assert((CCAP / 2 + 4) % 4 == 0, "code rows stay 16-byte aligned");
   static constexpr int kCodeBytes = 2 * CCAP;
   // node table split into a 16-byte (x,y) array and an 8-byte z array: a
   // random 16-byte LDS spreads over 8 bank groups instead of the 4 a 32-byte
@@ -591,14 +592,14 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
 // tile's rank-ordered fill list (coloured 256-node plans only).  NB = 3 buffers drop the
 // end-of-tile barrier (PipeSmem): C5 2.17 -> 2.035 ms.  All bitwise unchanged.
 template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
-          int OPT = 1, int NB = 2>
+          int OPT = 1, int NB = 2, int CCAP = (NB == 2 ? kPipeCodeCap : 2048)>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint8_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
                      const double2* __restrict__ mxy, const double* __restrict__ mz,
                      Coords<3> X, i64 ne, int ntiles, bool pos_s, double* __restrict__ navs,
                      double* __restrict__ svals) {
-  using SM = PipeSmem<CAP, NB, NB == 2 ? kPipeCodeCap : 2048>;
+  using SM = PipeSmem<CAP, NB, CCAP>;
   SM& S = *reinterpret_cast<SM*>(dm_smem);
   const int t = threadIdx.x;
   const int lane = t & 31;
@@ -1061,6 +1062,9 @@ int launch_navs(dm_ctx* c, int variant) {
           case 33: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 3>, sizeof(PipeSmem<256>)); break;
           case 35: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 5>, sizeof(PipeSmem<256>)); break;
           case 38: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          // tests: a 16-code shared buffer sends every tile down the
+          // global-memory path of the same kernel
+          case 41: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 3, 16>, sizeof(PipeSmem<256, 3, 16>)); break;
           default:  // coloured plans carry the rank-ordered fill list (OPT & 32)
             st = c->plan_colored
                      ? launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 3>, sizeof(PipeSmem<256, 3, 2048>))

@@ -485,6 +485,30 @@ def test_colored_plan_same_bits(name, scale, monkeypatch):
     np.testing.assert_array_equal(out[0][1], out[1][1])
 
 
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C4", 4)])
+def test_ring_global_path_same_bits(name, scale, monkeypatch):
+    """Tiles whose table or codes exceed the ring kernel's shared buffers are
+    evaluated from global memory by the same kernel: forcing every tile down
+    that path (DUALMESH_GATHER_CFG=41, a 16-code buffer) gives the same bits."""
+    from paper_2502_00778_b200 import Engine
+    m = meshgen.baseline_config(name, scale)
+    out = []
+    for cfg in ("0", "41"):
+        monkeypatch.setenv("DUALMESH_GATHER_CFG", cfg)
+        eng = Engine(0)
+        try:
+            eng.set_mesh(m)
+            eng.build_edges()
+            eng.navs(DF, GATHER)
+            eng.volumes(EDGE)
+            assert eng.plan_info()["ring_ok"]
+            out.append((eng.get_navs(), eng.get_volumes()))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+
+
 def test_twice_c5_scale():
     """A 320^3 Kuhn cube (196.6 M tets, 230 M edges; device-generated): the
     ring plan (codes beyond 2 GB, coloured 256-node tables) and the SPEC
