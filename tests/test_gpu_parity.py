@@ -4,6 +4,8 @@ edge structures bit-exact; GATHER navs and volumes bitwise equal to the
 serial oracle; SCATTER navs within 1e-12 per edge vector
 (||x_gpu - x_ref||_inf <= 1e-12 ||x_ref||_inf); closure <= 1e-13 scaled;
 |sum V - sum V_E| / sum V_E <= 1e-12."""
+import os
+
 import numpy as np
 import pytest
 
@@ -152,6 +154,36 @@ def test_full_size_properties(engine, name):
     nt = engine.get_navs()
     scale = engine.max_face_area()
     assert np.abs(nt - n1).max() <= 1e-13 * scale
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_full_size_oracle_parity(engine, oracle, name):
+    """BASELINE sizes against the CPU oracle itself: the edge list and origin
+    CSR bit for bit, the serial-order variant (GATHER_EXACT) and the edge
+    volumes bit for bit, the default ring walk within 1e-12 per edge vector
+    (or_metrics_mt on all host threads gives the serial loops' bits)."""
+    m = meshgen.baseline_config(name)
+    engine.set_mesh(m)
+    ne = engine.build_edges()
+    e, o = oracle.build_edges(m)
+    got = engine.edges()
+    assert ne == e.shape[0]
+    np.testing.assert_array_equal(got.edges, e)
+    np.testing.assert_array_equal(got.origin_start, o)
+    plan = oracle.plan(m, e, o)
+    try:
+        want_n, want_v = oracle.metrics_mt(plan, m.coords, os.cpu_count() or 1)
+    finally:
+        oracle.plan_free(plan)
+    engine.navs(DF, EXACT)
+    engine.volumes(EDGE)
+    np.testing.assert_array_equal(engine.get_navs(), want_n)
+    np.testing.assert_array_equal(engine.get_volumes(), want_v)
+    engine.navs(DF, GATHER)
+    engine.volumes(EDGE)
+    assert per_vector_rel(engine.get_navs(), want_n, m.dim) <= 1e-12
+    v = engine.get_volumes()
+    assert np.abs(v - want_v).max() <= 1e-12 * np.abs(want_v).max()
 
 
 def test_corrupt_hook_detected(engine):
