@@ -156,7 +156,7 @@ def test_full_size_properties(engine, name):
     assert np.abs(nt - n1).max() <= 1e-13 * scale
 
 
-@pytest.mark.parametrize("name", ["C3", "C5"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
 def test_full_size_oracle_parity(engine, oracle, name):
     """BASELINE sizes against the CPU oracle itself: the edge list and origin
     CSR bit for bit, the serial-order variant (GATHER_EXACT) and the edge
