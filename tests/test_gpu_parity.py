@@ -156,13 +156,16 @@ def test_full_size_properties(engine, name):
     assert np.abs(nt - n1).max() <= 1e-13 * scale
 
 
-@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C5", "2D-2048"])
 def test_full_size_oracle_parity(engine, oracle, name):
     """BASELINE sizes against the CPU oracle itself: the edge list and origin
     CSR bit for bit, the serial-order variant (GATHER_EXACT) and the edge
     volumes bit for bit, the default ring walk within 1e-12 per edge vector
     (or_metrics_mt on all host threads gives the serial loops' bits)."""
-    m = meshgen.baseline_config(name)
+    if name == "2D-2048":  # the C1 family at 2048^2 quads (8.4 M triangles)
+        m = meshgen.tri_square(2048, diag_seed=meshgen.SEED_DIAG, amp=0.2, seed=meshgen.SEED_JITTER)
+    else:
+        m = meshgen.baseline_config(name)
     engine.set_mesh(m)
     ne = engine.build_edges()
     e, o = oracle.build_edges(m)
