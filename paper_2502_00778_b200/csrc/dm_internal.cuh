@@ -215,7 +215,6 @@ struct dm_ctx {
   bool have_navs = false, have_vols = false;
   int navs_algo = -1;
   dm::DevBuf<double> navs, svals, vols, velem;
-  dm::DevBuf<double> bterms;  // ring path: fb * n_B per boundary facet
   bool svals_pos = false;  // svals indexed by ring position p (rings.cu), not edge id
 
   // verify / reductions scratch

@@ -11,7 +11,7 @@
 //   GATHER (default, 3D): the ring walk over the Morton-tile plan of rings.cu
 //       (k_navs_ring_pipe): one new table node per incidence, persistent CTAs
 //       with a double-buffered cp.async pipeline; dual-free (K3 in
-//       k_facet_terms + k_ring_boundary) and traditional forms; <= 1e-12 of
+//       k_ring_boundary) and traditional forms; <= 1e-12 of
 //       the serial loop, deterministic.
 //   GATHER_EXACT: row-table gather (k_navs_gather) summing in ascending
 //       element id -- bitwise the serial oracle; traditional: face list.
@@ -931,24 +931,14 @@ __global__ void __launch_bounds__(kEB)
 // edge, adds its facets' terms in ascending facet id to the scaled navs row
 // and recomputes s -- the same values added in the same order as the fused
 // tail, so the same bits.
-__global__ void __launch_bounds__(256)
-    k_facet_terms(Coords<3> X, const int32_t* __restrict__ bnd, i64 nB,
-                  double* __restrict__ terms) {
-  const i64 f = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (f >= nB) return;
-  constexpr double fb = 1.0 / 12.0;
-  double b0, b1, b2;
-  bnormal3(X, bnd + 3 * f, b0, b1, b2);
-  terms[3 * f] = fb * b0;
-  terms[3 * f + 1] = fb * b1;
-  terms[3 * f + 2] = fb * b2;
-}
-
+// Boundary pass of the ring path: one thread per boundary edge adds
+// fb * n_B of its facets (ascending facet id) to the scaled row and recomputes
+// s.  The facet terms are evaluated per edge from the facet's nodes (a
+// separate per-facet pass measured 0.0025 ms slower at C5 for the same bits).
 __global__ void __launch_bounds__(256)
     k_ring_boundary(const int4* __restrict__ seg, const u32* __restrict__ start, i64 ns,
-                    const u64* __restrict__ bedge_p, Coords<3> X,
-                    const double* __restrict__ terms, bool pos_s, double* __restrict__ navs,
-                    double* __restrict__ svals) {
+                    const u64* __restrict__ bedge_p, Coords<3> X, const int32_t* __restrict__ bnd,
+                    bool pos_s, double* __restrict__ navs, double* __restrict__ svals) {
   const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const int4 g = seg[i];  // {e, j, k, p}
@@ -957,10 +947,13 @@ __global__ void __launch_bounds__(256)
   const d4 xj = X[g.y], xk = X[g.z];
   double n[3] = {navs[3 * e], navs[3 * e + 1], navs[3 * e + 2]};  // already scaled
   for (u32 q = q0; q < q1; ++q) {
-    const double* t = terms + 3 * static_cast<i64>(bedge_p[q] & 0xffffffffu);
-    n[0] += t[0];
-    n[1] += t[1];
-    n[2] += t[2];
+    const i64 f = static_cast<i64>(bedge_p[q] & 0xffffffffu);
+    constexpr double fb = 1.0 / 12.0;
+    double b0, b1, b2;
+    bnormal3(X, bnd + 3 * f, b0, b1, b2);
+    n[0] += fb * b0;
+    n[1] += fb * b1;
+    n[2] += fb * b2;
   }
   double s = (xk.x - xj.x) * n[0] + (xk.y - xj.y) * n[1];
   s = s + (xk.z - xj.z) * n[2];
@@ -1083,11 +1076,8 @@ int launch_navs(dm_ctx* c, int variant) {
     tmark(c, 1);
     if constexpr (D == 3 && ALGO == kDualFree) {
       if (c->n_bedge > 0) {
-        DM_CK(c, c->bterms.ensure(static_cast<size_t>(3 * c->nB)));
-        DM_LAUNCH(c, k_facet_terms, grid_for(c->nB, 256), 256, 0, X, c->bnd.p, c->nB,
-                  c->bterms.p);
         DM_LAUNCH(c, k_ring_boundary, grid_for(c->n_bseg, 256), 256, 0, c->bseg.p,
-                  c->bseg_start.p, c->n_bseg, c->bedge_p.p, X, c->bterms.p, c->vol_by_rank,
+                  c->bseg_start.p, c->n_bseg, c->bedge_p.p, X, c->bnd.p, c->vol_by_rank,
                   c->navs.p, c->svals.p);
       }
     }
