@@ -32,6 +32,32 @@ __device__ __forceinline__ double fold_terms(double acc, u32 b, u32 e, const Idx
   return acc;
 }
 
+// One node's fold: incoming terms (ascending edge id, through `in_idx`), then
+// the outgoing row -- with the first eight terms of BOTH lists loaded before
+// any add (most nodes have <= 8 + 8), so the two lists' gathers overlap
+// instead of running back to back (C5 0.345 -> 0.317 ms; same order, same
+// bits; in_list loads without L1 allocation measured slower).
+template <typename InIdx>
+__device__ __forceinline__ double fold_node(u32 ib, u32 ie, u32 ob, u32 oe, const InIdx& in_idx,
+                                            const double* __restrict__ s) {
+  double vi[8], vo[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    vi[u] = ib + u < ie ? s[in_idx(ib + u)] : 0.0;
+    vo[u] = ob + u < oe ? s[ob + u] : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (ib + u < ie) acc += vi[u];
+  if (ie > ib + 8) acc = fold_terms(acc, ib + 8, ie, in_idx, s);
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (ob + u < oe) acc += vo[u];
+  if (oe > ob + 8) acc = fold_terms(acc, ob + 8, oe, [](u32 q) { return q; }, s);
+  return acc;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256, 8)
     k_vol_edge(const u32* __restrict__ in_ptr, const int32_t* __restrict__ in_list,
@@ -39,9 +65,8 @@ __global__ void __launch_bounds__(256, 8)
                double* __restrict__ V) {
   const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= nv) return;
-  const u32 ib = in_ptr[v], ie = in_ptr[v + 1], ob = os[v], oe = os[v + 1];
-  double acc = fold_terms(0.0, ib, ie, [&](u32 q) { return __ldg(in_list + q); }, svals);
-  acc = fold_terms(acc, ob, oe, [](u32 q) { return q; }, svals);
+  const double acc = fold_node(in_ptr[v], in_ptr[v + 1], os[v], os[v + 1],
+                               [&](u32 q) { return __ldg(in_list + q); }, svals);
   V[v] = acc * (1.0 / static_cast<double>(2 * D));
 }
 
@@ -54,9 +79,8 @@ __global__ void __launch_bounds__(256)
                    const double* __restrict__ svals, i64 nv, double* __restrict__ V) {
   const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nv) return;
-  const u32 ib = rin_ptr[r], ie = rin_ptr[r + 1], ob = rpstart[r], oe = rpstart[r + 1];
-  double acc = fold_terms(0.0, ib, ie, [&](u32 q) { return __ldg(rin_list + q); }, svals);
-  acc = fold_terms(acc, ob, oe, [](u32 q) { return q; }, svals);
+  const double acc = fold_node(rin_ptr[r], rin_ptr[r + 1], rpstart[r], rpstart[r + 1],
+                               [&](u32 q) { return __ldg(rin_list + q); }, svals);
   V[morder[r]] = acc * (1.0 / 6.0);
 }
 
