@@ -583,14 +583,17 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
   acc[2] = a2;
 }
 
-// OPT (valid results, all bitwise identical): 1 the (x, y) table and code
-// fill bypasses L1 (cp.async.cg: nothing a tile fills is re-read through
-// this SM's L1; C5 2.22 -> 2.17 ms), 2 streaming (evict-first) navs / s
-// stores (no change), 4 node ids / edge ids / metadata loaded with
-// L1::no_allocate (2.17 -> 2.19 ms), 16 mbarrier pipeline instead of the
-// tile barrier (NB = 3 only: 2.035 -> 2.015 ms), 32 the table fill walks the
-// tile's rank-ordered fill list (coloured 256-node plans only).  NB = 3 buffers drop the
-// end-of-tile barrier (PipeSmem): C5 2.17 -> 2.035 ms.  All bitwise unchanged.
+// OPT bits (all give the same bits; C5 element-loop times):
+//   1  the (x, y) table and code fill bypasses L1 (cp.async.cg: nothing a
+//      tile fills is re-read through this SM's L1): 2.22 -> 2.17 ms
+//   2  streaming (evict-first) navs / s stores: no change
+//   4  node ids / edge ids / metadata loaded with L1::no_allocate: 2.19 ms
+//   16 mbarrier full / empty pipeline instead of the tile barrier (NB = 3
+//      only): 2.035 -> 2.015 ms
+//   32 the table fill walks the tile's rank-ordered fill list (coloured
+//      256-node plans only): 2.015 -> 1.99 ms
+// NB = 3 buffers drop the end-of-tile barrier (PipeSmem): 2.17 -> 2.035 ms.
+// The default launch is OPT = 49 (1 | 16 | 32), NB = 3.
 template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
           int OPT = 1, int NB = 2, int CCAP = (NB == 2 ? kPipeCodeCap : 2048)>
 __global__ void __launch_bounds__(kEB, MINB)
@@ -650,10 +653,11 @@ __global__ void __launch_bounds__(kEB, MINB)
     if (!MB) cp_async_commit();
     const int4 m = m_cur;
     const int e = e_cur;
-    // m.w (the tile's boundary slice start) is not read by this kernel; keep
-    // its register live until here so the allocator cannot reuse it while
-    // the 16-byte metadata prefetch is still in flight (a write-after-write
-    // wait on the prefetch every tile; without this use ptxas also spills)
+    // m.w (the tile's boundary slice start) is not read by this kernel.  This
+    // use keeps the register allocation that fits 64 registers without
+    // spills; ptxas still reuses the dead w lane of the 16-byte prefetch
+    // while it is in flight, a wait the other warps hide (every way around
+    // it measured slower, profiles/r1_ncu_summary.md)
     asm volatile("" ::"r"(m.w));
     m_cur = m_nxt;
     e_cur = e_nxt;
