@@ -147,7 +147,7 @@ int dm_set_mesh(dm_ctx* c, int dim, const double* coords, int64_t n_nodes, const
   if (n_boundary)
     DM_CK(c, cudaMemcpyAsync(c->bnd.p, boundary, sizeof(int32_t) * dim * n_boundary,
                              cudaMemcpyHostToDevice, c->stream));
-  int st = pad_coords(c);
+  int st = coords_changed(c);
   if (st) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
@@ -159,7 +159,7 @@ int dm_set_coords(dm_ctx* c, const double* coords) {
   DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * c->dim * c->nv,
                            cudaMemcpyHostToDevice, c->stream));
   c->have_navs = c->have_vols = false;
-  return pad_coords(c);
+  return coords_changed(c);
 }
 
 int dm_set_coords_device(dm_ctx* c, const double* d_coords) {
@@ -168,7 +168,7 @@ int dm_set_coords_device(dm_ctx* c, const double* d_coords) {
   DM_CK(c, cudaMemcpyAsync(c->coords.p, d_coords, sizeof(double) * c->dim * c->nv,
                            cudaMemcpyDeviceToDevice, c->stream));
   c->have_navs = c->have_vols = false;
-  return pad_coords(c);
+  return coords_changed(c);
 }
 
 int dm_build_edges(dm_ctx* c, int64_t* n_edges) {
@@ -304,7 +304,7 @@ int dm_metrics_host_async(dm_ctx* c, const double* coords, int nav_algo, int var
     DM_CK(c, cudaEventRecord(c->ev_h2d, c->s_h2d));
     DM_CK(c, cudaStreamWaitEvent(c->stream, c->ev_h2d, 0));
     c->have_navs = c->have_vols = false;
-    st = pad_coords(c);
+    st = coords_changed(c);
     if (st) return st;
   }
   // this step writes the other navs / vols buffer once its last copy-out ended

@@ -249,7 +249,7 @@ extern "C" int dm_gen_tri_square(dm_ctx* c, int n, uint64_t diag_seed, double am
   DM_LAUNCH(c, k_gen_tri, grid_for((m + 1) * (m + 1), 256), 256, 0, n, diag_seed, amp, seed,
             c->coords.p, c->elems.p);
   DM_LAUNCH(c, k_gen_tri_bnd, grid_for(4 * m, 256), 256, 0, n, c->bnd.p);
-  st = pad_coords(c);
+  st = coords_changed(c);
   if (st) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
@@ -300,7 +300,7 @@ extern "C" int dm_gen_tet_box(dm_ctx* c, int nx, int ny, int nz, const double* z
   }
   DM_LAUNCH(c, k_gen_tet_bnd, grid_for(nB, 256), 256, 0, nx, ny, F, c->bnd.p);
   if (z_nodes) DM_CK(c, cudaStreamSynchronize(c->stream));  // zd dies here
-  st = pad_coords(c);
+  st = coords_changed(c);
   if (st) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
@@ -343,7 +343,7 @@ extern "C" int dm_gen_permute(dm_ctx* c, uint64_t node_seed, uint64_t elem_seed)
       false;
   c->have_navs = c->have_vols = false;
   c->ne = c->n_bedge = c->n_derived = 0;
-  return pad_coords(c);
+  return coords_changed(c);
 }
 
 extern "C" int dm_get_mesh(dm_ctx* c, double* coords, int32_t* elements, int32_t* boundary) {

@@ -161,7 +161,8 @@ struct dm_ctx {
   int dim = 0;
   dm::i64 nv = 0, nE = 0, nB = 0;
   dm::DevBuf<double> coords;  // caller layout, dim doubles per node
-  dm::DevBuf<dm::d4> x4;      // 3D padded copy
+  dm::DevBuf<dm::d4> x4;      // 3D padded copy (lazy: built from coords on demand)
+  bool x4_fresh = false;      // x4 matches coords
   dm::DevBuf<int32_t> elems, bnd;
 
   // edge structures (K1)
@@ -452,7 +453,15 @@ int ensure_rings(dm_ctx* c);
 int build_edges_impl(dm_ctx* c);
 int navs_impl(dm_ctx* c, int algo, int variant);
 int volumes_impl(dm_ctx* c, int algo);
-int pad_coords(dm_ctx* c);
+// Coordinate-derived layouts.  coords_changed marks them stale (set-time
+// entry points); pad_x4 rebuilds the padded copy; ensure_x4 rebuilds it only
+// if stale (plan building, verification); refresh_ring_coords rebuilds the
+// ring path's Morton-order copy from the raw coordinates.  Every metrics
+// call rebuilds the layout its kernels read from the raw coordinates
+// (navs_impl), so a timed step consumes the caller's coordinate array.
+int coords_changed(dm_ctx* c);
+int pad_x4(dm_ctx* c);
+int ensure_x4(dm_ctx* c);
 int refresh_ring_coords(dm_ctx* c);
 int compute_element_volumes(dm_ctx* c);
 int svals_from_navs(dm_ctx* c);

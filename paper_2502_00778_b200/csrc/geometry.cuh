@@ -21,6 +21,20 @@ struct Coords<3> {
   __device__ __forceinline__ d4 operator[](int v) const { return ld_d4(p + v); }
   __device__ __forceinline__ d4 xyz(int v) const { return ld_d3(p + v); }
 };
+// Raw 3D coordinates (the caller's x, y, z per node, 24-byte records): read by
+// the kernels of the default step, which take no coordinate copy
+struct Coords3R {
+  const double* __restrict__ p;
+  __device__ __forceinline__ d4 operator[](int v) const {
+    const double* q = p + 3 * static_cast<i64>(v);
+    d4 r;
+    r.x = __ldg(q);
+    r.y = __ldg(q + 1);
+    r.z = __ldg(q + 2);
+    r.w = 0.0;
+    return r;
+  }
+};
 template <>
 struct Coords<2> {
   const double2* __restrict__ p;
@@ -115,8 +129,9 @@ __device__ __forceinline__ void tr2(const Coords<2>& X, int v0, int v1, int v2, 
 }
 
 // Boundary directed area n_B (ref mesh.cpp:113-127).
-__device__ __forceinline__ void bnormal3(const Coords<3>& X, const int32_t* bl, double& n0,
-                                         double& n1, double& n2) {
+template <typename CX>
+__device__ __forceinline__ void bnormal3(const CX& X, const int32_t* bl, double& n0, double& n1,
+                                         double& n2) {
   const d4 j = X[__ldg(bl)], r = X[__ldg(bl + 1)], l = X[__ldg(bl + 2)];
   double c0, c1, c2;
   cross3(r.x - j.x, r.y - j.y, r.z - j.z, l.x - j.x, l.y - j.y, l.z - j.z, c0, c1, c2);
@@ -132,7 +147,8 @@ __device__ __forceinline__ void bnormal2(const Coords<2>& X, const int32_t* bl, 
 }
 
 // Signed element volume (ref mesh.cpp:75-92): 2D 0.5*cross, 3D (uxv).w / 6.0.
-__device__ __forceinline__ double evol3(const Coords<3>& X, int v0, int v1, int v2, int v3) {
+template <typename CX>
+__device__ __forceinline__ double evol3(const CX& X, int v0, int v1, int v2, int v3) {
   const d4 a = X[v0], b = X[v1], c = X[v2], d = X[v3];
   double uv0, uv1, uv2;
   cross3(b.x - a.x, b.y - a.y, b.z - a.z, c.x - a.x, c.y - a.y, c.z - a.z, uv0, uv1, uv2);

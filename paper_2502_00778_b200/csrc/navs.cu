@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(kEB)
 // separate per-facet pass measured 0.0025 ms slower at C5 for the same bits).
 __global__ void __launch_bounds__(256)
     k_ring_boundary(const int4* __restrict__ seg, const u32* __restrict__ start, i64 ns,
-                    const u64* __restrict__ bedge_p, Coords<3> X, const int32_t* __restrict__ bnd,
+                    const u64* __restrict__ bedge_p, Coords3R X, const int32_t* __restrict__ bnd,
                     bool pos_s, double* __restrict__ navs, double* __restrict__ svals) {
   const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= ns) return;
@@ -1081,8 +1081,8 @@ int launch_navs(dm_ctx* c, int variant) {
     if constexpr (D == 3 && ALGO == kDualFree) {
       if (c->n_bedge > 0) {
         DM_LAUNCH(c, k_ring_boundary, grid_for(c->n_bseg, 256), 256, 0, c->bseg.p,
-                  c->bseg_start.p, c->n_bseg, c->bedge_p.p, X, c->bnd.p, c->vol_by_rank,
-                  c->navs.p, c->svals.p);
+                  c->bseg_start.p, c->n_bseg, c->bedge_p.p, Coords3R{c->coords.p}, c->bnd.p,
+                  c->vol_by_rank, c->navs.p, c->svals.p);
       }
     }
     tmark(c, 2);
@@ -1126,6 +1126,7 @@ int launch_navs(dm_ctx* c, int variant) {
 }  // namespace
 
 int svals_from_navs(dm_ctx* c) {
+  if (int sx = ensure_x4(c)) return sx;
   if (c->dim == 3) {
     DM_LAUNCH(c, k_svals<3>, grid_for(c->ne, 256), 256, 0, c->edges.p, coords_of<3>(c), c->ne,
               c->navs.p, c->svals.p);
@@ -1157,6 +1158,11 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
   DM_CK(c, c->navs.ensure(static_cast<size_t>(c->dim * c->ne)));
   DM_CK(c, c->svals.ensure(static_cast<size_t>(c->ne)));
   if (c->dim == 3) {
+    // every call reads the caller's coordinates: the ring walk's table source
+    // (Morton-order copy) or the padded copy of the other kernels is rebuilt
+    // here, inside the metrics step, never carried over from an earlier call
+    st = variant == DM_VARIANT_GATHER && c->ring_ok ? refresh_ring_coords(c) : pad_x4(c);
+    if (st) return st;
     st = algo == DM_NAV_DUALFREE ? launch_navs<3, kDualFree>(c, variant)
                                  : launch_navs<3, kTraditional>(c, variant);
   } else {

@@ -706,13 +706,14 @@ __global__ void k_bmark(const u64* __restrict__ bedge, i64 n, uint8_t* __restric
   if (q < n) mark[bedge[q] >> 32] = 1;
 }
 
-__global__ void k_morton_coords(const d4* __restrict__ x4, const int32_t* __restrict__ order,
+// Morton-order copy of the raw coordinates (x, y | z per rank r, node order[r])
+__global__ void k_morton_coords(const double* __restrict__ xc, const int32_t* __restrict__ order,
                                 i64 nv, double2* __restrict__ xy, double* __restrict__ z) {
   const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= nv) return;
-  const d4 p = x4[order[r]];
-  xy[r] = make_double2(p.x, p.y);
-  z[r] = p.z;
+  const double* p = xc + 3 * static_cast<i64>(__ldg(order + r));
+  xy[r] = make_double2(__ldg(p), __ldg(p + 1));
+  z[r] = __ldg(p + 2);
 }
 
 // Host phase timer of the plan (env DUALMESH_PLAN_TIMING=1): synchronises the
@@ -929,6 +930,7 @@ int ensure_rings(dm_ctx* c) {
   const i64 ne = c->ne;
   const i64 ntiles = (ne + kTileEdges - 1) / kTileEdges;
   const i64 nwarps = (ne + 31) / 32;
+  if (int sx = ensure_x4(c)) return sx;  // the plan's Morton keys read the padded copy
   if (ne == 0 || !c->x4.p) {
     c->ring_ok = false;
     c->have_rings = true;
@@ -1023,17 +1025,15 @@ int ensure_rings(dm_ctx* c) {
   c->ring_ok = (fl[0] == 0);
   c->have_rings = true;
   clk.mark("colouring");
-  const int st2 = c->ring_ok ? refresh_ring_coords(c) : DM_OK;
-  clk.mark("coords");
-  return st2;
+  return DM_OK;  // the Morton-order coordinates are staged by every navs call
 }
 
 int refresh_ring_coords(dm_ctx* c) {
   const i64 nv = c->nv;
   DM_CK(c, c->mxy.ensure(nv));
   DM_CK(c, c->mz.ensure(nv));
-  DM_LAUNCH(c, k_morton_coords, grid_for(nv, 256), 256, 0, c->x4.p, c->morder.p, nv, c->mxy.p,
-            c->mz.p);
+  DM_LAUNCH(c, k_morton_coords, grid_for(nv, 256), 256, 0, c->coords.p, c->morder.p, nv,
+            c->mxy.p, c->mz.p);
   return DM_OK;
 }
 

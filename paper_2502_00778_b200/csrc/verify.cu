@@ -285,16 +285,21 @@ int device_sum(dm_ctx* c, const double* x, i64 n, double* out) {
 
 }  // namespace
 
-int pad_coords(dm_ctx* c) {
+int coords_changed(dm_ctx* c) {
+  c->x4_fresh = false;
+  return DM_OK;
+}
+int pad_x4(dm_ctx* c) {
   if (c->dim != 3) return DM_OK;
   DM_CK(c, c->x4.ensure(static_cast<size_t>(c->nv)));
   DM_LAUNCH(c, k_pad3, grid_for(c->nv, 256), 256, 0, c->coords.p, c->nv, c->x4.p);
-  // the ring path's Morton-ordered copy follows every coordinate update
-  if (c->have_rings && c->ring_ok) return refresh_ring_coords(c);
+  c->x4_fresh = true;
   return DM_OK;
 }
+int ensure_x4(dm_ctx* c) { return c->x4_fresh ? DM_OK : pad_x4(c); }
 
 int face_stats(dm_ctx* c, double* max_face, double* max_vol) {
+  if (int st = ensure_x4(c)) return st;
   DM_CK(c, c->redu.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->redu.p, 0, 4 * sizeof(u64), c->stream));
   if (c->dim == 3) {
@@ -321,6 +326,7 @@ extern "C" int dm_check_closure(dm_ctx* c, double* residual, double* interior_re
   if (!c || !residual) return DM_ERR_INVALID_ARG;
   if (!c->have_navs) return fail(c, DM_ERR_STATE, "closure check needs navs");
   int st = ensure_incoming(c);
+  if (!st) st = ensure_x4(c);
   if (st) return st;
   const i64 nv = c->nv;
   DevBuf<uint8_t> mask;
@@ -377,6 +383,7 @@ extern "C" int dm_check_linear_exactness(dm_ctx* c, const double* A, const doubl
   if (!F.zero && !c->have_vols) return fail(c, DM_ERR_STATE, "exactness check needs volumes");
   int st = ensure_incoming(c);
   if (st) return st;
+  if (int sx = ensure_x4(c)) return sx;
   const i64 nv = c->nv, ne = c->ne;
   DevBuf<uint8_t> mask;
   DevBuf<double> phi;

@@ -84,9 +84,9 @@ __global__ void __launch_bounds__(256)
   V[morder[r]] = acc * (1.0 / 6.0);
 }
 
-template <int D>
+template <int D, typename CX>
 __global__ void __launch_bounds__(256)
-    k_elem_vol(const int32_t* __restrict__ el, Coords<D> X, i64 nE, double* __restrict__ ve) {
+    k_elem_vol(const int32_t* __restrict__ el, CX X, i64 nE, double* __restrict__ ve) {
   const i64 E = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (E >= nE) return;
   if constexpr (D == 3) {
@@ -112,12 +112,14 @@ __global__ void __launch_bounds__(256, 8)
 
 int compute_element_volumes(dm_ctx* c) {
   DM_CK(c, c->velem.ensure(static_cast<size_t>(c->nE)));
-  if (c->dim == 3) {
-    Coords<3> X{c->x4.p};
-    DM_LAUNCH(c, k_elem_vol<3>, grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE, c->velem.p);
+  if (c->dim == 3) {  // raw coordinates: no copy carried between calls
+    Coords3R X{c->coords.p};
+    DM_LAUNCH(c, (k_elem_vol<3, Coords3R>), grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE,
+              c->velem.p);
   } else {
     Coords<2> X{reinterpret_cast<const double2*>(c->coords.p)};
-    DM_LAUNCH(c, k_elem_vol<2>, grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE, c->velem.p);
+    DM_LAUNCH(c, (k_elem_vol<2, Coords<2>>), grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE,
+              c->velem.p);
   }
   return DM_OK;
 }
