@@ -334,26 +334,6 @@ __device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
-// read-only loads that do not allocate in L1 (streamed once per tile)
-__device__ __forceinline__ int ld_na(const int* p) {
-  int v;
-  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ int4 ld_na4(const int4* p) {
-  int4 v;
-  asm("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
-      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-      : "l"(p));
-  return v;
-}
-// streaming (evict-first) stores of output rows that are not re-read soon
-__device__ __forceinline__ void st_cs(double* p, double v) {
-  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-__device__ __forceinline__ void st_cs2(double* p, double a, double b) {
-  asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(a), "d"(b) : "memory");
-}
 // mbarrier helpers (shared::cta): per-buffer full / empty phases of the ring
 // kernel's tile pipeline
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {

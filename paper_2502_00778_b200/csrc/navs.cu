@@ -195,19 +195,8 @@ __device__ __forceinline__ void store_navs_warp(const double* n, i64 wbase, i64 
 // Per-lane store of one 3D navs row (24 bytes at 24e): one 16-byte and one
 // 8-byte store, ordered by the row's 16-byte alignment (e even: xy | z,
 // e odd: x | yz).
-template <bool CS = false>
 __device__ __forceinline__ void store_nav_row(double* __restrict__ navs, i64 e, const double* n) {
   double* r = navs + 3 * e;
-  if constexpr (CS) {
-    if ((e & 1) == 0) {
-      st_cs2(r, n[0], n[1]);
-      st_cs(r + 2, n[2]);
-    } else {
-      st_cs(r, n[0]);
-      st_cs2(r + 1, n[1], n[2]);
-    }
-    return;
-  }
   if ((e & 1) == 0) {
     *reinterpret_cast<double2*>(r) = make_double2(n[0], n[1]);
     r[2] = n[2];
@@ -440,7 +429,7 @@ __device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m
 // node ids and this thread's edge id of `tile` into registers (always the
 // full CAP window: the tile list has a fixed stride, so no dependency on the
 // tile's metadata).
-template <int NI, bool NA = false, bool SF = false>
+template <int NI, bool SF = false>
 __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __restrict__ tnodes,
                                          const int32_t* __restrict__ eperm, i64 ne,
                                          int (&ids)[NI], int (&sl)[NI], int& eid) {
@@ -452,11 +441,10 @@ __device__ __forceinline__ void pipe_ids(int tile, int ntiles, const int32_t* __
       sl[0] = __ldg(reinterpret_cast<const uint8_t*>(tn + kTileFillSlots) + threadIdx.x);
     } else {
 #pragma unroll
-      for (int u = 0; u < NI; ++u)
-        ids[u] = NA ? ld_na(tn + threadIdx.x + u * kEB) : __ldg(tn + threadIdx.x + u * kEB);
+      for (int u = 0; u < NI; ++u) ids[u] = __ldg(tn + threadIdx.x + u * kEB);
     }
     const i64 p = static_cast<i64>(tile) * kEB + threadIdx.x;
-    eid = p < ne ? (NA ? ld_na(eperm + p) : __ldg(eperm + p)) : 0;
+    eid = p < ne ? __ldg(eperm + p) : 0;
   }
 }
 
@@ -586,8 +574,7 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W
 // OPT bits (all give the same bits; C5 element-loop times):
 //   1  the (x, y) table and code fill bypasses L1 (cp.async.cg: nothing a
 //      tile fills is re-read through this SM's L1): 2.22 -> 2.17 ms
-//   2  streaming (evict-first) navs / s stores: no change
-//   4  node ids / edge ids / metadata loaded with L1::no_allocate: 2.19 ms
+// (streaming stores and L1::no_allocate id loads were measured and dropped)
 //   16 mbarrier full / empty pipeline instead of the tile barrier (NB = 3
 //      only): 2.035 -> 2.015 ms
 //   32 the table fill walks the tile's rank-ordered fill list (coloured
@@ -628,13 +615,13 @@ __global__ void __launch_bounds__(kEB, MINB)
   int ids[CAP / kEB], sl[CAP / kEB];
   int e_nxt = 0;
   int4 m_cur = __ldg(meta + 2 * tile);
-  pipe_ids<CAP / kEB, (OPT & 4) != 0, (OPT & 32) != 0>(tile, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
+  pipe_ids<CAP / kEB, (OPT & 32) != 0>(tile, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
   int e_cur = e_nxt;
   pipe_issue<CAP, true, OPT>(S, 0, tile, m_cur, ids, sl, mxy, mz, rcodes, meta);
   if (MB) cp_async_mbar_arrive(&S.full[0]);
   else cp_async_commit();
   int4 m_nxt = tile + G < ntiles ? __ldg(meta + 2 * (tile + G)) : make_int4(0, 0, 0, 0);
-  pipe_ids<CAP / kEB, (OPT & 4) != 0, (OPT & 32) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
+  pipe_ids<CAP / kEB, (OPT & 32) != 0>(tile + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
   for (int it = 0; tile < ntiles; ++it, tile += G) {
     const int b = NB == 2 ? (it & 1) : it % NB;
     const int bn = NB == 2 ? (b ^ 1) : (b + 1 == NB ? 0 : b + 1);
@@ -661,9 +648,8 @@ __global__ void __launch_bounds__(kEB, MINB)
     asm volatile("" ::"r"(m.w));
     m_cur = m_nxt;
     e_cur = e_nxt;
-    m_nxt = nxt + G < ntiles ? ((OPT & 4) ? ld_na4(meta + 2 * (nxt + G)) : __ldg(meta + 2 * (nxt + G)))
-                             : make_int4(0, 0, 0, 0);
-    pipe_ids<CAP / kEB, (OPT & 4) != 0, (OPT & 32) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
+    m_nxt = nxt + G < ntiles ? __ldg(meta + 2 * (nxt + G)) : make_int4(0, 0, 0, 0);
+    pipe_ids<CAP / kEB, (OPT & 32) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
     if (MB) {
       mbar_wait(&S.full[b], static_cast<unsigned>(it / 3) & 1u);
     } else {
@@ -734,8 +720,7 @@ __global__ void __launch_bounds__(kEB, MINB)
       edge_tail_values<3, ALGO>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
       if (!(FAKE & 34) || s == -12345.0) {
         double* sp = svals + (pos_s ? p : static_cast<i64>(e));  // rings.cu: vol_by_rank
-        if (OPT & 2) st_cs(sp, s);
-        else *sp = s;
+        *sp = s;
       }
     }
     if (FAKE & 32) {  // probe: one 32-byte (x, y, z, s) row per edge
@@ -756,7 +741,7 @@ __global__ void __launch_bounds__(kEB, MINB)
         navs[2 * ne + e] = nv[2];
       }
     } else if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) {
-      store_nav_row<(OPT & 2) != 0>(navs, e, nv);
+      store_nav_row(navs, e, nv);
     }
     if (NB == 2) __syncthreads();  // buffer b is refilled next iteration
     if (MB) {
@@ -1052,12 +1037,12 @@ int launch_navs(dm_ctx* c, int variant) {
           case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          // A/B configurations of this round's pipeline (same bits): 30 the
+          // round's starting point (2 buffers, .ca fill), 36 + cp.async.cg,
+          // 37 + three buffers, 38 + mbarriers (all but the fill list)
           case 30: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 0>, sizeof(PipeSmem<256>)); break;
-          case 31: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1>, sizeof(PipeSmem<256>)); break;
           case 36: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 2>, sizeof(PipeSmem<256>)); break;
           case 37: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 33: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 3>, sizeof(PipeSmem<256>)); break;
-          case 35: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 5>, sizeof(PipeSmem<256>)); break;
           case 38: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           // tests: a 16-code shared buffer sends every tile down the
           // global-memory path of the same kernel
