@@ -163,20 +163,47 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def cpu_sample(steps, warmup, n=64, threads=None):
-    """CPU restatement of the path (oracle/oracle.c, or_metrics_mt: dual-free
-    navs + edge-based volumes, per-edge / per-node gathers in the serial
-    loops' summation order, bitwise equal to them) on a bounded sample of the
-    same grid family, all host threads; edge list and incidence lists
-    prebuilt (topology, like the GPU plan)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_rows(config, scale, steps, warmup, serial_reps, trad_reps, threads=None):
+    """The reference CPU path on the bench's own workload (SPEC time_algorithms,
+    SPEC.md:382-390,414): the oracle (oracle/oracle.c, CPU restatement of the
+    reference algorithm, test infrastructure) on the same grid as the GPU arm,
+    generated by the oracle's own generator (bitwise the GPU arm's grid,
+    tests/test_oracle.py).  Edge list, incidence and boundary lists are built
+    outside the timed regions, like the GPU plan.
+
+    rows: or_metrics_mt (dual-free navs + edge volumes, all host threads, the
+    serial loops' summation order -> same bits) over `steps` steps after
+    `warmup`; serial dual-free step (or_navs_dualfree + or_volumes_edge, one
+    thread) warm-up + `serial_reps`; serial traditional navs
+    (or_navs_traditional) warm-up + `trad_reps` (0 skips it)."""
     from oracle.oracle import Oracle
-    from paper_2502_00778_b200 import meshgen
+    if config != "C5":
+        raise ValueError("the CPU legs time the C5 family (oracle generator)")
     threads = threads or host_threads()
     O = Oracle()
-    m = meshgen.tet_cube(n, amp=0.15)
+    n = 256 // scale
+    t0 = time.perf_counter()
+    m = O.gen_tet_cube(n, amp=0.15, seed=42)
+    t1 = time.perf_counter()
     e, o = O.build_edges(m)
+    t2 = time.perf_counter()
     plan = O.plan(m, e, o)
+    t3 = time.perf_counter()
     out = (np.empty(3 * e.shape[0]), np.empty(e.shape[0]), np.empty(m.num_nodes()))
+    rows = {"grid": f"{n}^3 Kuhn cube, +-0.15h (seed 42), {m.num_elements()} tets, "
+                    f"{e.shape[0]} edges", "n_elements": m.num_elements(),
+            "host_cpu": cpu_model(), "host_threads": threads,
+            "setup_s": {"gen": t1 - t0, "build_edges": t2 - t1, "plan": t3 - t2}}
     try:
         for _ in range(warmup):
             O.metrics_mt(plan, m.coords, threads, out)
@@ -186,29 +213,70 @@ def cpu_sample(steps, warmup, n=64, threads=None):
         dt = (time.perf_counter() - t0) / steps
     finally:
         O.plan_free(plan)
-    return m.num_elements() / dt, dt, m, threads
+    rows["mt_step_ms"] = dt * 1e3
+    rows["mt_tets_per_s"] = m.num_elements() / dt
+    if serial_reps > 0 or trad_reps > 0:
+        t0 = time.perf_counter()
+        e2l, _, _ = O.edge_maps(m, e, o)
+        rows["setup_s"]["edge_maps"] = time.perf_counter() - t0
+
+        def best(fn, reps):
+            fn()  # warm-up
+            ts = []
+            for _ in range(reps):
+                a = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - a)
+            return min(ts) * 1e3, float(np.mean(ts)) * 1e3
+
+        if serial_reps > 0:
+            nv = O.navs_dualfree(m, e, o, e2l)
+            rows["serial_dualfree_navs_ms"], _ = best(lambda: O.navs_dualfree(m, e, o, e2l),
+                                                     serial_reps)
+            rows["serial_edge_volumes_ms"], _ = best(lambda: O.volumes_edge(m, e, nv), serial_reps)
+            st = rows["serial_dualfree_navs_ms"] + rows["serial_edge_volumes_ms"]
+            rows["serial_step_ms"] = st
+            rows["serial_tets_per_s"] = m.num_elements() / (st / 1e3)
+            rows["serial_reps"] = serial_reps
+        if trad_reps > 0:
+            rows["serial_traditional_navs_ms"], _ = best(
+                lambda: O.navs_traditional(m, e, o, e2l), trad_reps)
+            rows["trad_reps"] = trad_reps
+            if "serial_dualfree_navs_ms" in rows:
+                rows["cpu_traditional_over_dualfree_navs"] = (
+                    rows["serial_traditional_navs_ms"] / rows["serial_dualfree_navs_ms"])
+                rows["paper_traditional_over_dualfree_navs"] = 2.16
+    return rows
 
 
 def run_reference(args, world, rank, dist):
     if rank != 0:
         return
     steps, warmup = args.steps, args.warmup
-    n = args.ref_n
-    value, dt, m, th = cpu_sample(steps, warmup, n=n)
+    rows = cpu_rows(args.config, args.scale, steps, warmup, args.serial_reps, args.trad_reps)
+    value, th = rows["mt_tets_per_s"], rows["host_threads"]
     sample = (f"oracle/oracle.c or_metrics_mt (CPU restatement of the reference algorithm, "
-              f"-O2 -ffp-contract=off, {th} threads) on a {n}^3 Kuhn cube "
-              f"({m.num_elements()} tets, the C5 grid family), dual-free navs + edge volumes, "
-              f"{steps} steps after {warmup} warm-up")
+              f"-O2 -ffp-contract=off, {th} threads, {rows['host_cpu']}) on the full "
+              f"{args.config} grid ({rows['grid']}), dual-free navs + edge volumes, "
+              f"{steps} steps after {warmup} warm-up; serial rows in cpu_rows")
     line = {"metric": METRIC, "value": value, "unit": "tets/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": steps, "warmup": warmup, "ms_per_step": dt * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "C5 family (256^3 Kuhn, +-0.15h); "
-                                            f"timed on a {n}^3 sample"},
+            "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+            "ms_per_step": rows["mt_step_ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, args.scale),
+                       "n_elements": rows["n_elements"]},
             "cpu_baseline": {"value": value, "unit": "tets/s", "cores": th, "kind": "port",
                              "sample": sample},
+            "cpu_rows": rows,
             "e2e": {"value": value, "unit": "tets/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_name(config, scale):
+    if config == "C5" and scale == 1:
+        return "C5: 256^3 Kuhn cube, +-0.15h jitter (seed 42)"
+    return f"{config}/scale {scale}"
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -326,14 +394,16 @@ def run_ours(args, world, rank, local, dist):
     for _ in range(max(1, args.warmup // 2)):
         eng.navs(TR, _lib.DM_VARIANT_GATHER)
     torch.cuda.synchronize()
-    t_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    t_ev[0].record(stream)
-    for _ in range(K):
+    t_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    for k in range(K):
+        t_ev[k][0].record(stream)
         eng.navs(TR, _lib.DM_VARIANT_GATHER)
+        t_ev[k][1].record(stream)
         eng.volumes(EDGE)
-    t_ev[1].record(stream)
+        t_ev[k][2].record(stream)
     torch.cuda.synchronize()
-    trad_ms = t_ev[0].elapsed_time(t_ev[1]) / K
+    trad_ms = float(np.mean([e[0].elapsed_time(e[2]) for e in t_ev]))
+    trad_navs_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in t_ev]))
 
     # e2e: the public C-ABI step with host buffers (pinned), H2D coords + D2H navs/volumes
     e2e = None
@@ -389,22 +459,31 @@ def run_ours(args, world, rank, local, dist):
             traffic = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cv, cdt, cm, th = cpu_sample(args.cpu_steps, 1, n=args.cpu_n)
-        cpu = {"value": cv, "unit": "tets/s", "cores": th, "kind": "port",
-               "sample": f"oracle/oracle.c or_metrics_mt ({th} threads) on a {args.cpu_n}^3 "
-                         f"Kuhn cube ({cm.num_elements()} tets, same +-0.15h family), "
-                         f"dual-free navs + edge volumes, {args.cpu_steps} steps, "
-                         f"{cdt * 1e3:.1f} ms/step"}
+    crow = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == "C5":
+        crow = cpu_rows(args.config, args.scale, args.cpu_steps, 1, args.serial_reps,
+                        args.trad_reps)
+        cpu = {"value": crow["mt_tets_per_s"], "unit": "tets/s", "cores": crow["host_threads"],
+               "kind": "port",
+               "sample": f"oracle/oracle.c or_metrics_mt ({crow['host_threads']} threads, "
+                         f"{crow['host_cpu']}) on the same full grid ({crow['grid']}), "
+                         f"dual-free navs + edge volumes, {args.cpu_steps} steps after 1 "
+                         f"warm-up, {crow['mt_step_ms']:.1f} ms/step; serial rows in "
+                         f"cpu_rows"}
+        if "serial_step_ms" in crow:
+            cpu["serial_1_thread"] = {"value": crow["serial_tets_per_s"], "unit": "tets/s",
+                                      "cores": 1, "ms_per_step": crow["serial_step_ms"]}
+            crow["gpu_step_over_serial_step"] = crow["serial_step_ms"] / ms_step
+        crow["gpu_step_over_mt_step"] = crow["mt_step_ms"] / ms_step
+        if "serial_traditional_navs_ms" in crow:
+            crow["gpu_traditional_over_dualfree_navs"] = trad_navs_ms / nav_ms
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: 256^3 Kuhn cube, +-0.15h jitter (seed 42)"
-                                   if args.config == "C5" and args.scale == 1 else
-                                   f"{args.config}/scale {args.scale}",
+            "config": {"workload": workload_name(args.config, args.scale),
                        "n_elements": mesh.num_elements(), "n_nodes": mesh.num_nodes(),
                        "n_edges": ne, "n_boundary": mesh.num_boundary(),
                        "nav_variant": args.variant,
@@ -423,6 +502,7 @@ def run_ours(args, world, rank, local, dist):
                               "kernels_ms": {"element_loop": elem_ms, "boundary": bnd_ms,
                                              "volumes": kvol_ms}},
             "cpu_baseline": cpu,
+            "cpu_rows": crow,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
@@ -431,7 +511,9 @@ def run_ours(args, world, rank, local, dist):
                       "plan": eng.plan_info(), "edges_bytes": B["edges"],
                       "edges_GBps": B["edges"] / (edges_ms / 1e3) / 1e9,
                       "traditional_ms_per_step": trad_ms,
+                      "traditional_navs_ms": trad_navs_ms, "dualfree_navs_ms": nav_ms,
                       "gpu_speedup_dualfree_over_traditional": trad_ms / ms_step,
+                      "gpu_traditional_over_dualfree_navs": trad_navs_ms / nav_ms,
                       "meshgen_s": gen_s},
         }
         print(json.dumps(line), flush=True)
@@ -447,9 +529,11 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--variant", choices=["gather", "scatter"], default="gather")
-    ap.add_argument("--cpu-n", type=int, default=96)
-    ap.add_argument("--cpu-steps", type=int, default=10)
-    ap.add_argument("--ref-n", type=int, default=128)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--serial-reps", type=int, default=3,
+                    help="serial CPU dual-free step: warm-up + this many reps (0 skips)")
+    ap.add_argument("--trad-reps", type=int, default=1,
+                    help="serial CPU traditional navs: warm-up + this many reps (0 skips)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -695,3 +695,86 @@ int or_metrics_mt(const or_plan* p, const double* x, int nthreads, double* navs,
   }
   return 0;
 }
+
+/* ---- input synthesis for the CPU legs ------------------ */
+/* gen_tet_cube(n) + perturb_interior(amp, seed): the oracle's own generator,
+ * so the bench's CPU arm never loads the product's meshgen library.  Node
+ * (i,j,k) -> i + (n+1)j + (n+1)^2 k; each hex is cut into the 6 Kuhn tets
+ * that share its v000-v111 diagonal (one per axis order), positively
+ * oriented; each boundary quad into 2 triangles along its lowest-highest
+ * corner diagonal, outward.  Jitter: splitmix64, three draws
+ * per interior node in node order, d = (2u - 1) amp h, u = (r >> 11) 2^-53.
+ * tests/test_oracle.py pins it against the product generator bit for bit. */
+static uint64_t sm64(uint64_t* s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static double sm64_jit(uint64_t* s, double amp, double h) {
+  const double u = (double)(sm64(s) >> 11) * (1.0 / 9007199254740992.0);
+  return (2.0 * u - 1.0) * amp * h;
+}
+
+int or_gen_tet_cube(int n, double amp, uint64_t seed, double* x, int32_t* el, int32_t* bnd) {
+  if (n < 1 || !x || !el || !bnd) return -1;
+  const int64_t w = n + 1, w2 = w * w;
+  const double h = 1.0 / n;
+  uint64_t st = seed;
+  for (int64_t k = 0; k <= n; ++k)
+    for (int64_t j = 0; j <= n; ++j)
+      for (int64_t i = 0; i <= n; ++i) {
+        double* p = x + 3 * (i + w * j + w2 * k);
+        const int64_t ijk[3] = {i, j, k};
+        for (int a = 0; a < 3; ++a) p[a] = ijk[a] == n ? 1.0 : (double)ijk[a] * h;
+        if (amp != 0.0 && i > 0 && i < n && j > 0 && j < n && k > 0 && k < n)
+          for (int a = 0; a < 3; ++a) p[a] += sm64_jit(&st, amp, h);
+      }
+  /* axis orders of the 6 Kuhn paths; the tet (v000, v000+e_a, v000+e_a+e_b,
+   * v111) is positive when (a, b, c) is an even permutation, else its last
+   * two nodes are swapped */
+  static const int ord[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+  static const int even[6] = {1, 0, 0, 1, 1, 0};
+  const int64_t step[3] = {1, w, w2};
+  int32_t* t = el;
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t v0 = i + w * j + w2 * k, v7 = v0 + 1 + w + w2;
+        for (int p = 0; p < 6; ++p) {
+          const int64_t v1 = v0 + step[ord[p][0]], v2 = v1 + step[ord[p][1]];
+          t[0] = (int32_t)v0;
+          t[1] = (int32_t)v1;
+          t[2] = (int32_t)(even[p] ? v2 : v7);
+          t[3] = (int32_t)(even[p] ? v7 : v2);
+          t += 4;
+        }
+      }
+  /* boundary: for each axis, low side then high side; the quad's in-plane
+   * axes u < v, corners c(du, dv); triangles (c00, c10, c11), (c00, c11, c01)
+   * as seen with the outward normal along +axis, reversed on the low side */
+  int32_t* b = bnd;
+  for (int ax = 0; ax < 3; ++ax) {
+    const int u = ax == 0 ? 1 : 0, v = ax == 2 ? 1 : 2;
+    /* (e_u x e_v) . e_ax > 0 for ax = 0, 2 and < 0 for ax = 1 */
+    const int uv_out = ax != 1;
+    for (int side = 0; side < 2; ++side) {
+      const int flip = (side == 1) != uv_out; /* reverse (c10 <-> c11 order) */
+      const int64_t base = side ? (int64_t)n * step[ax] : 0;
+      for (int64_t qv = 0; qv < n; ++qv)
+        for (int64_t qu = 0; qu < n; ++qu) {
+          const int64_t c00 = base + qu * step[u] + qv * step[v];
+          const int64_t c10 = c00 + step[u], c01 = c00 + step[v], c11 = c10 + step[v];
+          const int64_t tri[2][3] = {{c00, c10, c11}, {c00, c11, c01}};
+          for (int q = 0; q < 2; ++q) {
+            b[0] = (int32_t)tri[q][0];
+            b[1] = (int32_t)(flip ? tri[q][2] : tri[q][1]);
+            b[2] = (int32_t)(flip ? tri[q][1] : tri[q][2]);
+            b += 3;
+          }
+        }
+    }
+  }
+  return 0;
+}

@@ -89,6 +89,11 @@ void or_plan_free(or_plan* plan);
 int or_metrics_mt(const or_plan* plan, const double* x, int nthreads, double* navs, double* s,
                   double* volumes);
 
+/* Input synthesis: Kuhn cube n^3 x 6 tets, interior
+ * jitter amp*h per axis from splitmix64(seed).  x: 3(n+1)^3, el: 24 n^3,
+ * bnd: 36 n^2 entries. */
+int or_gen_tet_cube(int n, double amp, uint64_t seed, double* x, int32_t* el, int32_t* bnd);
+
 #ifdef __cplusplus
 }
 #endif

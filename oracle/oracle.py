@@ -31,6 +31,28 @@ def _p(a, t):
     return None if a is None else a.ctypes.data_as(C.POINTER(t))
 
 
+class SimpleMesh:
+    """Mesh arrays (same attribute surface as the product's Mesh)."""
+
+    def __init__(self, dim, coords, elements, boundary):
+        self.dim, self.coords, self.elements, self.boundary = dim, coords, elements, boundary
+
+    def num_nodes(self):
+        return self.coords.size // self.dim
+
+    def num_elements(self):
+        return self.elements.size // (self.dim + 1)
+
+    def num_boundary(self):
+        return self.boundary.size // self.dim
+
+    def element(self, e):
+        return self.elements[(self.dim + 1) * e:(self.dim + 1) * (e + 1)]
+
+    def boundary_element(self, b):
+        return self.boundary[self.dim * b:self.dim * (b + 1)]
+
+
 class Oracle:
     def __init__(self):
         if not os.path.exists(ORACLE_SO):
@@ -60,11 +82,24 @@ class Oracle:
             "or_plan_create": (P, [C.c_int, i64, I32P, i64, I32P, i64, I32P, U64P, i64]),
             "or_plan_free": (None, [P]),
             "or_metrics_mt": (C.c_int, [P, DP, C.c_int, DP, DP, DP]),
+            "or_gen_tet_cube": (C.c_int, [C.c_int, C.c_double, C.c_uint64, DP, I32P, I32P]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
             f.restype, f.argtypes = r, a
         self.L = L
+
+    # input synthesis ---------------------------------------------------------
+    def gen_tet_cube(self, n, amp=0.15, seed=42):
+        """SPEC gen_tet_cube + perturb_interior (oracle-owned; equals the
+        product generator bit for bit, tests/test_oracle.py)."""
+        x = np.empty(3 * (n + 1) ** 3, np.float64)
+        el = np.empty(24 * n ** 3, np.int32)
+        bd = np.empty(36 * n * n, np.int32)
+        if self.L.or_gen_tet_cube(n, amp, seed, _p(x, C.c_double), _p(el, C.c_int32),
+                                  _p(bd, C.c_int32)):
+            raise ValueError("or_gen_tet_cube")
+        return SimpleMesh(3, x, el, bd)
 
     # edges -----------------------------------------------------------------
     def build_edges(self, mesh):

@@ -297,7 +297,10 @@ int dm_metrics_host_async(dm_ctx* c, const double* coords, int nav_algo, int var
   }
   int st = DM_OK;
   if (coords) {
-    // the previous step's kernels read the resident coordinates
+    // every kernel or copy already queued on the compute stream (earlier
+    // steps, dm_navs / dm_volumes / verify calls, dm_set_coords copies) may
+    // still read the resident coordinates: the copy-in waits for all of it
+    DM_CK(c, cudaEventRecord(c->ev_comp, c->stream));
     DM_CK(c, cudaStreamWaitEvent(c->s_h2d, c->ev_comp, 0));
     DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * c->dim * c->nv,
                              cudaMemcpyHostToDevice, c->s_h2d));

@@ -2,6 +2,7 @@
 //
 // Host-only: these entry points touch no device (they load and run on a
 // machine without a GPU).  The formats are described in include/dualmesh/io.hpp.
+#include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstdio>
@@ -87,7 +88,13 @@ Parsed parse_mesh(const std::string& text) {
   long long nv = 0;
   keyword("nodes", nv);
   if (nv >= (1ll << 31)) throw ParseError{line, "node ids are 32-bit"};
-  P.coords.resize(static_cast<size_t>(dim * nv));
+  // grown line by line: a declared count is only trusted as far as the
+  // remaining input could hold it (every value takes >= 2 bytes), so a huge
+  // count over a short file reports the count mismatch, not bad_alloc
+  auto cap = [&](long long values) {
+    return static_cast<size_t>(std::min<long long>(values, (all.size() - std::min(pos, all.size())) / 2 + 1));
+  };
+  P.coords.reserve(cap(dim * nv));
   // the next data line of a section; a missing one (end of file or a
   // keyword line) is a count mismatch reported at that line
   auto data_line = [&](const char* section, long long want, long long got) {
@@ -100,12 +107,15 @@ Parsed parse_mesh(const std::string& text) {
     data_line("node", nv, v);
     if (static_cast<long long>(tk.size()) != dim)
       throw ParseError{line, "expected " + std::to_string(dim) + " coordinates"};
-    for (int d = 0; d < dim; ++d)
-      if (!to_f64(tk[d], P.coords[dim * v + d]))
-        throw ParseError{line, "bad number \"" + std::string(tk[d]) + "\""};
+    for (int d = 0; d < dim; ++d) {
+      double xv;
+      if (!to_f64(tk[d], xv)) throw ParseError{line, "bad number \"" + std::string(tk[d]) + "\""};
+      P.coords.push_back(xv);
+    }
   }
   auto ids = [&](const char* section, long long count, int per, std::vector<int32_t>& out) {
-    out.resize(static_cast<size_t>(count * per));
+    out.clear();
+    out.reserve(cap(count * per));
     for (long long r = 0; r < count; ++r) {
       data_line(section, count, r);
       if (static_cast<int>(tk.size()) != per)
@@ -116,7 +126,7 @@ Parsed parse_mesh(const std::string& text) {
         if (id < 1 || id > nv)
           throw ParseError{line, "invalid index " + std::to_string(id) + " (nodes are 1.." +
                                      std::to_string(nv) + ")"};
-        out[static_cast<size_t>(r * per + a)] = static_cast<int32_t>(id - 1);
+        out.push_back(static_cast<int32_t>(id - 1));
       }
     }
   };

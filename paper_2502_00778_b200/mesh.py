@@ -187,6 +187,10 @@ class Engine:
 
     def set_coords(self, coords: np.ndarray):
         coords = np.ascontiguousarray(coords, np.float64)
+        # dm_set_coords reads dim * n_nodes doubles from the buffer
+        want = self.mesh.dim * self.mesh.num_nodes() if self.mesh is not None else None
+        if want is None or coords.size != want:
+            raise ValueError(f"coords must hold dim*n_nodes = {want} values, got {coords.size}")
         self._ck(self._lib.dm_set_coords(self._c, ptr(coords, C.c_double)), "dm_set_coords")
 
     # ---------------------------------------------------------------- edges

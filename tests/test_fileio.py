@@ -59,6 +59,10 @@ def test_mesh_round_trip_bitwise(tmp_path, mesh_fn):
     ("dualmesh v1\ndim 2\nnodes 3\n0 0\n1 0\n0 1\nelements 2\n1 2 3\n", 8, "count mismatch"),
     ("dualmesh v1\ndim 2\nnodes 3\n0 0\n1 0\n0 1\nelements 1\n1 2 4\n", 8, "invalid index"),
     ("dualmesh v1\ndim 2\nnodes 3\n0 0\n1 0\nelements 1\n1 2 3\n", 6, "count mismatch"),
+    # huge declared counts over a short file: count mismatch, not an allocation failure
+    ("dualmesh v1\ndim 3\nnodes 2000000000\n0 0 0\n", 4, "count mismatch"),
+    ("dualmesh v1\ndim 2\nnodes 3\n0 0\n1 0\n0 1\nelements 1000000000000\n1 2 3\n", 8,
+     "count mismatch"),
     ("dualmesh v2\n", 1, "header"),
     ("dualmesh v1\ndim 4\n", 2, "dim"),
     ("dualmesh v1\ndim 2\nnodes 1\n0 x\nelements 0\n", 4, "bad number"),

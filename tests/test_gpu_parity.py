@@ -29,6 +29,16 @@ def per_vector_rel(a, b, dim):
     return float((num / den).max())
 
 
+def oracle_i32p():
+    import ctypes as C
+    return C.POINTER(C.c_int32)
+
+
+def oracle_u64p():
+    import ctypes as C
+    return C.POINTER(C.c_uint64)
+
+
 def run_all(eng, mesh):
     eng.set_mesh(mesh)
     eng.build_edges()
@@ -222,8 +232,21 @@ def test_edge_of_and_helpers(engine, oracle):
     a[:2500] = el.edges[:2500, 1]  # reversed present pairs
     b[:2500] = el.edges[:2500, 0]
     got = engine.edge_of(a, b)
-    want = np.array([el.edge_of(int(x), int(y)) for x, y in zip(a, b)])
+    # the reference's own EdgeList::edge_of (mesh.cpp:58-73, oracle/_ref) is
+    # the checker; the oracle restatement must agree with it too
+    from oracle.oracle import RefMesh, ref_available
+    if ref_available():
+        r = RefMesh(m)
+        re_, ro = r.build_edges()
+        np.testing.assert_array_equal(re_, el.edges)
+        want = np.array([r.edge_of(int(x), int(y)) for x, y in zip(a, b)])
+    else:
+        want = np.array([oracle.L.or_edge_of(el.edges.ctypes.data_as(oracle_i32p()),
+                                             el.origin_start.ctypes.data_as(oracle_u64p()),
+                                             m.num_nodes(), int(x), int(y))
+                         for x, y in zip(a, b)])
     np.testing.assert_array_equal(got, want)
+    assert (want[:2500] >= 0).all() and (want[2500:] == -1).any()
     assert engine.max_face_area() == oracle.max_face_area(m)
     assert engine.max_element_volume() == oracle.max_element_volume(m)
     assert abs(engine.total_volume() - 1.0) <= 1e-14
@@ -495,6 +518,64 @@ def test_pipelined_host_steps(engine, name, scale):
     finally:
         for p in bufs:
             lib.dm_host_free(p)
+
+
+def test_async_step_after_unsynced_calls(engine):
+    """dm_navs / dm_volumes (and a dm_set_coords copy) still queued on the
+    compute stream, then dm_metrics_host_async with other coordinates and no
+    sync in between: the copy-in must wait for them, so both the
+    earlier fields and the async step equal their synchronous counterparts."""
+    import ctypes as C
+    m = meshgen.baseline_config("C2", 1)
+    engine.set_mesh(m)
+    engine.build_edges()
+    rng = np.random.default_rng(5)
+    inner = (m.coords > 0) * (m.coords < 1)
+    xa = m.coords + rng.uniform(-2e-3, 2e-3, m.coords.size) * inner
+    xb = m.coords + rng.uniform(-2e-3, 2e-3, m.coords.size) * inner
+    nd, nn = m.dim * engine.n_edges, m.num_nodes()
+    # references, synchronous
+    engine.set_coords(xa)
+    engine.navs(DF, GATHER)
+    engine.volumes(EDGE)
+    ref_a = (engine.get_navs(), engine.get_volumes())
+    engine.set_coords(xb)
+    engine.navs(DF, GATHER)
+    engine.volumes(EDGE)
+    ref_b = (engine.get_navs(), engine.get_volumes())
+    lib = _lib.capi()
+    ps = [C.c_void_p() for _ in range(3)]
+    for p, n in zip(ps, (m.coords.size, nd, nn)):
+        assert lib.dm_host_alloc(8 * n, C.byref(p)) == 0
+    try:
+        arr = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n,))
+               for p, n in zip(ps, (m.coords.size, nd, nn))]
+        arr[0][:] = xb
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        for _ in range(3):
+            engine.set_coords(xa)          # queued copy on the compute stream
+            engine.navs(DF, GATHER)        # queued kernels reading xa
+            engine.volumes(EDGE)
+            engine.metrics_host_async(dp(arr[0]), DF, GATHER, EDGE, dp(arr[1]), dp(arr[2]))
+            engine.sync()
+            np.testing.assert_array_equal(arr[1], ref_b[0])
+            np.testing.assert_array_equal(arr[2], ref_b[1])
+        # the first dm_navs of the loop computed on xa: check it via a rerun
+        engine.set_coords(xa)
+        engine.navs(DF, GATHER)
+        engine.volumes(EDGE)
+        np.testing.assert_array_equal(engine.get_navs(), ref_a[0])
+        np.testing.assert_array_equal(engine.get_volumes(), ref_a[1])
+    finally:
+        for p in ps:
+            lib.dm_host_free(p)
+
+
+def test_set_coords_checks_length(engine):
+    m = meshgen.baseline_config("C2", 8)
+    engine.set_mesh(m)
+    with pytest.raises(ValueError):
+        engine.set_coords(m.coords[:-1])
 
 
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C3", 4), ("C5", 2)])

@@ -261,3 +261,17 @@ def test_linear_exactness_spec_examples(oracle, mesh_fn, tol):
     n2 = n.copy()
     n2[D * q:D * q + D] += 1e-3
     assert oracle.check_linear_exactness(m, e, n2, v, A, b) > 1e3 * tol
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 16])
+def test_oracle_generator_equals_product_generator(oracle, n):
+    """The bench's CPU legs generate their grid with the oracle's own
+    generator (or_gen_tet_cube); it must be bitwise the grid the GPU arm
+    times (BASELINE C2/C5 family)."""
+    from paper_2502_00778_b200 import meshgen
+    a = oracle.gen_tet_cube(n, amp=0.15, seed=42)
+    b = meshgen.tet_cube(n, amp=0.15)
+    assert np.array_equal(a.coords, b.coords)
+    assert np.array_equal(a.elements, b.elements)
+    assert np.array_equal(a.boundary, b.boundary)
+    assert oracle.max_element_volume(a) > 0
