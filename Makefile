@@ -16,7 +16,7 @@ CXXFLAGS := -O2 -fPIC -std=c++20 -ffp-contract=off -Iinclude
 
 CU_SRCS := $(CSRC)/capi.cu $(CSRC)/primitives.cu $(CSRC)/edges.cu $(CSRC)/navs.cu \
            $(CSRC)/volumes.cu $(CSRC)/verify.cu $(CSRC)/validate.cu $(CSRC)/tables.cu \
-           $(CSRC)/rings.cu $(CSRC)/devgen.cu $(CSRC)/devmem.cu
+           $(CSRC)/rings.cu $(CSRC)/rowplan.cu $(CSRC)/devgen.cu $(CSRC)/devmem.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) include/dm_capi.h
 

@@ -135,7 +135,8 @@ int dm_set_mesh(dm_ctx* c, int dim, const double* coords, int64_t n_nodes, const
   c->nv = n_nodes;
   c->nE = n_elements;
   c->nB = n_boundary;
-  DM_CK(c, c->coords.ensure(static_cast<size_t>(dim * n_nodes)));
+  // two spare records: the row plan's TMA copies round node runs up to even ids
+  DM_CK(c, c->coords.ensure(static_cast<size_t>(dim * (n_nodes + 2))));
   DM_CK(c, c->elems.ensure(static_cast<size_t>((dim + 1) * n_elements)));
   DM_CK(c, c->bnd.ensure(static_cast<size_t>(dim * n_boundary)));
   if (n_nodes)

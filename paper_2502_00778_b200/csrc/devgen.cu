@@ -228,7 +228,7 @@ int begin_mesh(dm_ctx* c, int dim, i64 nv, i64 nE, i64 nB) {
   c->nv = nv;
   c->nE = nE;
   c->nB = nB;
-  DM_CK(c, c->coords.ensure(static_cast<size_t>(dim * nv)));
+  DM_CK(c, c->coords.ensure(static_cast<size_t>(dim * (nv + 2))));  // row plan: even-rounded runs
   DM_CK(c, c->elems.ensure(static_cast<size_t>((dim + 1) * nE)));
   DM_CK(c, c->bnd.ensure(static_cast<size_t>(dim * nB)));
   return DM_OK;

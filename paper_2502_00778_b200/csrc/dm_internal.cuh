@@ -208,6 +208,12 @@ struct dm_ctx {
   dm::i64 n_bseg = 0;              // boundary edges (segments of bedge_p)
   dm::DevBuf<int4> bseg;           // per boundary edge {e, j, k, p}
   dm::DevBuf<dm::u32> bseg_start;  // its facets: bedge_p[bseg_start[i] .. bseg_start[i+1])
+  // row-tile plan (rowplan.cu), chosen over the Morton tiles for node
+  // numberings whose id-contiguous edge ranges have small node tables
+  bool row_plan = false;
+  dm::i64 rt_ntiles = 0;
+  dm::DevBuf<int4> rt_meta;         // per tile {code offset (32 B units), code bytes, runs, 0}
+  dm::DevBuf<int2> rt_runs;         // kRowRuns per tile {first node, nodes | slot << 16}
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
   dm::DevBuf<int32_t> n2e;
@@ -293,6 +299,13 @@ constexpr int kTileNodeCap = 1536;
 constexpr int kTileFillRanks = 256;
 constexpr int kTileFillSlots = 512;
 constexpr int kRingMax = 24;
+// Row-tile plan (rowplan.cu): tiles are contiguous edge-id ranges of at most
+// kRowTile edges (7 warps) whose node table -- node-id runs copied straight
+// from the caller's coordinates -- holds at most kRowSlots records.
+constexpr int kRowTile = 224;
+constexpr int kRowSlots = 256;
+constexpr int kRowRuns = 32;       // node runs per tile (TMA bulk copies)
+constexpr int kRowCodeCap = 4096;  // code bytes per tile (tile header + warp blocks)
 
 inline unsigned grid_for(i64 n, int per_block) {
   return static_cast<unsigned>((n + per_block - 1) / per_block);
@@ -359,6 +372,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!done);
+}
+// TMA bulk copy global -> shared (no tensor map): `bytes` (multiple of 16,
+// both addresses 16-byte aligned) complete_tx on `bar`; the issuing thread
+// first registers them with an arrive + expect_tx.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1; }" ::"r"(a),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes,
+                                         uint64_t* bar) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s),
+      "l"(gmem), "r"(bytes), "r"(b)
+      : "memory");
+}
+// TMA bulk copy shared -> global (bulk-group completion); the source must be
+// made visible to the async proxy first (fence_async_smem).
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(s),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
@@ -430,6 +477,9 @@ int ensure_n2e(dm_ctx* c);
 int ensure_ifl(dm_ctx* c);  // face-list incidence for the FACES / traditional fallbacks
 int ensure_tables(dm_ctx* c);
 int ensure_rings(dm_ctx* c);
+// rowplan.cu: builds the row-tile plan if the node numbering allows it
+// (sets c->row_plan); called by ensure_rings before the Morton plan.
+int try_row_plan(dm_ctx* c);
 int build_edges_impl(dm_ctx* c);
 int navs_impl(dm_ctx* c, int algo, int variant);
 int volumes_impl(dm_ctx* c, int algo);

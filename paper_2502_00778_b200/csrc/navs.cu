@@ -415,7 +415,19 @@ __device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m
       }
     }
   }
-  if (m.y <= SM::kCodeBytes) {
+  if constexpr ((OPT & 128) != 0) {
+    // the tile's code block (contiguous, a multiple of 32 bytes) in one TMA
+    // bulk copy completing on full[b]; thread 0 is the extra arrival
+    if (t == 0) {
+      if (m.y <= SM::kCodeBytes && m.y > 0) {
+        mbar_arrive_expect_tx(&S.full[b], static_cast<unsigned>(m.y));
+        bulk_g2s(&S.cd[b][0], rcodes + 32 * static_cast<i64>(m.x), static_cast<unsigned>(m.y),
+                 &S.full[b]);
+      } else {
+        mbar_arrive(&S.full[b]);
+      }
+    }
+  } else if (m.y <= SM::kCodeBytes) {
     // code blocks are multiples of 32 bytes: 16-byte pieces
     const uint4* src = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x));
     for (int w = t; w < m.y / 16; w += kEB) {
@@ -471,19 +483,56 @@ struct RingCodes {
     if constexpr (W == 2) return (raw(0) & 0x8000u) != 0;
     else return (blk[lane] & 32) != 0;
   }
+  // closed ring: its last slot repeats m_0 (rings.cu k_ring_codes)
+  __device__ __forceinline__ bool closed() const {
+    if constexpr (W == 2) return (raw(0) & 0x4000u) != 0;
+    else return (blk[lane] & 128) != 0;
+  }
 };
 
 // Walks one edge's ring; T(slot) returns the node record of a tile slot.
 // x_j is not needed by the walk; the caller reads it afterwards (fewer live
-// registers across the loop).
-template <int W, int RU = 1, typename TabFn>
-__device__ __forceinline__ void ring_walk(const TabFn& T, const RingCodes<W>& C, double* acc,
+// registers across the loop).  KEEP0: a closed ring's last term reuses
+// d_0 = m_0 - x_k from registers instead of re-reading m_0 from the table
+// (same operands, same bits).
+template <int RU = 1, bool KEEP0 = false, typename CT, typename TabFn>
+__device__ __forceinline__ void ring_walk(const TabFn& T, const CT& C, double* acc,
                                           d4& xk) {
   const int n = C.count();
   xk = T(C.slot(1));
   const d4 mp = T(C.slot(2));
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if constexpr (KEEP0) {
+    static_assert(RU == 1, "KEEP0 walks one step at a time");
+    const bool cl = C.closed();
+    const double fx = dx, fy = dy, fz = dz;
+    const int nr = cl ? n - 1 : n;
+    for (int i = 0; i < nr; ++i) {
+      const d4 m = T(C.raw(3 + i));
+      const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
+      double c0, c1, c2;
+      cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
+      a0 += c0;
+      a1 += c1;
+      a2 += c2;
+      dx = ex;
+      dy = ey;
+      dz = ez;
+    }
+    if (cl) {
+      double c0, c1, c2;
+      cross3(dx, dy, dz, fx, fy, fz, c0, c1, c2);
+      a0 += c0;
+      a1 += c1;
+      a2 += c2;
+    }
+    const bool neg = C.negative();
+    acc[0] = neg ? -a0 : a0;
+    acc[1] = neg ? -a1 : a1;
+    acc[2] = neg ? -a2 : a2;
+    return;
+  }
   for (int i0 = 0; i0 < n; i0 += RU) {
     unsigned w[RU];
 #pragma unroll
@@ -523,8 +572,8 @@ __device__ __forceinline__ void ring_walk(const TabFn& T, const RingCodes<W>& C,
 // it).  The centroids are summed from S = x_j + x_k (= 2m exactly) instead of
 // in local order, so results are within rounding of the serial loop (<= 1e-12
 // per edge vector), not bitwise; x_j / x_k are re-read by the caller.
-template <int W, typename TabFn>
-__device__ __forceinline__ void ring_walk_trad(const TabFn& T, const RingCodes<W>& C, double* acc) {
+template <typename CT, typename TabFn>
+__device__ __forceinline__ void ring_walk_trad(const TabFn& T, const CT& C, double* acc) {
   const int n = C.count();
   double mx, my, mz, ex, ey, ez;
   {
@@ -601,11 +650,12 @@ __global__ void __launch_bounds__(kEB, MINB)
   // evaluation; a warp waits only for the fill it reads and, before
   // refilling a buffer, for every warp to be done with its previous use
   constexpr bool MB = (OPT & 16) != 0;
-  static_assert(!MB || NB == 3, "the mbarrier pipeline uses three buffers");
+  static_assert(!MB || NB >= 3, "the mbarrier pipeline uses three or more buffers");
+  static_assert(!(OPT & 128) || MB, "the TMA code fill completes on the full mbarriers");
   if (MB) {
     if (t == 0) {
       for (int i = 0; i < NB; ++i) {
-        mbar_init(&S.full[i], kEB);
+        mbar_init(&S.full[i], kEB + ((OPT & 128) ? 1 : 0));
         mbar_init(&S.empty[i], kEB / 32);
       }
     }
@@ -631,8 +681,9 @@ __global__ void __launch_bounds__(kEB, MINB)
     // 8 no ring walk, 16 component-major navs stores, 32 one 32-byte row
     // (navs, s) per edge
     if (nxt < ntiles) {
-      // buffer bn's use (it + 1) / 3 waits for its previous use to be read
-      if (MB && it >= 2) mbar_wait(&S.empty[bn], static_cast<unsigned>((it + 1) / 3 - 1) & 1u);
+      // buffer bn's use (it + 1) / NB waits for its previous use to be read
+      if (MB && it + 1 >= NB)
+        mbar_wait(&S.empty[bn], static_cast<unsigned>((it + 1) / NB - 1) & 1u);
       if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
       else pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
       if (MB) cp_async_mbar_arrive(&S.full[bn]);
@@ -651,7 +702,7 @@ __global__ void __launch_bounds__(kEB, MINB)
     m_nxt = nxt + G < ntiles ? __ldg(meta + 2 * (nxt + G)) : make_int4(0, 0, 0, 0);
     pipe_ids<CAP / kEB, (OPT & 32) != 0>(nxt + G, ntiles, tnodes, eperm, ne, ids, sl, e_nxt);
     if (MB) {
-      mbar_wait(&S.full[b], static_cast<unsigned>(it / 3) & 1u);
+      mbar_wait(&S.full[b], static_cast<unsigned>(it / NB) & 1u);
     } else {
       cp_async_wait<1>();
       __syncthreads();
@@ -680,7 +731,7 @@ __global__ void __launch_bounds__(kEB, MINB)
         };
         const RingCodes<W> C{reinterpret_cast<const uint8_t*>(S.cd[b]) + wo, lane};
         if constexpr (ALGO == kTraditional) {
-          ring_walk_trad<W>(T, C, acc);
+          ring_walk_trad(T, C, acc);
           xk = T(C.slot(1));
           xj = T(C.slot(0));
         } else {
@@ -688,7 +739,7 @@ __global__ void __launch_bounds__(kEB, MINB)
             xk = T(C.slot(1));
             acc[0] = xk.x;
           } else {
-            ring_walk<W, RU>(T, C, acc, xk);
+            ring_walk<RU, (OPT & 64) != 0>(T, C, acc, xk);
           }
           xj = T(C.slot(0));
         }
@@ -704,10 +755,10 @@ __global__ void __launch_bounds__(kEB, MINB)
         };
         const RingCodes<W> C{rcodes + 32 * static_cast<i64>(m.x) + wo, lane};
         if constexpr (ALGO == kTraditional) {
-          ring_walk_trad<W>(T, C, acc);
+          ring_walk_trad(T, C, acc);
           xk = T(C.slot(1));
         } else {
-          ring_walk<W>(T, C, acc, xk);
+          ring_walk(T, C, acc, xk);
         }
         xj = T(C.slot(0));
       }
@@ -750,6 +801,150 @@ __global__ void __launch_bounds__(kEB, MINB)
     }
   }
   cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------ GATHER (row tiles)
+// The 3D default for node numberings with spatial coherence (rowplan.cu).
+// Persistent CTAs of kRowTile threads walk the row tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ...  Per tile, warp 0 issues TMA bulk copies of the
+// next tile's node runs (straight from the caller's coordinates) and code
+// block into the other buffer, completing on that buffer's mbarrier; each
+// thread walks its edge's ring from the table, stages its navs row and s term
+// in shared memory, and after the tile barrier thread 0 writes the tile's
+// rows as two bulk stores (the <= 2 rows outside the 16-byte-aligned middle
+// with plain stores).  Same arithmetic as k_navs_ring_pipe.
+struct RowCodes {
+  const uint8_t* __restrict__ st;  // step rows of the warp block
+  int lane, hdr;
+  __device__ __forceinline__ unsigned raw(int s) const { return st[s * 32 + lane]; }
+  __device__ __forceinline__ unsigned slot(int s) const { return raw(s); }
+  __device__ __forceinline__ int count() const { return hdr & 31; }
+  __device__ __forceinline__ bool negative() const { return (hdr & 32) != 0; }
+  __device__ __forceinline__ bool closed() const { return (hdr & 128) != 0; }
+};
+
+struct RowSmem {
+  double tab[2][3 * kRowSlots];       // node records (x, y, z), 24 B per slot
+  uint8_t cd[2][kRowCodeCap];         // tile header + warp code blocks
+  double stg[2][3 * (kRowTile + 2)];  // staged navs rows (row r = e - e0 + (e0 & 1))
+  double sst[2][kRowTile + 2];        // staged s terms
+  uint64_t full[2];
+};
+static_assert(sizeof(double) * 3 * (kRowTile + 2) % 16 == 0 && (kRowTile + 2) * 8 % 16 == 0,
+              "RowSmem members stay 16-byte aligned");
+
+template <int ALGO, int MINB>
+__global__ void __launch_bounds__(kRowTile, MINB)
+    k_navs_row(const int4* __restrict__ meta, const int2* __restrict__ runs,
+               const uint8_t* __restrict__ rcodes, const double* __restrict__ X, int ntiles,
+               double* __restrict__ navs, double* __restrict__ svals) {
+  RowSmem& S = *reinterpret_cast<RowSmem*>(dm_smem);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  const int G = gridDim.x;
+  if (t == 0) {
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+  }
+  __syncthreads();
+  // warp 0: node runs + code block of a tile into buffer b (one arrival with
+  // the transaction bytes, then the copies)
+  auto issue = [&](int b, const int4& m, const int2& rn) {
+    const unsigned bytes = lane < m.z ? 24u * static_cast<unsigned>(rn.y & 0xffff) : 0u;
+    const unsigned total = __reduce_add_sync(0xffffffffu, bytes) + static_cast<unsigned>(m.y);
+    if (lane == 0) mbar_arrive_expect_tx(&S.full[b], total);
+    __syncwarp();
+    if (lane < m.z)
+      bulk_g2s(&S.tab[b][3 * (rn.y >> 16)], X + 3 * static_cast<i64>(rn.x), bytes, &S.full[b]);
+    if (lane == 0)
+      bulk_g2s(S.cd[b], rcodes + 32 * static_cast<i64>(m.x), static_cast<unsigned>(m.y),
+               &S.full[b]);
+  };
+  auto ld_runs = [&](int tl, int nr) -> int2 {
+    return lane < nr ? __ldg(runs + static_cast<i64>(tl) * kRowRuns + lane) : make_int2(0, 0);
+  };
+  int4 mA = make_int4(0, 0, 0, 0), mB = make_int4(0, 0, 0, 0);
+  int2 rA = make_int2(0, 0);
+  if (warp == 0) {
+    const int4 m0 = __ldg(meta + tile);
+    issue(0, m0, ld_runs(tile, m0.z));
+    if (tile + G < ntiles) {
+      mA = __ldg(meta + tile + G);
+      rA = ld_runs(tile + G, mA.z);
+    }
+    if (tile + 2 * G < ntiles) mB = __ldg(meta + tile + 2 * G);
+  }
+  for (int it = 0; tile < ntiles; ++it, tile += G) {
+    const int b = it & 1;
+    const int nxt = tile + G;
+    if (warp == 0) {
+      if (nxt < ntiles) issue(b ^ 1, mA, rA);
+      rA = nxt + G < ntiles ? ld_runs(nxt + G, mB.z) : make_int2(0, 0);
+      mA = mB;
+      mB = nxt + 2 * G < ntiles ? __ldg(meta + nxt + 2 * G) : make_int4(0, 0, 0, 0);
+    }
+    mbar_wait(&S.full[b], static_cast<unsigned>(it >> 1) & 1u);
+    const int* hd = reinterpret_cast<const int*>(S.cd[b]);
+    const int e0 = hd[0], cnt = hd[1], sh = e0 & 1;
+    if (t < cnt) {
+      const unsigned wo = reinterpret_cast<const uint16_t*>(hd + 2)[warp];
+      const uint8_t* blk = S.cd[b] + wo;
+      const int off = blk[32 + lane];
+      const RowCodes C{blk + 64, lane, blk[lane]};
+      const double* tab = S.tab[b];
+      auto T = [&](unsigned i) -> d4 {
+        const double* q = tab + 3 * i;
+        d4 r;
+        r.x = q[0];
+        r.y = q[1];
+        r.z = q[2];
+        r.w = 0.0;
+        return r;
+      };
+      double acc[3];
+      d4 xj, xk;
+      if constexpr (ALGO == kTraditional) {
+        ring_walk_trad(T, C, acc);
+        xk = T(C.slot(1));
+      } else {
+        ring_walk(T, C, acc, xk);
+      }
+      xj = T(C.slot(0));
+      double nv[3], s;
+      edge_tail_values<3, ALGO>(Coords<3>{nullptr}, 0, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
+      const int r = off + sh;
+      double* row = S.stg[b] + 3 * r;
+      row[0] = nv[0];
+      row[1] = nv[1];
+      row[2] = nv[2];
+      S.sst[b][r] = s;
+    }
+    fence_async_smem();
+    if (t == 0) bulk_wait_read<0>();  // the previous tile's stores have read their stage
+    __syncthreads();
+    if (t == 0) {
+      const int a = e0 + sh, end = e0 + cnt, bend = end & ~1;
+      if (bend > a) {
+        bulk_s2g(navs + 3 * static_cast<i64>(a), S.stg[b] + 3 * (a - e0 + sh),
+                 24u * static_cast<unsigned>(bend - a));
+        bulk_s2g(svals + a, S.sst[b] + (a - e0 + sh), 8u * static_cast<unsigned>(bend - a));
+      }
+      bulk_commit();
+      auto plain = [&](int e) {
+        const int r = e - e0 + sh;
+        navs[3 * static_cast<i64>(e)] = S.stg[b][3 * r];
+        navs[3 * static_cast<i64>(e) + 1] = S.stg[b][3 * r + 1];
+        navs[3 * static_cast<i64>(e) + 2] = S.stg[b][3 * r + 2];
+        svals[e] = S.sst[b][r];
+      };
+      if (sh) plain(e0);
+      if ((end & 1) && end - 1 >= a) plain(end - 1);
+    }
+  }
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ GATHER_FACES
@@ -1000,6 +1195,37 @@ int launch_navs(dm_ctx* c, int variant) {
               c->svals.p);
     tmark(c, 1);
     tmark(c, 2);
+  } else if (variant == DM_VARIANT_GATHER && D == 3 && c->ring_ok && c->row_plan) {
+    tmark(c, 0);
+    if constexpr (D == 3) {
+      auto launch = [&](auto kern) -> int {
+        const int smem = static_cast<int>(sizeof(RowSmem));
+        DM_CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0, nsm = 0;
+        DM_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowTile, smem));
+        DM_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+        const unsigned grid = static_cast<unsigned>(
+            std::min<i64>(c->rt_ntiles, static_cast<i64>(nsm) * std::max(per_sm, 1)));
+        DM_LAUNCH(c, kern, grid, kRowTile, smem, c->rt_meta.p, c->rt_runs.p, c->rcodes.p,
+                  c->coords.p, static_cast<int>(c->rt_ntiles), c->navs.p, c->svals.p);
+        return DM_OK;
+      };
+      int st = DM_OK;
+      if (ALGO == kTraditional) st = launch(k_navs_row<kTraditional, 2>);
+      else if (c->gather_cfg == 61) st = launch(k_navs_row<kDualFree, 4>);
+      else if (c->gather_cfg == 62) st = launch(k_navs_row<kDualFree, 6>);
+      else st = launch(k_navs_row<kDualFree, 5>);  // 56 registers, 5 x 35 KB shared
+      if (st) return st;
+    }
+    tmark(c, 1);
+    if constexpr (D == 3 && ALGO == kDualFree) {
+      if (c->n_bedge > 0) {
+        DM_LAUNCH(c, k_ring_boundary, grid_for(c->n_bseg, 256), 256, 0, c->bseg.p,
+                  c->bseg_start.p, c->n_bseg, c->bedge_p.p, Coords3R{c->coords.p}, c->bnd.p,
+                  false, c->navs.p, c->svals.p);
+      }
+    }
+    tmark(c, 2);
   } else if (variant == DM_VARIANT_GATHER && D == 3 && c->ring_ok) {
     tmark(c, 0);
     if constexpr (D == 3) {
@@ -1044,6 +1270,12 @@ int launch_navs(dm_ctx* c, int variant) {
           case 36: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 2>, sizeof(PipeSmem<256>)); break;
           case 37: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           case 38: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 51: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 128, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 52: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 64 | 128, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
+          case 53: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 4>, sizeof(PipeSmem<256, 4, 2048>)); break;
+          case 54: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 128, 4>, sizeof(PipeSmem<256, 4, 2048>)); break;
+          case 55: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 128, 5>, sizeof(PipeSmem<256, 5, 2048>)); break;
+          case 50: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 64, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
           // tests: a 16-code shared buffer sends every tile down the
           // global-memory path of the same kernel
           case 41: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 3, 16>, sizeof(PipeSmem<256, 3, 16>)); break;
@@ -1146,8 +1378,11 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
     // every call reads the caller's coordinates: the ring walk's table source
     // (Morton-order copy) or the padded copy of the other kernels is rebuilt
     // here, inside the metrics step, never carried over from an earlier call
-    st = variant == DM_VARIANT_GATHER && c->ring_ok ? refresh_ring_coords(c) : pad_x4(c);
-    if (st) return st;
+    // (the row-tile plan reads the caller's coordinates directly: no copy)
+    if (!(variant == DM_VARIANT_GATHER && c->ring_ok && c->row_plan)) {
+      st = variant == DM_VARIANT_GATHER && c->ring_ok ? refresh_ring_coords(c) : pad_x4(c);
+      if (st) return st;
+    }
     st = algo == DM_NAV_DUALFREE ? launch_navs<3, kDualFree>(c, variant)
                                  : launch_navs<3, kTraditional>(c, variant);
   } else {
@@ -1155,7 +1390,8 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
                                  : launch_navs<2, kTraditional>(c, variant);
   }
   if (st) return st;
-  c->svals_pos = variant == DM_VARIANT_GATHER && c->dim == 3 && c->ring_ok && c->vol_by_rank;
+  c->svals_pos = variant == DM_VARIANT_GATHER && c->dim == 3 && c->ring_ok && !c->row_plan &&
+                c->vol_by_rank;
   c->have_navs = true;
   c->navs_algo = algo;
   c->have_vols = false;

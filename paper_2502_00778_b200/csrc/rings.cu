@@ -60,6 +60,7 @@
 #include <vector>
 
 #include "dm_internal.cuh"
+#include "ring_encode.cuh"
 
 #include <chrono>
 #include <cstdio>
@@ -151,14 +152,6 @@ __device__ __forceinline__ int tslot(const int32_t* list, int n, int v) {
   return lo;
 }
 
-// parity of the permutation taking (a0,a1,a2) to (b0,b1,b2): +1 even, -1 odd
-__device__ __forceinline__ int perm_sign(int a0, int a1, int a2, int b0, int b1, int b2) {
-  // rotate (a) so that a0 == b0, then compare the second entries
-  const int x1 = a0 == b0 ? a1 : (a1 == b0 ? a2 : a0);
-  (void)b2;
-  return x1 == b1 ? 1 : -1;
-}
-
 template <int W>
 __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __restrict__ eperm,
                              const int32_t* __restrict__ inc_ptr,
@@ -176,37 +169,8 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
   const int2 jk = edges[e];
   const int j = jk.x, k = jk.y;
   const int pb = inc_ptr[e], n = inc_ptr[e + 1] - pb;
-  if (n > kRingMax) {
-    atomicOr(flag, 4);
-    return;
-  }
-  int a[kRingMax], b[kRingMax], p0[kRingMax], p1[kRingMax], p2[kRingMax];
-  for (int i = 0; i < n; ++i) {
-    const int4 v = reinterpret_cast<const int4*>(el)[inc[pb + i]];
-    const int vs[4] = {v.x, v.y, v.z, v.w};
-    const int ij = vs[0] == j ? 0 : (vs[1] == j ? 1 : (vs[2] == j ? 2 : 3));
-    const unsigned f = (kOppPacked >> (6 * ij)) & 63u;  // ref mesh.cpp:15
-    p0[i] = vs[f & 3];
-    p1[i] = vs[(f >> 2) & 3];
-    p2[i] = vs[(f >> 4) & 3];
-    int o[2], no = 0;
-    for (int q = 0; q < 4; ++q)
-      if (vs[q] != j && vs[q] != k) o[no++] = vs[q];
-    a[i] = o[0];
-    b[i] = o[1];
-  }
-  // start: the smallest node seen exactly once (open chain), else a[0]
-  int start = -1;
-  for (int i = 0; i < n; ++i)
-    for (int s = 0; s < 2; ++s) {
-      const int v = s ? b[i] : a[i];
-      int cnt = 0;
-      for (int q = 0; q < n; ++q) cnt += (a[q] == v) + (b[q] == v);
-      if (cnt == 1 && (start < 0 || v < start)) start = v;
-    }
-  if (start < 0) start = a[0];
   // step s of this edge lives at out[s * 32]; W == 1: one byte per step
-  // after a 32-byte header (n | sign << 5 | boundary << 6 per lane)
+  // after a 32-byte header (n | sign << 5 | boundary << 6 | closed << 7 per lane)
   uint8_t* blk = rcodes + static_cast<i64>(wstart[p >> 5]) * 32;
   uint16_t* out = reinterpret_cast<uint16_t*>(blk) + (p & 31);
   uint8_t* out8 = blk + 32 + (p & 31);
@@ -214,41 +178,24 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
     if constexpr (W == 2) out[step * 32] = static_cast<uint16_t>(v);
     else out8[step * 32] = static_cast<uint8_t>(v);
   };
-  int sg0 = 0;
-  const int s_start = tslot(list, nl, rank[start]);
-  put(2, W == 2 ? (s_start | (bmark[e] ? 0x8000u : 0u)) : s_start);
-  unsigned used = 0;
-  int cur = start;
-  for (int step = 0; step < n; ++step) {
-    int pick = -1;
-    for (int i = 0; i < n; ++i)
-      if (!(used >> i & 1u) && (a[i] == cur || b[i] == cur)) {
-        pick = i;
-        break;
-      }
-    if (pick < 0) {
-      atomicOr(flag, 8);  // non-manifold fan: the walk cannot continue
-      return;
-    }
-    used |= 1u << pick;
-    const int nxt = a[pick] == cur ? b[pick] : a[pick];
-    const int sg = perm_sign(k, cur, nxt, p0[pick], p1[pick], p2[pick]);
-    if (step == 0) sg0 = sg;
-    else if (sg != sg0) {
-      atomicOr(flag, 16);  // inconsistently oriented fan
-      return;
-    }
-    put(3 + step, tslot(list, nl, rank[nxt]));
-    cur = nxt;
+  const RingWalk r = ring_walk_encode(j, k, pb, n, inc, el, [&](int step, int v) {
+    const int sl = tslot(list, nl, rank[v]);
+    put(2 + step, (W == 2 && step == 0) ? (sl | (bmark[e] ? 0x8000u : 0u)) : sl);
+  });
+  if (r.fail) {
+    atomicOr(flag, r.fail);
+    return;
   }
+  // closed: the last ring slot repeats slot(m_0) (word-0 bit 14 / header bit 7)
   const int sj = tslot(list, nl, rank[j]), sk = tslot(list, nl, rank[k]);
   if constexpr (W == 2) {
-    put(0, sj | (sg0 < 0 ? 0x8000u : 0u));
+    put(0, sj | (r.sign < 0 ? 0x8000u : 0u) | (r.closed ? 0x4000u : 0u));
     put(1, sk | n << 11);
   } else {
     put(0, sj);
     put(1, sk);
-    blk[p & 31] = static_cast<uint8_t>(n | (sg0 < 0 ? 32 : 0) | (bmark[e] ? 64 : 0));
+    blk[p & 31] = static_cast<uint8_t>(n | (r.sign < 0 ? 32 : 0) | (bmark[e] ? 64 : 0) |
+                                       (r.closed ? 128 : 0));
   }
 }
 
@@ -924,6 +871,20 @@ int ensure_rings(dm_ctx* c) {
   clk.mark("boundary edges");
   if (c->dim != 3) {
     c->ring_ok = false;
+    c->have_rings = true;
+    return DM_OK;
+  }
+  // row tiles first (rowplan.cu): contiguous edge ranges whose tables fit
+  c->row_plan = false;
+  if (int sr = try_row_plan(c)) return sr;
+  clk.mark("row plan");
+  if (c->row_plan) {
+    c->ring_ok = true;
+    c->code_width = 1;
+    c->vol_by_rank = false;
+    c->plan_colored = false;
+    c->ring_max_nodes = kRowSlots;
+    c->ring_fail = 0;
     c->have_rings = true;
     return DM_OK;
   }
