@@ -188,7 +188,8 @@ int dm_sync(dm_ctx* ctx); /* waits for the ctx stream and the pipelined copies *
 int dm_set_timing(dm_ctx* ctx, int enable);
 int dm_get_timings(dm_ctx* ctx, float* ms, int n);
 int64_t dm_kernel_launches(const dm_ctx* ctx);
-/* Which element-loop kernels the plan enables: info[0] ring path built,
+/* Which element-loop kernels the plan enables: info[0] ring path built (1: Morton
+ * tiles, rings.cu; 2: row tiles, rowplan.cu),
  * [1] ring path usable, [2] row tables built, [3] row tables usable,
  * [4] max tile node count (ring path), [5] failure bits of the ring build (2: a tile
  * touches > 1536 nodes, 4: an edge has > 24 incident elements, 8: non-manifold fan,

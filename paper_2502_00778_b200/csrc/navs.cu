@@ -366,7 +366,6 @@ __global__ void __launch_bounds__(kEB, MINB)
 // applied once.  Tiles with more than CAP nodes or kPipeCodeCap codes are
 // evaluated straight from global memory (same arithmetic, same order).
 constexpr int kPipeCodeCap = 4096;  // 16-bit codes per buffer
-constexpr int kPipeCodeBytes = 2 * kPipeCodeCap;
 extern __shared__ __align__(128) unsigned char dm_smem[];
 
 // NB buffers of CCAP 16-bit code units each.  With two buffers a tile ends
@@ -492,68 +491,27 @@ struct RingCodes {
 
 // Walks one edge's ring; T(slot) returns the node record of a tile slot.
 // x_j is not needed by the walk; the caller reads it afterwards (fewer live
-// registers across the loop).  KEEP0: a closed ring's last term reuses
-// d_0 = m_0 - x_k from registers instead of re-reading m_0 from the table
-// (same operands, same bits).
-template <int RU = 1, bool KEEP0 = false, typename CT, typename TabFn>
-__device__ __forceinline__ void ring_walk(const TabFn& T, const CT& C, double* acc,
-                                          d4& xk) {
+// registers across the loop).  (Keeping d_0 in registers instead of
+// re-reading m_0 for a closed ring's last term measured 10 % slower: the six
+// extra registers cost the loop its unrolling.)
+template <typename CT, typename TabFn>
+__device__ __forceinline__ void ring_walk(const TabFn& T, const CT& C, double* acc, d4& xk) {
   const int n = C.count();
   xk = T(C.slot(1));
   const d4 mp = T(C.slot(2));
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  if constexpr (KEEP0) {
-    static_assert(RU == 1, "KEEP0 walks one step at a time");
-    const bool cl = C.closed();
-    const double fx = dx, fy = dy, fz = dz;
-    const int nr = cl ? n - 1 : n;
-    for (int i = 0; i < nr; ++i) {
-      const d4 m = T(C.raw(3 + i));
-      const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
-      double c0, c1, c2;
-      cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
-      a0 += c0;
-      a1 += c1;
-      a2 += c2;
-      dx = ex;
-      dy = ey;
-      dz = ez;
-    }
-    if (cl) {
-      double c0, c1, c2;
-      cross3(dx, dy, dz, fx, fy, fz, c0, c1, c2);
-      a0 += c0;
-      a1 += c1;
-      a2 += c2;
-    }
-    const bool neg = C.negative();
-    acc[0] = neg ? -a0 : a0;
-    acc[1] = neg ? -a1 : a1;
-    acc[2] = neg ? -a2 : a2;
-    return;
-  }
-  for (int i0 = 0; i0 < n; i0 += RU) {
-    unsigned w[RU];
-#pragma unroll
-    for (int u = 0; u < RU; ++u) w[u] = i0 + u < n ? C.raw(3 + i0 + u) : 0u;
-    d4 m[RU];
-#pragma unroll
-    for (int u = 0; u < RU; ++u) m[u] = T(w[u]);
-#pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      if (i0 + u < n) {
-        const double ex = m[u].x - xk.x, ey = m[u].y - xk.y, ez = m[u].z - xk.z;
-        double c0, c1, c2;
-        cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
-        a0 += c0;
-        a1 += c1;
-        a2 += c2;
-        dx = ex;
-        dy = ey;
-        dz = ez;
-      }
-    }
+  for (int i = 0; i < n; ++i) {
+    const d4 m = T(C.raw(3 + i));
+    const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
+    double c0, c1, c2;
+    cross3(dx, dy, dz, ex, ey, ez, c0, c1, c2);
+    a0 += c0;
+    a1 += c1;
+    a2 += c2;
+    dx = ex;
+    dy = ey;
+    dz = ez;
   }
   const bool neg = C.negative();
   acc[0] = neg ? -a0 : a0;
@@ -620,18 +578,19 @@ __device__ __forceinline__ void ring_walk_trad(const TabFn& T, const CT& C, doub
   acc[2] = a2;
 }
 
-// OPT bits (all give the same bits; C5 element-loop times):
+// OPT bits (all give the same bits; C5 element-loop times, round 1):
 //   1  the (x, y) table and code fill bypasses L1 (cp.async.cg: nothing a
 //      tile fills is re-read through this SM's L1): 2.22 -> 2.17 ms
-// (streaming stores and L1::no_allocate id loads were measured and dropped)
 //   16 mbarrier full / empty pipeline instead of the tile barrier (NB = 3
 //      only): 2.035 -> 2.015 ms
 //   32 the table fill walks the tile's rank-ordered fill list (coloured
 //      256-node plans only): 2.015 -> 1.99 ms
 // NB = 3 buffers drop the end-of-tile barrier (PipeSmem): 2.17 -> 2.035 ms.
-// The default launch is OPT = 49 (1 | 16 | 32), NB = 3.
-template <int CAP, int MINB, int W = 2, int RU = 1, int FAKE = 0, int ALGO = kDualFree,
-          int OPT = 1, int NB = 2, int CCAP = (NB == 2 ? kPipeCodeCap : 2048)>
+// The default launch is OPT = 49 (1 | 16 | 32), NB = 3.  Measured and
+// dropped (profiles/): streaming stores, L1::no_allocate id loads, a TMA
+// bulk code fill (no change), four or five buffers (slower: less L1).
+template <int CAP, int MINB, int W, int ALGO, int OPT, int NB,
+          int CCAP = (NB == 2 ? kPipeCodeCap : 2048)>
 __global__ void __launch_bounds__(kEB, MINB)
     k_navs_ring_pipe(const int32_t* __restrict__ eperm, const uint8_t* __restrict__ rcodes,
                      const int32_t* __restrict__ tnodes, const int4* __restrict__ meta,
@@ -651,11 +610,10 @@ __global__ void __launch_bounds__(kEB, MINB)
   // refilling a buffer, for every warp to be done with its previous use
   constexpr bool MB = (OPT & 16) != 0;
   static_assert(!MB || NB >= 3, "the mbarrier pipeline uses three or more buffers");
-  static_assert(!(OPT & 128) || MB, "the TMA code fill completes on the full mbarriers");
   if (MB) {
     if (t == 0) {
       for (int i = 0; i < NB; ++i) {
-        mbar_init(&S.full[i], kEB + ((OPT & 128) ? 1 : 0));
+        mbar_init(&S.full[i], kEB);
         mbar_init(&S.empty[i], kEB / 32);
       }
     }
@@ -676,16 +634,11 @@ __global__ void __launch_bounds__(kEB, MINB)
     const int b = NB == 2 ? (it & 1) : it % NB;
     const int bn = NB == 2 ? (b ^ 1) : (b + 1 == NB ? 0 : b + 1);
     const int nxt = tile + G;
-    // FAKE (timing probes only, results invalid): 1 conflict-free table
-    // slots, 2 no stores, 4 no coordinate fill after the first two tiles,
-    // 8 no ring walk, 16 component-major navs stores, 32 one 32-byte row
-    // (navs, s) per edge
     if (nxt < ntiles) {
       // buffer bn's use (it + 1) / NB waits for its previous use to be read
       if (MB && it + 1 >= NB)
         mbar_wait(&S.empty[bn], static_cast<unsigned>((it + 1) / NB - 1) & 1u);
-      if ((FAKE & 4) && it >= 1) pipe_issue<CAP, false, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
-      else pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
+      pipe_issue<CAP, true, OPT>(S, bn, nxt, m_nxt, ids, sl, mxy, mz, rcodes, meta);
       if (MB) cp_async_mbar_arrive(&S.full[bn]);
     }
     if (!MB) cp_async_commit();
@@ -721,7 +674,6 @@ __global__ void __launch_bounds__(kEB, MINB)
         const double2* xy = S.xy[b];
         const double* zz = S.z[b];
         auto T = [&](unsigned i) -> d4 {
-          if (FAKE & 1) i = (i & ~15u) | (lane & 15u);
           const double2 v = xy[i];
           d4 r;
           r.x = v.x;
@@ -733,16 +685,10 @@ __global__ void __launch_bounds__(kEB, MINB)
         if constexpr (ALGO == kTraditional) {
           ring_walk_trad(T, C, acc);
           xk = T(C.slot(1));
-          xj = T(C.slot(0));
         } else {
-          if (FAKE & 8) {
-            xk = T(C.slot(1));
-            acc[0] = xk.x;
-          } else {
-            ring_walk<RU, (OPT & 64) != 0>(T, C, acc, xk);
-          }
-          xj = T(C.slot(0));
+          ring_walk(T, C, acc, xk);
         }
+        xj = T(C.slot(0));
       } else {
         auto T = [&](unsigned i) -> d4 {
           const int r = __ldg(tn + i);
@@ -763,35 +709,12 @@ __global__ void __launch_bounds__(kEB, MINB)
         xj = T(C.slot(0));
       }
     }
-    double nv[3] = {0.0, 0.0, 0.0};
-    double s = 0.0;
     if (valid) {
       // scale pass; boundary edges get their facet terms (and s) from
       // k_ring_boundary, launched right after on the same stream
+      double nv[3], s;
       edge_tail_values<3, ALGO>(X, p, acc, xj, xk, nullptr, 0u, 0u, nullptr, nv, s);
-      if (!(FAKE & 34) || s == -12345.0) {
-        double* sp = svals + (pos_s ? p : static_cast<i64>(e));  // rings.cu: vol_by_rank
-        *sp = s;
-      }
-    }
-    if (FAKE & 32) {  // probe: one 32-byte (x, y, z, s) row per edge
-      if (valid) {
-        i64 r = 4 * static_cast<i64>(e);
-        if (r + 4 > 3 * ne) r -= 3 * ne - 4;
-        d4 q;
-        q.x = nv[0];
-        q.y = nv[1];
-        q.z = nv[2];
-        q.w = s;
-        *reinterpret_cast<d4*>(navs + (r & ~3ll)) = q;
-      }
-    } else if (FAKE & 16) {  // probe: component-major (SoA) navs stores
-      if (valid) {
-        navs[e] = nv[0];
-        navs[ne + e] = nv[1];
-        navs[2 * ne + e] = nv[2];
-      }
-    } else if (valid && (!(FAKE & 2) || nv[0] == -12345.0)) {
+      svals[pos_s ? p : static_cast<i64>(e)] = s;  // rings.cu: vol_by_rank
       store_nav_row(navs, e, nv);
     }
     if (NB == 2) __syncthreads();  // buffer b is refilled next iteration
@@ -820,7 +743,6 @@ struct RowCodes {
   __device__ __forceinline__ unsigned slot(int s) const { return raw(s); }
   __device__ __forceinline__ int count() const { return hdr & 31; }
   __device__ __forceinline__ bool negative() const { return (hdr & 32) != 0; }
-  __device__ __forceinline__ bool closed() const { return (hdr & 128) != 0; }
 };
 
 struct RowSmem {
@@ -833,6 +755,11 @@ struct RowSmem {
 static_assert(sizeof(double) * 3 * (kRowTile + 2) % 16 == 0 && (kRowTile + 2) * 8 % 16 == 0,
               "RowSmem members stay 16-byte aligned");
 
+// Design notes (C5, element loop, profiles/r2_ncu_summary.md): 5 CTAs of 56
+// registers beat 4 of 70 (1.55 vs 1.67 ms); a decoupled form without the tile
+// barrier (rotating lane blocks, the last warp refilling and storing) and
+// coalesced 16-byte stores from the stage instead of the bulk stores were
+// both slower (1.79, 1.73 ms); a third stage buffer changed nothing.
 template <int ALGO, int MINB>
 __global__ void __launch_bounds__(kRowTile, MINB)
     k_navs_row(const int4* __restrict__ meta, const int2* __restrict__ runs,
@@ -881,6 +808,8 @@ __global__ void __launch_bounds__(kRowTile, MINB)
     const int b = it & 1;
     const int nxt = tile + G;
     if (warp == 0) {
+      // buffer b ^ 1 was last read by tile it - 1: every warp is past the
+      // barrier that ended it
       if (nxt < ntiles) issue(b ^ 1, mA, rA);
       rA = nxt + G < ntiles ? ld_runs(nxt + G, mB.z) : make_int2(0, 0);
       mA = mB;
@@ -1212,8 +1141,6 @@ int launch_navs(dm_ctx* c, int variant) {
       };
       int st = DM_OK;
       if (ALGO == kTraditional) st = launch(k_navs_row<kTraditional, 2>);
-      else if (c->gather_cfg == 61) st = launch(k_navs_row<kDualFree, 4>);
-      else if (c->gather_cfg == 62) st = launch(k_navs_row<kDualFree, 6>);
       else st = launch(k_navs_row<kDualFree, 5>);  // 56 registers, 5 x 35 KB shared
       if (st) return st;
     }
@@ -1243,54 +1170,22 @@ int launch_navs(dm_ctx* c, int variant) {
       };
       int st = DM_OK;
       // the code width and the table size follow the plan (8-bit codes and a
-      // 256-node table when every tile fits, else 16-bit codes, 512 nodes);
-      // DUALMESH_GATHER_CFG 20-25 are the timing probes of the kernel
+      // 256-node table when every tile fits, else 16-bit codes, 512 nodes)
+      using S3 = PipeSmem<256, 3, 2048>;
       if (ALGO == kTraditional) {  // ~30 live doubles in the walk: 2 CTAs/SM, no spills
         st = c->code_width == 1
-                 ? (c->gather_cfg == 36
-                        ? launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional>, sizeof(PipeSmem<256>))
-                        : launch(k_navs_ring_pipe<256, 2, 1, 1, 0, kTraditional, 17, 3>,
-                                 sizeof(PipeSmem<256, 3, 2048>)))
-                 : launch(k_navs_ring_pipe<512, 2, 2, 1, 0, kTraditional>, sizeof(PipeSmem<512>));
+                 ? launch(k_navs_ring_pipe<256, 2, 1, kTraditional, 17, 3>, sizeof(S3))
+                 : launch(k_navs_ring_pipe<512, 2, 2, kTraditional, 1, 2>, sizeof(PipeSmem<512>));
       } else if (c->code_width == 1) {
-        switch (c->gather_cfg) {
-          case 20: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 1, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 21: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 2, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 22: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 4, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 23: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 8, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 24: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 6, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 25: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 14, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 26: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 16, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 27: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 3, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 28: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 32, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          // A/B configurations of this round's pipeline (same bits): 30 the
-          // round's starting point (2 buffers, .ca fill), 36 + cp.async.cg,
-          // 37 + three buffers, 38 + mbarriers (all but the fill list)
-          case 30: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 0>, sizeof(PipeSmem<256>)); break;
-          case 36: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 2>, sizeof(PipeSmem<256>)); break;
-          case 37: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 1, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 38: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 51: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 128, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 52: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 64 | 128, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          case 53: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 4>, sizeof(PipeSmem<256, 4, 2048>)); break;
-          case 54: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 128, 4>, sizeof(PipeSmem<256, 4, 2048>)); break;
-          case 55: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 128, 5>, sizeof(PipeSmem<256, 5, 2048>)); break;
-          case 50: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49 | 64, 3>, sizeof(PipeSmem<256, 3, 2048>)); break;
-          // tests: a 16-code shared buffer sends every tile down the
-          // global-memory path of the same kernel
-          case 41: st = launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 3, 16>, sizeof(PipeSmem<256, 3, 16>)); break;
-          default:  // coloured plans carry the rank-ordered fill list (OPT & 32)
-            st = c->plan_colored
-                     ? launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 49, 3>, sizeof(PipeSmem<256, 3, 2048>))
-                     : launch(k_navs_ring_pipe<256, 4, 1, 1, 0, kDualFree, 17, 3>, sizeof(PipeSmem<256, 3, 2048>));
-            break;
-        }
+        if (c->gather_cfg == 41)  // test hook: a 16-code shared buffer sends every
+                                  // tile down the global-memory path of the kernel
+          st = launch(k_navs_ring_pipe<256, 4, 1, kDualFree, 49, 3, 16>, sizeof(PipeSmem<256, 3, 16>));
+        else if (c->plan_colored)  // coloured plans carry the rank-ordered fill list (OPT & 32)
+          st = launch(k_navs_ring_pipe<256, 4, 1, kDualFree, 49, 3>, sizeof(S3));
+        else
+          st = launch(k_navs_ring_pipe<256, 4, 1, kDualFree, 17, 3>, sizeof(S3));
       } else {
-        switch (c->gather_cfg) {
-          case 13: st = launch(k_navs_ring_pipe<512, 3, 2>, sizeof(PipeSmem<512>)); break;
-          case 10: st = launch(k_navs_ring_pipe<1024, 2, 2>, sizeof(PipeSmem<1024>)); break;
-          default: st = launch(k_navs_ring_pipe<512, 4, 2>, sizeof(PipeSmem<512>)); break;
-        }
+        st = launch(k_navs_ring_pipe<512, 4, 2, kDualFree, 1, 2>, sizeof(PipeSmem<512>));
       }
       if (st) return st;
     }
@@ -1314,10 +1209,7 @@ int launch_navs(dm_ctx* c, int variant) {
 #define DM_FACES(U, MINB)                                                                     \
   DM_LAUNCH(c, (k_navs_faces<D, ALGO, U, MINB>), tiles, kEB, 0, c->edges.p, c->inc_ptr.p,      \
             c->ifl.p, X, ne, c->bedge.p, c->tile_bptr.p, c->bnd.p, c->navs.p, c->svals.p)
-    switch (c->gather_cfg) {
-      case 1: DM_FACES(4, 2); break;
-      default: DM_FACES(2, 3); break;
-    }
+    DM_FACES(2, 3);
 #undef DM_FACES
     tmark(c, 1);
     tmark(c, 2);
@@ -1327,12 +1219,7 @@ int launch_navs(dm_ctx* c, int variant) {
   DM_LAUNCH(c, (k_navs_gather<D, U, MINB>), tiles, kEB, 0, c->edges.p, c->inc_ptr.p,           \
             c->codes.p, c->adj_ptr.p, c->adj.p, c->os.p, c->tile_meta.p, X, ne, c->bedge.p,  \
             c->tile_bptr.p, c->bnd.p, c->navs.p, c->svals.p)
-    switch (c->gather_cfg) {
-      case 1: DM_TABLE(2, 4); break;
-      case 2: DM_TABLE(4, 2); break;
-      case 3: DM_TABLE(1, 4); break;
-      default: DM_TABLE(2, 3); break;
-    }
+    DM_TABLE(2, 3);
 #undef DM_TABLE
     tmark(c, 1);
     tmark(c, 2);

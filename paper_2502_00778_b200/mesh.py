@@ -359,6 +359,7 @@ class Engine:
         info = np.zeros(8, np.int64)
         self._ck(self._lib.dm_plan_info(self._c, ptr(info, C.c_int64)), "dm_plan_info")
         return {"rings_built": bool(info[0]), "ring_ok": bool(info[1]),
+                "tiles": {0: None, 1: "morton", 2: "row"}.get(int(info[0])),
                 "tables_built": bool(info[2]), "table_ok": bool(info[3]),
                 "ring_max_tile_nodes": int(info[4]), "ring_fail_bits": int(info[5]),
                 "volume_order": "morton" if info[6] else "node",

@@ -585,6 +585,7 @@ def test_colored_plan_same_bits(name, scale, monkeypatch):
     from paper_2502_00778_b200 import Engine
     m = meshgen.baseline_config(name, scale)
     out = []
+    monkeypatch.setenv("DUALMESH_ROW_PLAN", "0")  # the colouring is a Morton-tile pass
     for flag in ("0", "1"):
         monkeypatch.setenv("DUALMESH_PLAN_COLOR", flag)
         eng = Engine(0)
@@ -609,6 +610,7 @@ def test_ring_global_path_same_bits(name, scale, monkeypatch):
     from paper_2502_00778_b200 import Engine
     m = meshgen.baseline_config(name, scale)
     out = []
+    monkeypatch.setenv("DUALMESH_ROW_PLAN", "0")  # the global-memory path is the Morton kernel's
     for cfg in ("0", "41"):
         monkeypatch.setenv("DUALMESH_GATHER_CFG", cfg)
         eng = Engine(0)
@@ -659,7 +661,7 @@ def test_twice_c5_scale():
         eng.navs(DF, GATHER)
         eng.volumes(EDGE)
         info = eng.plan_info()
-        assert info["ring_ok"] and info["colored"]
+        assert info["ring_ok"] and info["tiles"] == "row"
         r, ri = eng.check_closure()
         assert r <= 1e-13 and ri <= 1e-13
         rel, sv, _ = eng.check_total_volume()
@@ -668,3 +670,36 @@ def test_twice_c5_scale():
         assert eng.check_linear_exactness(A, np.array([0.1, -0.2, 0.3])) <= 1e-11
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("name,scale", [("C2", 1), ("C4", 4), ("C5", 2), ("C3", 4)])
+def test_row_and_morton_plans_same_bits(name, scale, monkeypatch, oracle):
+    """Both tilings of the ring walk (rowplan.cu row tiles, rings.cu Morton
+    tiles) walk every ring from the same start in the same direction with the
+    same arithmetic: navs, s terms and volumes are bitwise identical, and within
+    1e-12 per edge vector of the serial oracle.  Randomly numbered grids (C3)
+    must fall back to the Morton tiles."""
+    from paper_2502_00778_b200 import Engine
+    m = meshgen.baseline_config(name, scale)
+    out, kinds = [], []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("DUALMESH_ROW_PLAN", flag)
+        eng = Engine(0)
+        try:
+            eng.set_mesh(m)
+            eng.build_edges()
+            eng.navs(DF, GATHER)
+            eng.volumes(EDGE)
+            kinds.append(eng.plan_info()["tiles"])
+            n, v = eng.get_navs(), eng.get_volumes()
+            eng.navs(TR, GATHER)
+            out.append((n, v, eng.get_navs()))
+        finally:
+            eng.close()
+    assert kinds[1] == "morton"
+    assert kinds[0] == ("morton" if name == "C3" else "row")
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_array_equal(a, b)
+    e, o = oracle.build_edges(m)
+    want = oracle.navs_dualfree(m, e, o)
+    assert per_vector_rel(out[0][0], want, 3) <= 1e-12
