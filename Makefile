@@ -26,6 +26,7 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+
 build/host_api.o: $(CSRC)/host_api.cpp include/dualmesh/mesh.hpp include/dualmesh/metrics.hpp include/dm_capi.h
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -c $< -o $@

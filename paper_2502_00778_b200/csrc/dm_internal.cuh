@@ -212,7 +212,7 @@ struct dm_ctx {
   // numberings whose id-contiguous edge ranges have small node tables
   bool row_plan = false;
   dm::i64 rt_ntiles = 0;
-  dm::DevBuf<int4> rt_meta;         // per tile {code offset (32 B units), code bytes, runs, 0}
+  dm::DevBuf<int4> rt_meta;         // per tile {code offset (32 B units), code bytes, runs, run block}
   dm::DevBuf<int2> rt_runs;         // kRowRuns per tile {first node, nodes | slot << 16}
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
@@ -284,7 +284,10 @@ inline int fail(dm_ctx* c, int code, const std::string& msg) {
     if ((grid) > 0) {                                                                 \
       kern<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                  \
       (ctx)->launches++;                                                              \
-      DM_CK(ctx, cudaGetLastError());                                                 \
+      cudaError_t _le = cudaGetLastError();                                           \
+      if (_le != cudaSuccess)                                                         \
+        return ::dm::fail((ctx), _le == cudaErrorMemoryAllocation ? DM_ERR_OOM : DM_ERR_CUDA, \
+                          std::string("launch of " #kern ": ") + cudaGetErrorString(_le)); \
     }                                                                                 \
   } while (0)
 
@@ -495,6 +498,28 @@ int ensure_x4(dm_ctx* c);
 int refresh_ring_coords(dm_ctx* c);
 int compute_element_volumes(dm_ctx* c);
 int svals_from_navs(dm_ctx* c);
+
+// Host phase timer of the plan (env DUALMESH_PLAN_TIMING=1): synchronises the
+// stream at each mark and prints the wall time since the previous one.
+struct PlanClock {
+  dm_ctx* c;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PlanClock(dm_ctx* ctx) : c(ctx) {
+    const char* e = std::getenv("DUALMESH_PLAN_TIMING");
+    on = e && std::atoi(e) == 1;
+    if (on) cudaStreamSynchronize(c->stream);
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(c->stream);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[plan] %-22s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 // Read a device int flag (synchronises the stream).
 int read_flag(dm_ctx* c, int* value);

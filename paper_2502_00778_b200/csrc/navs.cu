@@ -790,17 +790,17 @@ __global__ void __launch_bounds__(kRowTile, MINB)
       bulk_g2s(S.cd[b], rcodes + 32 * static_cast<i64>(m.x), static_cast<unsigned>(m.y),
                &S.full[b]);
   };
-  auto ld_runs = [&](int tl, int nr) -> int2 {
+  auto ld_runs = [&](int tl, int nr) -> int2 {  // tl: the tile's run block (meta .w)
     return lane < nr ? __ldg(runs + static_cast<i64>(tl) * kRowRuns + lane) : make_int2(0, 0);
   };
   int4 mA = make_int4(0, 0, 0, 0), mB = make_int4(0, 0, 0, 0);
   int2 rA = make_int2(0, 0);
   if (warp == 0) {
     const int4 m0 = __ldg(meta + tile);
-    issue(0, m0, ld_runs(tile, m0.z));
+    issue(0, m0, ld_runs(m0.w, m0.z));
     if (tile + G < ntiles) {
       mA = __ldg(meta + tile + G);
-      rA = ld_runs(tile + G, mA.z);
+      rA = ld_runs(mA.w, mA.z);
     }
     if (tile + 2 * G < ntiles) mB = __ldg(meta + tile + 2 * G);
   }
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(kRowTile, MINB)
       // buffer b ^ 1 was last read by tile it - 1: every warp is past the
       // barrier that ended it
       if (nxt < ntiles) issue(b ^ 1, mA, rA);
-      rA = nxt + G < ntiles ? ld_runs(nxt + G, mB.z) : make_int2(0, 0);
+      rA = nxt + G < ntiles ? ld_runs(mB.w, mB.z) : make_int2(0, 0);
       mA = mB;
       mB = nxt + 2 * G < ntiles ? __ldg(meta + nxt + 2 * G) : make_int4(0, 0, 0, 0);
     }

@@ -663,28 +663,6 @@ __global__ void k_morton_coords(const double* __restrict__ xc, const int32_t* __
   z[r] = __ldg(p + 2);
 }
 
-// Host phase timer of the plan (env DUALMESH_PLAN_TIMING=1): synchronises the
-// stream at each mark and prints the wall time since the previous one.
-struct PlanClock {
-  dm_ctx* c;
-  bool on;
-  std::chrono::steady_clock::time_point t;
-  explicit PlanClock(dm_ctx* ctx) : c(ctx) {
-    const char* e = std::getenv("DUALMESH_PLAN_TIMING");
-    on = e && std::atoi(e) == 1;
-    if (on) cudaStreamSynchronize(c->stream);
-    t = std::chrono::steady_clock::now();
-  }
-  void mark(const char* what) {
-    if (!on) return;
-    cudaStreamSynchronize(c->stream);
-    const auto n = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[plan] %-22s %8.2f ms\n", what,
-                 std::chrono::duration<double, std::milli>(n - t).count());
-    t = n;
-  }
-};
-
 // First arena block: the plan's peak of temporaries in one allocation
 // (k0, k1, i0, rank-sort scratch, rk, cellpack ~ 40 B/node; pinv, bmark,
 // warp sizes ~ 6 B/edge).

@@ -24,13 +24,15 @@
 // The plan is used when the tiles split little (<= 25 % more tiles than
 // ne / kRowTile); otherwise the Morton plan of rings.cu.
 //
-// Code block of a tile (32-byte units, contiguous):
+// Code block of a tile (32-byte units, contiguous, at a fixed kRowCodeCap
+// stride -- the builder writes every tile in one pass, no size scan):
 //   [tile header 32 B: e0 (i32), cnt (i32), eight u16 byte offsets of the
 //    warp blocks from the tile's code start]
 //   per warp w: [32 B: n | sign << 5 | closed << 7 per lane]
 //               [32 B: edge offset e - e0 per lane]
 //               [S_w steps x 32 B: slot(j), slot(k), slot(m_0), slot(m_1) ..]
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -40,9 +42,10 @@
 namespace dm {
 namespace {
 
-constexpr int kRTThreads = 256;   // plan kernels: one CTA per tile
+constexpr int kRTThreads = 256;   // plan kernel: one CTA per tile
 constexpr int kRTHash = 4096;
 constexpr int kRTUniqCap = 512;
+constexpr int kRTCodeUnits = kRowCodeCap / 32;
 
 // infeasibility bits of a candidate tile
 constexpr int kRTTooManyNodes = 1;
@@ -58,6 +61,7 @@ struct RTShared {
   int nruns, nslots;
   int2 runs[kRowRuns];
   int wmax[8];
+  int woff[8];
 };
 
 __device__ __forceinline__ void bitonic_sort_int(int* a, int P, int t) {
@@ -92,19 +96,23 @@ __device__ __forceinline__ void bitonic_sort_u32(unsigned* a, int t) {
     }
 }
 
-// One CTA per candidate tile {e0, cnt}: the node set, its runs, the
-// direction-major lane order and the code size.  BUILD: also writes the runs,
-// each edge's tile and lane position and the block sizes.
-template <bool BUILD>
+// One CTA per candidate tile {e0, cnt} (tile index p = base + blockIdx.x):
+// the tile's node set (shared-memory hash set), sorted; its runs of node-id
+// pairs (a run covers pairs [a, b], i.e. nodes [2a, 2b + 2): every copy is
+// 16-byte aligned; consecutive or equal pairs extend a run); the
+// direction-major lane order; and, if the tile fits (<= kRowRuns runs,
+// <= kRowSlots slots, <= kRowCodeCap code bytes), its runs and its code block
+// at codes + p * kRowCodeCap.  Otherwise bad[p] says why (the host splits it).
 __global__ void __launch_bounds__(kRTThreads)
-    k_rt_tile(const int2* __restrict__ cand, const int2* __restrict__ edges,
-              const u32* __restrict__ os, const int32_t* __restrict__ inc_ptr,
-              const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
-              uint8_t* __restrict__ bad, int2* __restrict__ runs_out, int32_t* __restrict__ tile_of,
-              uint8_t* __restrict__ pos, u32* __restrict__ wsz, int* __restrict__ nruns_out) {
+    k_rt_build(const int2* __restrict__ cand, int base, const int2* __restrict__ edges,
+               const u32* __restrict__ os, const int32_t* __restrict__ inc_ptr,
+               const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
+               uint8_t* __restrict__ bad, int2* __restrict__ runs_out, int* __restrict__ nruns_out,
+               int* __restrict__ bytes_out, uint8_t* __restrict__ codes) {
   __shared__ RTShared S;
-  const int t = threadIdx.x, f = blockIdx.x;
-  const int2 cd = cand[f];
+  const int t = threadIdx.x, lane = t & 31;
+  const i64 p = static_cast<i64>(base) + blockIdx.x;
+  const int2 cd = cand[blockIdx.x];
   const int e0 = cd.x, cnt = cd.y;
   for (int i = t; i < kRTHash; i += kRTThreads) S.hs[i] = -1;
   if (t == 0) S.n_uniq = 0;
@@ -115,8 +123,8 @@ __global__ void __launch_bounds__(kRTThreads)
     for (int probe = 0; probe < kRTHash; ++probe, h = (h + 1) & (kRTHash - 1)) {
       const int old = atomicCAS(&S.hs[h], -1, v);
       if (old == -1) {
-        const int p = atomicAdd(&S.n_uniq, 1);
-        if (p < kRTUniqCap) S.uq[p] = v;
+        const int q = atomicAdd(&S.n_uniq, 1);
+        if (q < kRTUniqCap) S.uq[q] = v;
         return;
       }
       if (old == v) return;
@@ -131,12 +139,16 @@ __global__ void __launch_bounds__(kRTThreads)
     insert(jk.y);
     const int pb = inc_ptr[e];
     n_inc = inc_ptr[e + 1] - pb;
-    for (int q = 0; q < n_inc; ++q) {
+    int last = -1;
+    for (int q = 0; q < n_inc; ++q) {  // the ring nodes: the two others of each element
       const int4 v = reinterpret_cast<const int4*>(el)[inc[pb + q]];
-      insert(v.x);
-      insert(v.y);
-      insert(v.z);
-      insert(v.w);
+      const int vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (vs[a] != jk.x && vs[a] != jk.y && vs[a] != last) {
+          insert(vs[a]);
+          last = vs[a];
+        }
     }
     // direction-major: index of the edge inside its origin row, then origin
     key = (static_cast<unsigned>(e - static_cast<int>(os[jk.x])) << 8) | static_cast<unsigned>(t);
@@ -144,11 +156,10 @@ __global__ void __launch_bounds__(kRTThreads)
   S.key[t] = key;
   __syncthreads();
   const int nu = S.n_uniq;
-  int badbits = 0;
-  if (nu > kRTUniqCap) badbits |= kRTTooManyNodes;
+  int badbits = nu > kRTUniqCap ? kRTTooManyNodes : 0;
   if (__syncthreads_or(t < cnt && n_inc > kRingMax)) badbits |= kRTRingTooLong;
   if (badbits) {
-    if (t == 0) bad[f] = static_cast<uint8_t>(badbits);
+    if (t == 0) bad[p] = static_cast<uint8_t>(badbits);
     return;
   }
   int P = 2;
@@ -156,77 +167,86 @@ __global__ void __launch_bounds__(kRTThreads)
   for (int i = nu + t; i < P; i += kRTThreads) S.uq[i] = 0x7fffffff;
   __syncthreads();
   bitonic_sort_int(S.uq, P, t);
-  // runs of the sorted node ids, each copied as an even-aligned range
-  // [2*floor(a/2), 2*ceil((b+1)/2)); a node within one past the current range
-  // extends it (at most one padding record) instead of opening a run
+  // runs of node pairs: a node whose pair exceeds the previous node's pair
+  // by more than one opens a run (thread 0; ~240 sorted nodes)
   if (t == 0) {
-    int nr = 0, slots = 0, cs = 0, ce = 0;
-    bool ok = true;
+    int nr = 0, slots = 0, a = 0, last = -2;
     for (int i = 0; i < nu; ++i) {
-      const int v = S.uq[i];
-      if (i > 0 && v <= ce + 1) {
-        ce = max(ce, (v + 2) & ~1);
-        continue;
+      const int pr = S.uq[i] >> 1;
+      if (pr > last + 1) {
+        if (i > 0) {
+          if (nr < kRowRuns) S.runs[nr] = make_int2(2 * a, (2 * (last - a + 1)) | slots << 16);
+          slots += 2 * (last - a + 1);
+          ++nr;
+        }
+        a = pr;
       }
-      if (i > 0) {
-        if (nr < kRowRuns) S.runs[nr] = make_int2(cs, (ce - cs) | slots << 16);
-        ++nr;
-        slots += ce - cs;
-      }
-      cs = v & ~1;
-      ce = (v + 2) & ~1;
+      last = pr;
     }
     if (nu > 0) {
-      if (nr < kRowRuns) S.runs[nr] = make_int2(cs, (ce - cs) | slots << 16);
+      if (nr < kRowRuns) S.runs[nr] = make_int2(2 * a, (2 * (last - a + 1)) | slots << 16);
+      slots += 2 * (last - a + 1);
       ++nr;
-      slots += ce - cs;
     }
-    ok = nr <= kRowRuns && slots <= kRowSlots;
     S.nruns = nr;
-    S.nslots = ok ? slots : -1;
+    S.nslots = slots;
   }
   // lane order
   bitonic_sort_u32(S.key, t);
   const unsigned kq = S.key[t];
-  int ring = 0;
-  if (t < cnt) {
-    const int q = static_cast<int>(kq & 0xffu);
-    const int e = e0 + q;
-    ring = inc_ptr[e + 1] - inc_ptr[e];
-    atomicMax(&S.wmax[t >> 5], ring + 3);
-    if (BUILD) {
-      tile_of[e] = f;
-      pos[e] = static_cast<uint8_t>(t);
-    }
-  }
+  const int q = static_cast<int>(kq & 0xffu);
+  const int e = e0 + q;
+  if (t < cnt) atomicMax(&S.wmax[t >> 5], inc_ptr[e + 1] - inc_ptr[e] + 3);
   __syncthreads();
   if (S.nruns > kRowRuns) badbits |= kRTTooManyRuns;
-  if (S.nslots < 0 && S.nruns <= kRowRuns) badbits |= kRTTooManyNodes;
-  int units = 1;  // tile header
-  for (int w = 0; w < kRowTile / 32; ++w)
-    if (w * 32 < cnt) units += 2 + S.wmax[w];
-  if (32 * units > kRowCodeCap) badbits |= kRTTooManyCodes;
-  if (t == 0) bad[f] = static_cast<uint8_t>(badbits);
-  if (!BUILD) return;
-  if (t < kRowRuns) runs_out[static_cast<i64>(f) * kRowRuns + t] = t < S.nruns ? S.runs[t] : make_int2(0, 0);
-  if (t < 8) wsz[8 * static_cast<i64>(f) + t] = t == 0 ? 1u : (32 * (t - 1) < cnt ? 2u + S.wmax[t - 1] : 0u);
-  if (t == 0) nruns_out[f] = S.nruns;
+  else if (S.nslots > kRowSlots) badbits |= kRTTooManyNodes;
+  if (t == 0) {  // warp block byte offsets (S.woff[7]: the tile's code bytes)
+    int units = 1;  // tile header
+    for (int w = 0; w < kRowTile / 32; ++w) {
+      S.woff[w] = 32 * units;
+      if (w * 32 < cnt) units += 2 + S.wmax[w];
+    }
+    S.woff[kRowTile / 32] = 32 * units;
+  }
+  __syncthreads();
+  const int units = S.woff[kRowTile / 32] / 32;
+  if (units > kRTCodeUnits) badbits |= kRTTooManyCodes;
+  if (t == 0) bad[p] = static_cast<uint8_t>(badbits);
+  if (badbits) return;
+  if (t < kRowRuns) runs_out[p * kRowRuns + t] = t < S.nruns ? S.runs[t] : make_int2(0, 0);
+  if (t == 0) {
+    nruns_out[p] = S.nruns;
+    bytes_out[p] = 32 * units;
+  }
+  uint8_t* tb = codes + p * kRowCodeCap;
+  if (t == 0) {  // tile header: e0, cnt, warp block offsets
+    int* h = reinterpret_cast<int*>(tb);
+    h[0] = e0;
+    h[1] = cnt;
+    uint16_t* wo = reinterpret_cast<uint16_t*>(h + 2);
+    for (int w = 0; w < 8; ++w) wo[w] = static_cast<uint16_t>(S.woff[w]);
+  }
+  if (t < cnt) tb[S.woff[t >> 5] + 32 + lane] = static_cast<uint8_t>(q);  // lane -> edge
 }
 
-// Ring codes of every edge (one thread per edge).
-__global__ void k_rt_codes(const int2* __restrict__ tiles, const int2* __restrict__ edges,
-                           const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
-                           const int32_t* __restrict__ el, const int32_t* __restrict__ tile_of,
-                           const uint8_t* __restrict__ pos, const int2* __restrict__ runs,
-                           const int* __restrict__ nruns, const u32* __restrict__ woff, i64 ne,
-                           uint8_t* __restrict__ codes, int* __restrict__ flag) {
-  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= ne) return;
-  const int f = tile_of[e];
-  const int p = pos[e];
-  const int lane = p & 31, w = p >> 5;
-  const int2* R = runs + static_cast<i64>(f) * kRowRuns;
-  const int nr = nruns[f];
+// Ring codes (k_rt_build has written the tile header and each lane's edge
+// offset): one CTA per tile, the runs in shared memory, one thread per lane.
+__global__ void __launch_bounds__(kRowTile)
+    k_rt_codes(const int* __restrict__ order, const int2* __restrict__ edges,
+               const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+               const int32_t* __restrict__ el, const int2* __restrict__ runs,
+               const int* __restrict__ nruns, uint8_t* __restrict__ codes,
+               int* __restrict__ flag) {
+  __shared__ int2 R[kRowRuns];
+  const int t = threadIdx.x, lane = t & 31;
+  const i64 p = order[blockIdx.x];
+  const int nr = nruns[p];
+  if (t < nr) R[t] = runs[p * kRowRuns + t];
+  __syncthreads();
+  uint8_t* tb = codes + p * kRowCodeCap;
+  const int* h = reinterpret_cast<const int*>(tb);
+  const int e0 = h[0], cnt = h[1];
+  if (t >= cnt) return;
   auto slot = [&](int v) -> int {
     for (int r = 0; r < nr; ++r) {
       const int2 x = R[r];
@@ -234,42 +254,33 @@ __global__ void k_rt_codes(const int2* __restrict__ tiles, const int2* __restric
     }
     return -1;
   };
-  const i64 tbase = 32 * static_cast<i64>(woff[8 * static_cast<i64>(f)]);
-  uint8_t* blk = codes + 32 * static_cast<i64>(woff[8 * static_cast<i64>(f) + 1 + w]);
+  uint8_t* blk = tb + reinterpret_cast<const uint16_t*>(h + 2)[t >> 5];
+  const int e = e0 + blk[32 + lane];
   const int2 jk = edges[e];
   const int pb = inc_ptr[e], n = inc_ptr[e + 1] - pb;
   int miss = 0;
-  const RingWalk r = ring_walk_encode(jk.x, jk.y, pb, n, inc, el, [&](int step, int v) {
-    const int s = slot(v);
-    miss |= s < 0;
-    blk[64 + (2 + step) * 32 + lane] = static_cast<uint8_t>(s);
+  const RingWalk rw = ring_walk_encode(jk.x, jk.y, pb, n, inc, el, [&](int step, int v) {
+    const int sl = slot(v);
+    miss |= sl < 0;
+    blk[64 + (2 + step) * 32 + lane] = static_cast<uint8_t>(sl);
   });
-  if (r.fail || miss) {
-    atomicOr(flag, r.fail | (miss ? 1 : 0));
+  if (rw.fail || miss) {
+    atomicOr(flag, rw.fail | (miss ? 1 : 0));
     return;
   }
-  const int sj = slot(jk.x), sk = slot(jk.y);
-  blk[64 + lane] = static_cast<uint8_t>(sj);
-  blk[64 + 32 + lane] = static_cast<uint8_t>(sk);
-  blk[lane] = static_cast<uint8_t>(n | (r.sign < 0 ? 32 : 0) | (r.closed ? 128 : 0));
-  blk[32 + lane] = static_cast<uint8_t>(e - tiles[f].x);
-  if (p == 0) {  // tile header
-    int* h = reinterpret_cast<int*>(codes + tbase);
-    h[0] = tiles[f].x;
-    h[1] = tiles[f].y;
-    uint16_t* wo = reinterpret_cast<uint16_t*>(h + 2);
-    for (int q = 0; q < 8; ++q)
-      wo[q] = static_cast<uint16_t>(32 * (woff[8 * static_cast<i64>(f) + 1 + q] -
-                                          woff[8 * static_cast<i64>(f)]));
-  }
+  blk[64 + lane] = static_cast<uint8_t>(slot(jk.x));
+  blk[64 + 32 + lane] = static_cast<uint8_t>(slot(jk.y));
+  blk[lane] = static_cast<uint8_t>(n | (rw.sign < 0 ? 32 : 0) | (rw.closed ? 128 : 0));
 }
 
-__global__ void k_rt_meta(const u32* __restrict__ woff, const int* __restrict__ nruns, i64 ntiles,
-                          int4* __restrict__ meta) {
+// meta[f] = {code offset (32 B units), code bytes, runs, provisional index}
+// for the tiles in ascending e0 order
+__global__ void k_rt_meta(const int* __restrict__ order, const int* __restrict__ nruns,
+                          const int* __restrict__ bytes, i64 ntiles, int4* __restrict__ meta) {
   const i64 f = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (f >= ntiles) return;
-  const u32 a = woff[8 * f], b = woff[8 * f + 8];
-  meta[f] = make_int4(static_cast<int>(a), static_cast<int>(32 * (b - a)), nruns[f], 0);
+  const int p = order[f];
+  meta[f] = make_int4(p * (kRowCodeCap / 32), bytes[p], nruns[p], p);
 }
 
 __global__ void k_rt_cand(i64 ne, i64 n, int2* __restrict__ cand) {
@@ -305,96 +316,100 @@ size_t rt_block(const dm_ctx* c) { return static_cast<size_t>(16 * c->ne) + (64u
 int try_row_plan(dm_ctx* c) {
   c->row_plan = false;
   if (c->dim != 3 || c->ne == 0) return DM_OK;
-  if (const char* e = std::getenv("DUALMESH_ROW_PLAN"))
-    if (std::atoi(e) == 0) return DM_OK;
+  if (const char* ev = std::getenv("DUALMESH_ROW_PLAN"))
+    if (std::atoi(ev) == 0) return DM_OK;
   ArenaScope scratch(c->arena);
+  PlanClock clk(c);
   const i64 ne = c->ne;
   const i64 n0 = (ne + kRowTile - 1) / kRowTile;
+  // provisional tiles: the level-0 ranges p < n0, then the halves of tiles
+  // that did not fit, appended level by level (about 2 % of tiles at C5)
+  const i64 cap = n0 + n0 / 4 + 1024;
   ScratchBuf<int2> cand(c->arena, rt_block(c));
   ScratchBuf<uint8_t> bad(c->arena, rt_block(c));
+  ScratchBuf<int> nruns(c->arena, rt_block(c)), bytes(c->arena, rt_block(c));
   DM_CK(c, cand.ensure(n0));
-  DM_CK(c, bad.ensure(n0));
+  DM_CK(c, bad.ensure(cap));
+  DM_CK(c, nruns.ensure(cap));
+  DM_CK(c, bytes.ensure(cap));
+  DM_CK(c, c->rt_runs.ensure(static_cast<size_t>(cap * kRowRuns)));
+  DM_CK(c, c->rcodes.ensure(static_cast<size_t>(cap) * kRowCodeCap));
+  DM_CK(c, c->flag.ensure(4));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
   DM_LAUNCH(c, k_rt_cand, grid_for(n0, 256), 256, 0, ne, n0, cand.p);
-  // level 0: fixed kRowTile ranges; infeasible tiles are split in halves
-  std::vector<int2> fin, pend(static_cast<size_t>(n0));
-  DM_CK(c, cudaMemcpyAsync(pend.data(), cand.p, n0 * sizeof(int2), cudaMemcpyDeviceToHost,
+  std::vector<int2> all(static_cast<size_t>(n0));  // provisional tiles, host copy
+  DM_CK(c, cudaMemcpyAsync(all.data(), cand.p, n0 * sizeof(int2), cudaMemcpyDeviceToHost,
                            c->stream));
   std::vector<uint8_t> hb;
-  bool first = true;
-  while (!pend.empty()) {
-    const i64 np = static_cast<i64>(pend.size());
-    DM_CK(c, cand.ensure(np));
-    DM_CK(c, bad.ensure(np));
-    if (!first)
-      DM_CK(c, cudaMemcpyAsync(cand.p, pend.data(), np * sizeof(int2), cudaMemcpyHostToDevice,
-                               c->stream));
-    DM_LAUNCH(c, k_rt_tile<false>, static_cast<unsigned>(np), kRTThreads, 0, cand.p, c->edges.p,
-              c->os.p, c->inc_ptr.p, c->inc.p, c->elems.p, bad.p, nullptr, nullptr, nullptr,
-              nullptr, nullptr);
+  std::vector<int> child(static_cast<size_t>(n0), -1);  // first of the two halves
+  i64 base = 0, np = n0;
+  for (int level = 0; np > 0; ++level) {
+    if (level > 0)
+      DM_CK(c, cudaMemcpyAsync(cand.p, all.data() + base, np * sizeof(int2),
+                               cudaMemcpyHostToDevice, c->stream));
+    DM_LAUNCH(c, k_rt_build, static_cast<unsigned>(np), kRTThreads, 0, cand.p,
+              static_cast<int>(base), c->edges.p, c->os.p, c->inc_ptr.p, c->inc.p, c->elems.p,
+              bad.p, c->rt_runs.p, nruns.p, bytes.p, c->rcodes.p);
     hb.resize(static_cast<size_t>(np));
-    DM_CK(c, cudaMemcpyAsync(hb.data(), bad.p, np, cudaMemcpyDeviceToHost, c->stream));
+    DM_CK(c, cudaMemcpyAsync(hb.data(), bad.p + base, np, cudaMemcpyDeviceToHost, c->stream));
     DM_CK(c, cudaStreamSynchronize(c->stream));
-    std::vector<int2> next;
     i64 nbad = 0;
+    const i64 next = base + np;
     for (i64 i = 0; i < np; ++i) {
-      const int2 t = pend[static_cast<size_t>(i)];
-      if (!hb[static_cast<size_t>(i)]) {
-        fin.push_back(t);
-        continue;
-      }
+      if (!hb[static_cast<size_t>(i)]) continue;
       ++nbad;
-      if ((hb[static_cast<size_t>(i)] & kRTRingTooLong) || t.y < 2) return DM_OK;  // Morton plan
-      const int h = t.y >= 4 ? (t.y / 2 + 1) & ~1 : 1;  // even splits keep e0 even
-      next.push_back(make_int2(t.x, h));
-      next.push_back(make_int2(t.x + h, t.y - h));
+      const int2 tl = all[static_cast<size_t>(base + i)];
+      if ((hb[static_cast<size_t>(i)] & kRTRingTooLong) || tl.y < 2) return DM_OK;  // Morton plan
+      const int h = tl.y >= 4 ? (tl.y / 2 + 1) & ~1 : 1;  // even splits keep e0 even
+      child[static_cast<size_t>(base + i)] = static_cast<int>(all.size());
+      all.push_back(make_int2(tl.x, h));
+      all.push_back(make_int2(tl.x + h, tl.y - h));
+      child.push_back(-1);
+      child.push_back(-1);
     }
-    if (first && nbad * 4 > n0) return DM_OK;  // tables too large: Morton plan
-    first = false;
-    pend.swap(next);
+    if (level == 0 && nbad * 4 > n0) return DM_OK;  // tables too large: Morton plan
+    if (static_cast<i64>(all.size()) > cap) return DM_OK;
+    base = next;
+    np = static_cast<i64>(all.size()) - next;
+    DM_CK(c, cand.ensure(np > 0 ? np : 1));
   }
-  const i64 nt = static_cast<i64>(fin.size());
+  clk.mark("row tiles: build + split");
+  // final order: every level-0 tile, or its halves in place, depth first
+  std::vector<int> order;
+  order.reserve(all.size());
+  std::vector<int> stack;
+  for (i64 i = n0 - 1; i >= 0; --i) stack.push_back(static_cast<int>(i));
+  while (!stack.empty()) {
+    const int pv = stack.back();
+    stack.pop_back();
+    const int ch = child[static_cast<size_t>(pv)];
+    if (ch < 0) {
+      order.push_back(pv);
+    } else {
+      stack.push_back(ch + 1);
+      stack.push_back(ch);
+    }
+  }
+  const i64 nt = static_cast<i64>(order.size());
   if (nt * 4 > n0 * 5) return DM_OK;
-  std::sort(fin.begin(), fin.end(), [](const int2& a, const int2& b) { return a.x < b.x; });
-  ScratchBuf<int2> tiles(c->arena, rt_block(c));
-  ScratchBuf<int32_t> tile_of(c->arena, rt_block(c));
-  ScratchBuf<uint8_t> pos(c->arena, rt_block(c));
-  ScratchBuf<u32> woff(c->arena, rt_block(c));
-  ScratchBuf<int> nruns(c->arena, rt_block(c));
-  DM_CK(c, tiles.ensure(nt));
-  DM_CK(c, tile_of.ensure(ne));
-  DM_CK(c, pos.ensure(ne));
-  DM_CK(c, woff.ensure(8 * nt + 1));
-  DM_CK(c, nruns.ensure(nt));
-  DM_CK(c, bad.ensure(nt));
-  DM_CK(c, c->rt_runs.ensure(static_cast<size_t>(nt * kRowRuns)));
+  ScratchBuf<int> dorder(c->arena, rt_block(c));
+  DM_CK(c, dorder.ensure(nt));
+  DM_CK(c, cudaMemcpyAsync(dorder.p, order.data(), nt * sizeof(int), cudaMemcpyHostToDevice,
+                           c->stream));
   DM_CK(c, c->rt_meta.ensure(static_cast<size_t>(nt)));
-  DM_CK(c, cudaMemcpyAsync(tiles.p, fin.data(), nt * sizeof(int2), cudaMemcpyHostToDevice,
-                           c->stream));
-  DM_LAUNCH(c, k_rt_tile<true>, static_cast<unsigned>(nt), kRTThreads, 0, tiles.p, c->edges.p,
-            c->os.p, c->inc_ptr.p, c->inc.p, c->elems.p, bad.p, c->rt_runs.p, tile_of.p, pos.p,
-            woff.p, nruns.p);
-  int st = scan_exclusive(c, woff.p, woff.p, 8 * nt);
-  if (st) return st;
-  u32 units = 0;
-  DM_CK(c, cudaMemcpyAsync(&units, woff.p + 8 * nt, sizeof(u32), cudaMemcpyDeviceToHost,
-                           c->stream));
-  DM_CK(c, cudaStreamSynchronize(c->stream));
-  const size_t nbytes = 32 * static_cast<size_t>(units);
-  DM_CK(c, c->rcodes.ensure(nbytes + 16));
-  DM_CK(c, cudaMemsetAsync(c->rcodes.p, 0, nbytes + 16, c->stream));
-  DM_CK(c, c->flag.ensure(4));
-  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->stream));
-  DM_LAUNCH(c, k_rt_codes, grid_for(ne, 128), 128, 0, tiles.p, c->edges.p, c->inc_ptr.p, c->inc.p,
-            c->elems.p, tile_of.p, pos.p, c->rt_runs.p, nruns.p, woff.p, ne, c->rcodes.p,
-            c->flag.p);
-  DM_LAUNCH(c, k_rt_meta, grid_for(nt, 256), 256, 0, woff.p, nruns.p, nt, c->rt_meta.p);
-  int fl = 0;
-  DM_CK(c, cudaMemcpyAsync(&fl, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  DM_CK(c, cudaStreamSynchronize(c->stream));
-  if (fl) {  // a fan the walk cannot encode: the Morton plan reports it
-    c->ring_fail = fl;
-    return DM_OK;
+  DM_LAUNCH(c, k_rt_codes, static_cast<unsigned>(nt), kRowTile, 0, dorder.p, c->edges.p,
+            c->inc_ptr.p, c->inc.p, c->elems.p, c->rt_runs.p, nruns.p, c->rcodes.p, c->flag.p);
+  DM_LAUNCH(c, k_rt_meta, grid_for(nt, 256), 256, 0, dorder.p, nruns.p, bytes.p, nt, c->rt_meta.p);
+  {
+    int fl = 0;
+    DM_CK(c, cudaMemcpyAsync(&fl, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    DM_CK(c, cudaStreamSynchronize(c->stream));
+    if (fl) {  // a fan the walk cannot encode: the Morton plan reports it
+      c->ring_fail = fl;
+      return DM_OK;
+    }
   }
+  clk.mark("row tiles: codes");
   // boundary pass lists: positions are edge ids
   const i64 nb = c->n_bedge;
   DM_CK(c, c->bedge_p.ensure(nb > 0 ? nb : 1));
@@ -405,7 +420,7 @@ int try_row_plan(dm_ctx* c) {
     ScratchBuf<u32> idx(c->arena, rt_block(c));
     DM_CK(c, idx.ensure(nb + 1));
     DM_LAUNCH(c, k_rt_bflag, grid_for(nb, 256), 256, 0, c->bedge_p.p, nb, idx.p);
-    st = scan_exclusive(c, idx.p, idx.p, nb);
+    int st = scan_exclusive(c, idx.p, idx.p, nb);
     if (st) return st;
     u32 ns = 0;
     DM_CK(c, cudaMemcpyAsync(&ns, idx.p + nb, sizeof(u32), cudaMemcpyDeviceToHost, c->stream));
@@ -415,6 +430,43 @@ int try_row_plan(dm_ctx* c) {
     DM_LAUNCH(c, k_rt_bseg_fill, grid_for(nb, 256), 256, 0, c->bedge_p.p, nb, idx.p, c->edges.p,
               c->bseg.p, c->bseg_start.p);
     c->n_bseg = ns;
+  }
+  clk.mark("row tiles: meta + boundary lists");
+  if (const char* ck = std::getenv("DUALMESH_PLAN_CHECK")) {  // debugging aid: host audit
+    if (std::atoi(ck) == 1) {
+      std::vector<int4> hm(static_cast<size_t>(nt));
+      std::vector<int2> hr(static_cast<size_t>(all.size()) * kRowRuns);
+      DM_CK(c, cudaMemcpy(hm.data(), c->rt_meta.p, nt * sizeof(int4), cudaMemcpyDeviceToHost));
+      DM_CK(c, cudaMemcpy(hr.data(), c->rt_runs.p, hr.size() * sizeof(int2),
+                          cudaMemcpyDeviceToHost));
+      std::vector<uint8_t> blk(kRowCodeCap);
+      i64 next_e = 0;
+      for (i64 f = 0; f < nt; ++f) {
+        const int4 m = hm[static_cast<size_t>(f)];
+        DM_CK(c, cudaMemcpy(blk.data(), c->rcodes.p + 32 * static_cast<i64>(m.x), kRowCodeCap,
+                            cudaMemcpyDeviceToHost));
+        const int* h = reinterpret_cast<const int*>(blk.data());
+        const uint16_t* wo = reinterpret_cast<const uint16_t*>(h + 2);
+        int slots = 0;
+        bool ok = m.y > 0 && m.y <= kRowCodeCap && m.z > 0 && m.z <= kRowRuns && h[0] == next_e &&
+                  h[1] > 0 && h[1] <= kRowTile && wo[7] == m.y;
+        for (int r = 0; r < m.z && ok; ++r) {
+          const int2 x = hr[static_cast<size_t>(m.w) * kRowRuns + r];
+          ok = (x.x & 1) == 0 && (x.y & 0xffff) > 0 && (x.y >> 16) == slots;
+          slots += x.y & 0xffff;
+        }
+        ok = ok && slots <= kRowSlots;
+        if (!ok) {
+          std::fprintf(stderr, "[plan check] tile %lld: meta {%d %d %d %d} header e0 %d cnt %d "
+                       "(expected e0 %lld) slots %d\n", static_cast<long long>(f), m.x, m.y,
+                       m.z, m.w, h[0], h[1], static_cast<long long>(next_e), slots);
+          return fail(c, DM_ERR_CUDA, "row plan audit failed");
+        }
+        next_e = h[0] + h[1];
+      }
+      if (next_e != ne) return fail(c, DM_ERR_CUDA, "row plan audit: edges not covered");
+      std::fprintf(stderr, "[plan check] %lld row tiles ok\n", static_cast<long long>(nt));
+    }
   }
   c->rt_ntiles = nt;
   c->row_plan = true;
