@@ -16,11 +16,12 @@ CXXFLAGS := -O2 -fPIC -std=c++20 -ffp-contract=off -Iinclude
 
 CU_SRCS := $(CSRC)/capi.cu $(CSRC)/primitives.cu $(CSRC)/edges.cu $(CSRC)/navs.cu \
            $(CSRC)/volumes.cu $(CSRC)/verify.cu $(CSRC)/validate.cu $(CSRC)/tables.cu \
-           $(CSRC)/rings.cu $(CSRC)/rowplan.cu $(CSRC)/devgen.cu $(CSRC)/devmem.cu
+           $(CSRC)/rings.cu $(CSRC)/rowplan.cu $(CSRC)/devgen.cu $(CSRC)/devmem.cu $(CSRC)/hostio.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HDRS := $(wildcard $(CSRC)/*.cuh) include/dm_capi.h
 
-all: $(LIBDIR)/libdualmesh.so $(LIBDIR)/libdm_meshgen.so oracle tests/cpp/_build/libapi_probe.so
+all: $(LIBDIR)/libdualmesh.so $(LIBDIR)/libdm_meshgen.so oracle tests/cpp/_build/libapi_probe.so \
+     tools/_build/cpp_api_bench
 
 build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p build
@@ -47,6 +48,11 @@ $(LIBDIR)/libdm_meshgen.so: $(CSRC)/meshgen.cpp include/dm_meshgen.h
 tests/cpp/_build/libapi_probe.so: tests/cpp/api_probe.cpp $(LIBDIR)/libdualmesh.so include/dualmesh/mesh.hpp include/dualmesh/metrics.hpp include/dualmesh/io.hpp
 	@mkdir -p tests/cpp/_build
 	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(LIBDIR) -ldualmesh -Wl,-rpath,'$$ORIGIN/../../../$(LIBDIR)'
+
+# C++ API timing tool (bench.py reports it as extra.cpp_api)
+tools/_build/cpp_api_bench: tools/cpp_api_bench.cpp $(LIBDIR)/libdualmesh.so $(LIBDIR)/libdm_meshgen.so include/dualmesh/mesh.hpp include/dualmesh/metrics.hpp
+	@mkdir -p tools/_build
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(LIBDIR) -ldualmesh -ldm_meshgen -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
 oracle:
 	$(MAKE) -C oracle

@@ -2,6 +2,7 @@
 // context lifetime, mesh upload, result download, timing and plumbing.
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "dm_internal.cuh"
 
@@ -108,6 +109,7 @@ void dm_destroy(dm_ctx* c) {
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
   }
+  release_stage(c);
   delete c;
 }
 
@@ -135,15 +137,10 @@ int dm_set_mesh(dm_ctx* c, int dim, const double* coords, int64_t n_nodes, const
   DM_CK(c, c->coords.ensure(static_cast<size_t>(dim * (n_nodes + 2))));
   DM_CK(c, c->elems.ensure(static_cast<size_t>((dim + 1) * n_elements)));
   DM_CK(c, c->bnd.ensure(static_cast<size_t>(dim * n_boundary)));
-  if (n_nodes)
-    DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * dim * n_nodes,
-                             cudaMemcpyHostToDevice, c->stream));
-  if (n_elements)
-    DM_CK(c, cudaMemcpyAsync(c->elems.p, elements, sizeof(int32_t) * (dim + 1) * n_elements,
-                             cudaMemcpyHostToDevice, c->stream));
-  if (n_boundary)
-    DM_CK(c, cudaMemcpyAsync(c->bnd.p, boundary, sizeof(int32_t) * dim * n_boundary,
-                             cudaMemcpyHostToDevice, c->stream));
+  if (int st = copy_h2d(c, c->coords.p, coords, sizeof(double) * dim * n_nodes)) return st;
+  if (int st = copy_h2d(c, c->elems.p, elements, sizeof(int32_t) * (dim + 1) * n_elements))
+    return st;
+  if (int st = copy_h2d(c, c->bnd.p, boundary, sizeof(int32_t) * dim * n_boundary)) return st;
   int st = coords_changed(c);
   if (st) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
@@ -153,8 +150,7 @@ int dm_set_mesh(dm_ctx* c, int dim, const double* coords, int64_t n_nodes, const
 int dm_set_coords(dm_ctx* c, const double* coords) {
   if (!c || !coords) return DM_ERR_INVALID_ARG;
   if (c->dim == 0) return fail(c, DM_ERR_STATE, "dm_set_coords before dm_set_mesh");
-  DM_CK(c, cudaMemcpyAsync(c->coords.p, coords, sizeof(double) * c->dim * c->nv,
-                           cudaMemcpyHostToDevice, c->stream));
+  if (int st = copy_h2d(c, c->coords.p, coords, sizeof(double) * c->dim * c->nv)) return st;
   c->have_navs = c->have_vols = false;
   return coords_changed(c);
 }
@@ -181,19 +177,13 @@ int dm_get_edges(dm_ctx* c, int32_t* edges, uint64_t* origin_start) {
   if (!c) return DM_ERR_INVALID_ARG;
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
   if (edges && c->ne)
-    DM_CK(c, cudaMemcpyAsync(edges, c->edges.p, sizeof(int2) * c->ne, cudaMemcpyDeviceToHost,
-                             c->stream));
+    if (int st = copy_d2h(c, edges, c->edges.p, sizeof(int2) * c->ne)) return st;
   if (origin_start) {
     // widen the 32-bit device CSR to the reference's size_t (mesh.hpp:50)
-    std::uint32_t* tmp = nullptr;
-    DM_CK(c, cudaMallocHost(&tmp, sizeof(std::uint32_t) * (c->nv + 1)));
-    cudaError_t e = cudaMemcpyAsync(tmp, c->os.p, sizeof(std::uint32_t) * (c->nv + 1),
-                                    cudaMemcpyDeviceToHost, c->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    if (e == cudaSuccess)
-      for (int64_t v = 0; v <= c->nv; ++v) origin_start[v] = tmp[v];
-    cudaFreeHost(tmp);
-    DM_CK(c, e);
+    std::vector<std::uint32_t> tmp(static_cast<size_t>(c->nv + 1));
+    if (int st = copy_d2h(c, tmp.data(), c->os.p, sizeof(std::uint32_t) * (c->nv + 1)))
+      return st;
+    for (int64_t v = 0; v <= c->nv; ++v) origin_start[v] = tmp[static_cast<size_t>(v)];
   }
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
@@ -203,8 +193,7 @@ int dm_get_e2l(dm_ctx* c, int32_t* e2l) {
   if (!c || !e2l) return DM_ERR_INVALID_ARG;
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
   const int L = c->dim == 3 ? 6 : 3;
-  DM_CK(c, cudaMemcpyAsync(e2l, c->e2l.p, sizeof(int32_t) * L * c->nE, cudaMemcpyDeviceToHost,
-                           c->stream));
+  if (int st = copy_d2h(c, e2l, c->e2l.p, sizeof(int32_t) * L * c->nE)) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
 }
@@ -214,11 +203,9 @@ int dm_get_incidence(dm_ctx* c, int32_t* inc_ptr, int32_t* inc) {
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
   const int L = c->dim == 3 ? 6 : 3;
   if (inc_ptr)
-    DM_CK(c, cudaMemcpyAsync(inc_ptr, c->inc_ptr.p, sizeof(int32_t) * (c->ne + 1),
-                             cudaMemcpyDeviceToHost, c->stream));
+    if (int st = copy_d2h(c, inc_ptr, c->inc_ptr.p, sizeof(int32_t) * (c->ne + 1))) return st;
   if (inc && c->nE)
-    DM_CK(c, cudaMemcpyAsync(inc, c->inc.p, sizeof(int32_t) * L * c->nE, cudaMemcpyDeviceToHost,
-                             c->stream));
+    if (int st = copy_d2h(c, inc, c->inc.p, sizeof(int32_t) * L * c->nE)) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
 }
@@ -239,8 +226,7 @@ int dm_volumes(dm_ctx* c, int vol_algo) {
 int dm_get_navs(dm_ctx* c, double* navs) {
   if (!c || !navs) return DM_ERR_INVALID_ARG;
   if (!c->have_navs) return fail(c, DM_ERR_STATE, "navs not computed");
-  DM_CK(c, cudaMemcpyAsync(navs, c->navs.p, sizeof(double) * c->dim * c->ne,
-                           cudaMemcpyDeviceToHost, c->stream));
+  if (int st = copy_d2h(c, navs, c->navs.p, sizeof(double) * c->dim * c->ne)) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
 }
@@ -250,8 +236,7 @@ int dm_put_navs(dm_ctx* c, const double* navs) {
   if (!c->have_edges) return fail(c, DM_ERR_STATE, "edges not built");
   if (int w = wait_out_copies(c)) return w;
   DM_CK(c, c->navs.ensure(static_cast<size_t>(c->dim * c->ne)));
-  DM_CK(c, cudaMemcpyAsync(c->navs.p, navs, sizeof(double) * c->dim * c->ne,
-                           cudaMemcpyHostToDevice, c->stream));
+  if (int st = copy_h2d(c, c->navs.p, navs, sizeof(double) * c->dim * c->ne)) return st;
   DM_CK(c, c->svals.ensure(static_cast<size_t>(c->ne)));
   int st = svals_from_navs(c);
   c->svals_pos = false;
@@ -267,8 +252,7 @@ int dm_put_volumes(dm_ctx* c, const double* volumes) {
   if (c->dim == 0) return fail(c, DM_ERR_STATE, "no mesh");
   if (int w = wait_out_copies(c)) return w;
   DM_CK(c, c->vols.ensure(static_cast<size_t>(c->nv)));
-  DM_CK(c, cudaMemcpyAsync(c->vols.p, volumes, sizeof(double) * c->nv, cudaMemcpyHostToDevice,
-                           c->stream));
+  if (int st = copy_h2d(c, c->vols.p, volumes, sizeof(double) * c->nv)) return st;
   c->have_vols = true;
   return DM_OK;
 }
@@ -276,8 +260,7 @@ int dm_put_volumes(dm_ctx* c, const double* volumes) {
 int dm_get_volumes(dm_ctx* c, double* volumes) {
   if (!c || !volumes) return DM_ERR_INVALID_ARG;
   if (!c->have_vols) return fail(c, DM_ERR_STATE, "volumes not computed");
-  DM_CK(c, cudaMemcpyAsync(volumes, c->vols.p, sizeof(double) * c->nv, cudaMemcpyDeviceToHost,
-                           c->stream));
+  if (int st = copy_d2h(c, volumes, c->vols.p, sizeof(double) * c->nv)) return st;
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
 }

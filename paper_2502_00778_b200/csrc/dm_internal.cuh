@@ -255,6 +255,10 @@ struct dm_ctx {
   int out_slot = 0;
   dm::DevBuf<double> navs_alt, vols_alt;
 
+  // pinned staging buffers of the pageable host copies (hostio.cu)
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+
   // timing
   bool timing = false;
   cudaEvent_t ev[8] = {nullptr};
@@ -520,6 +524,14 @@ struct PlanClock {
     t = n;
   }
 };
+
+// hostio.cu: copies between device buffers and caller host memory on the ctx
+// stream -- pinned host memory directly, pageable memory chunked through two
+// pinned staging buffers with multi-threaded host copies.  copy_h2d returns
+// once `src` may be reused; copy_d2h once `dst` is filled.
+int copy_h2d(dm_ctx* c, void* dst, const void* src, size_t bytes);
+int copy_d2h(dm_ctx* c, void* dst, const void* src, size_t bytes);
+void release_stage(dm_ctx* c);
 
 // Read a device int flag (synchronises the stream).
 int read_flag(dm_ctx* c, int* value);

@@ -4,14 +4,25 @@
 //
 // Each host thread owns one dm_ctx (C-ABI threading rule).  The functions
 // are pure functions of their arguments, like the reference: every call
-// uploads the mesh it is given.  Status codes become exceptions here and
-// only here: DM_ERR_INVALID_ARG / MESH_EDGE_MISMATCH / EDGE_ABSENT ->
-// std::invalid_argument, everything else -> std::runtime_error.
+// takes the mesh it is given -- uploading it in full when its connectivity
+// differs from the resident one, only its coordinates otherwise (the edge
+// list, plan and derived CSRs stay on the device).  Status codes become
+// exceptions here and only here: DM_ERR_INVALID_ARG / MESH_EDGE_MISMATCH /
+// EDGE_ABSENT -> std::invalid_argument, everything else -> std::runtime_error.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <sys/mman.h>
+#include <initializer_list>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <utility>
+#include <vector>
 
 #include "dm_capi.h"
 #include "dualmesh/mesh.hpp"
@@ -20,10 +31,33 @@
 namespace dualmesh {
 namespace {
 
+// Per-thread context plus the topology it holds.  The functions are pure
+// functions of their arguments, like the reference, but consecutive calls on
+// one mesh (time stepping, a deforming grid, verify after metrics) share its
+// topology: a call whose connectivity fingerprint (dim, sizes, elements,
+// boundary) matches the resident one only refreshes the coordinates, keeping
+// the edge list, the ring plan and the derived CSRs on the device.  The
+// fingerprint is a full hash of the arrays (multi-threaded, ~10 ms for C5's
+// 1.6 GB), so a changed element is always seen.
+struct Topology {
+  bool valid = false;
+  int dim = 0;
+  std::size_t nv = 0, nE = 0, nB = 0;
+  std::uint64_t fp = 0;
+  bool edges_built = false;
+  std::uint64_t fp_edges = 0;  // fingerprint of an EdgeList verified equal to the device's
+};
+
 struct ThreadCtx {
   dm_ctx* c = nullptr;
+  Topology topo;
   ~ThreadCtx() { dm_destroy(c); }
 };
+
+ThreadCtx& tctx() {
+  thread_local ThreadCtx t;
+  return t;
+}
 
 void check(dm_ctx* c, int st, const char* what) {
   if (st == DM_OK) return;
@@ -34,7 +68,7 @@ void check(dm_ctx* c, int st, const char* what) {
 }
 
 dm_ctx* ctx() {
-  thread_local ThreadCtx t;
+  ThreadCtx& t = tctx();
   if (!t.c) {
     const char* dev = std::getenv("DUALMESH_DEVICE");
     int st = dm_create(&t.c, dev ? std::atoi(dev) : 0);
@@ -48,31 +82,155 @@ dm_ctx* ctx() {
   return t.c;
 }
 
+// env DUALMESH_API_TRACE=1: wall time of each phase of a call on stderr
+struct ApiTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  ApiTrace() {
+    const char* e = std::getenv("DUALMESH_API_TRACE");
+    on = e && e[0] == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[api] %-28s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
+// Sizes a result vector for n elements with its pages faulted in by all
+// cores first (transparent huge pages requested): resize() alone would fault
+// and zero ~3 GB of navs at C5 page by page on one thread (about 1 s).
+template <typename T>
+void sized(std::vector<T>& v, std::size_t n) {
+  v.clear();
+  v.reserve(n);
+  const std::size_t bytes = n * sizeof(T);
+  if (bytes >= (std::size_t(64) << 20)) {
+    auto* p = reinterpret_cast<unsigned char*>(v.data());
+    const std::size_t page = 4096;
+    const auto a = reinterpret_cast<std::uintptr_t>(p);
+    const std::uintptr_t lo = (a + (std::size_t(2) << 20) - 1) & ~((std::size_t(2) << 20) - 1);
+    if (lo < a + bytes) madvise(reinterpret_cast<void*>(lo), a + bytes - lo, MADV_HUGEPAGE);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t nt = std::min<std::size_t>(16, hw);
+    std::vector<std::thread> th;
+    for (std::size_t i = 0; i < nt; ++i)
+      th.emplace_back([=] {
+        const std::size_t b0 = bytes * i / nt, b1 = bytes * (i + 1) / nt;
+        for (std::size_t o = b0 & ~(page - 1); o < b1; o += page)
+          reinterpret_cast<volatile unsigned char*>(p)[o] = 0;
+      });
+    for (auto& t : th) t.join();
+  }
+  v.resize(n);
+}
+
+// 64-bit fingerprint of byte ranges: per-slice multiply-xorshift chains over
+// 8-byte words on up to 16 threads, combined in slice order.
+std::uint64_t fingerprint(std::initializer_list<std::pair<const void*, std::size_t>> parts) {
+  std::uint64_t h = 0x9E3779B97F4A7C15ull;
+  for (const auto& [ptr, bytes] : parts) {
+    const auto* p = static_cast<const unsigned char*>(ptr);
+    const std::size_t nw = bytes / 8;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t nt = bytes < (std::size_t(8) << 20) ? 1 : std::min<std::size_t>(16, hw);
+    std::vector<std::uint64_t> part(nt, 0);
+    auto run = [&](std::size_t i) {
+      const std::size_t a = nw * i / nt, b = nw * (i + 1) / nt;
+      std::uint64_t x = 0xD6E8FEB86659FD93ull ^ i;
+      for (std::size_t w = a; w < b; ++w) {
+        std::uint64_t v;
+        std::memcpy(&v, p + 8 * w, 8);
+        x = (x ^ v) * 0x9E3779B97F4A7C15ull;
+        x ^= x >> 29;
+      }
+      part[i] = x;
+    };
+    std::vector<std::thread> th;
+    for (std::size_t i = 1; i < nt; ++i) th.emplace_back(run, i);
+    run(0);
+    for (auto& t : th) t.join();
+    for (std::size_t i = 0; i < nt; ++i) h = (h ^ part[i]) * 0xC2B2AE3D27D4EB4Full;
+    std::uint64_t tail = bytes;
+    for (std::size_t k = 8 * nw; k < bytes; ++k) tail = tail * 131 + p[k];
+    h = (h ^ tail) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 31;
+  }
+  return h;
+}
+
 dm_ctx* upload(const Mesh& m) {
   dm_ctx* c = ctx();
   if (m.dim != 2 && m.dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+  Topology& T = tctx().topo;
+  ApiTrace tr;
+  const std::size_t nv = m.num_nodes(), nE = m.num_elements(), nB = m.num_boundary();
+  const std::uint64_t fp =
+      fingerprint({{&m.dim, sizeof(m.dim)},
+                   {m.elements.data(), m.elements.size() * sizeof(Index)},
+                   {m.boundary.data(), m.boundary.size() * sizeof(Index)}});
+  tr.mark("upload: fingerprint");
+  if (T.valid && T.dim == m.dim && T.nv == nv && T.nE == nE && T.nB == nB && T.fp == fp) {
+    check(c, dm_set_coords(c, m.coords.data()), "dm_set_coords");  // same topology
+    tr.mark("upload: coordinates");
+    return c;
+  }
+  T.valid = false;
   check(c,
-        dm_set_mesh(c, m.dim, m.coords.data(), static_cast<int64_t>(m.num_nodes()),
-                    m.elements.data(), static_cast<int64_t>(m.num_elements()), m.boundary.data(),
-                    static_cast<int64_t>(m.num_boundary())),
+        dm_set_mesh(c, m.dim, m.coords.data(), static_cast<int64_t>(nv), m.elements.data(),
+                    static_cast<int64_t>(nE), m.boundary.data(), static_cast<int64_t>(nB)),
         "dm_set_mesh");
+  T = Topology{true, m.dim, nv, nE, nB, fp, false, 0};
+  tr.mark("upload: mesh");
   return c;
 }
 
-// Upload + GPU edge extraction, then confirm the caller's EdgeList is the
-// one this mesh produces ("mesh/edge mismatch").
+// The resident topology's edge list (built once per topology).
+int64_t ensure_edges(dm_ctx* c) {
+  Topology& T = tctx().topo;
+  int64_t ne = 0;
+  if (!T.edges_built) {
+    check(c, dm_build_edges(c, &ne), "dm_build_edges");
+    T.edges_built = true;
+    T.fp_edges = 0;
+  } else {
+    dm_device_view v;
+    check(c, dm_device_views(c, &v), "dm_device_views");
+    ne = v.n_edges;
+  }
+  return ne;
+}
+
+std::uint64_t edgelist_fp(const EdgeList& l) {
+  return fingerprint({{l.edges.data(), l.edges.size() * sizeof(l.edges[0])},
+                      {l.origin_start.data(), l.origin_start.size() * sizeof(std::size_t)}});
+}
+
+// Upload (or refresh) + the resident edge list, then confirm the caller's
+// EdgeList is the one this mesh produces ("mesh/edge
+// mismatch"): compared element by element the first time a list is seen for
+// this topology, by fingerprint afterwards.
 dm_ctx* upload_with_edges(const Mesh& m, const EdgeList& given) {
   dm_ctx* c = upload(m);
-  int64_t ne = 0;
-  check(c, dm_build_edges(c, &ne), "dm_build_edges");
+  const int64_t ne = ensure_edges(c);
   if (static_cast<std::size_t>(ne) != given.size() ||
       given.origin_start.size() != m.num_nodes() + 1)
     throw std::invalid_argument("mesh/edge mismatch");
+  Topology& T = tctx().topo;
+  const std::uint64_t fp = edgelist_fp(given);
+  if (T.fp_edges != 0 && fp == T.fp_edges) return c;
   std::vector<int32_t> e(2 * static_cast<std::size_t>(ne));
-  check(c, dm_get_edges(c, e.data(), nullptr), "dm_get_edges");
+  std::vector<uint64_t> os(m.num_nodes() + 1);
+  check(c, dm_get_edges(c, e.data(), os.data()), "dm_get_edges");
   for (std::size_t i = 0; i < given.size(); ++i)
     if (e[2 * i] != given.edges[i][0] || e[2 * i + 1] != given.edges[i][1])
       throw std::invalid_argument("mesh/edge mismatch");
+  for (std::size_t v = 0; v < os.size(); ++v)
+    if (os[v] != given.origin_start[v]) throw std::invalid_argument("mesh/edge mismatch");
+  T.fp_edges = fp;
   return c;
 }
 
@@ -103,14 +261,20 @@ Index EdgeList::edge_of(Index a, Index b) const {
 
 EdgeList build_edges(const Mesh& mesh) {
   dm_ctx* c = upload(mesh);
-  int64_t ne = 0;
-  check(c, dm_build_edges(c, &ne), "dm_build_edges");
+  ApiTrace tr;
+  const int64_t ne = ensure_edges(c);
+  tr.mark("build_edges: K1");
   EdgeList out;
-  out.edges.resize(static_cast<std::size_t>(ne));
-  std::vector<uint64_t> os(mesh.num_nodes() + 1);
-  check(c, dm_get_edges(c, reinterpret_cast<int32_t*>(out.edges.data()), os.data()),
+  sized(out.edges, static_cast<std::size_t>(ne));
+  sized(out.origin_start, mesh.num_nodes() + 1);
+  tr.mark("build_edges: allocate");
+  static_assert(sizeof(std::size_t) == sizeof(uint64_t), "origin_start is 64-bit");
+  check(c, dm_get_edges(c, reinterpret_cast<int32_t*>(out.edges.data()),
+                        reinterpret_cast<uint64_t*>(out.origin_start.data())),
         "dm_get_edges");
-  out.origin_start.assign(os.begin(), os.end());
+  tr.mark("build_edges: copy out");
+  tctx().topo.fp_edges = edgelist_fp(out);  // this exact list needs no re-verification
+  tr.mark("build_edges: fingerprint");
   return out;
 }
 
@@ -256,16 +420,21 @@ std::vector<bool> boundary_node_mask(const Mesh& mesh) {
 // ---------------------------------------------------------------- metrics.hpp
 namespace {
 LumpedNavField fetch_navs(dm_ctx* c, const Mesh& mesh, std::size_t ne) {
+  ApiTrace tr;
   LumpedNavField f;
   f.dim = mesh.dim;
-  f.navs.resize(ne * static_cast<std::size_t>(mesh.dim));
+  sized(f.navs, ne * static_cast<std::size_t>(mesh.dim));
+  tr.mark("navs: allocate");
   check(c, dm_get_navs(c, f.navs.data()), "dm_get_navs");
+  tr.mark("navs: compute + copy out");
   return f;
 }
 DualVolumeField fetch_vols(dm_ctx* c, const Mesh& mesh) {
+  ApiTrace tr;
   DualVolumeField v;
-  v.volumes.resize(mesh.num_nodes());
+  sized(v.volumes, mesh.num_nodes());
   check(c, dm_get_volumes(c, v.volumes.data()), "dm_get_volumes");
+  tr.mark("volumes: allocate + copy out");
   return v;
 }
 void put_navs(dm_ctx* c, const Mesh& mesh, const EdgeList& edges, const LumpedNavField& navs) {

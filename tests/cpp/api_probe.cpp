@@ -125,18 +125,29 @@ int64_t probe_io(const char* in_path, const char* mesh_out, const char* metrics_
 }
 
 // mesh/edge mismatch must raise std::invalid_argument.
+// A foreign EdgeList must throw std::invalid_argument ("mesh/edge mismatch"),
+// whether it differs in size or, with the same size, in one entry (the
+// topology and its own list resident, so only the content check can see it).
 int probe_mismatch(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne) {
   auto m = make(dim, x, nv, el, ne, nullptr, 0);
   auto l = dualmesh::build_edges(m);
-  l.edges.pop_back();
-  try {
-    dualmesh::lumped_navs_dualfree(m, l);
-  } catch (const std::invalid_argument&) {
-    return 1;
-  } catch (...) {
-    return 2;
+  (void)dualmesh::lumped_navs_dualfree(m, l);  // the genuine list is accepted
+  auto shorter = l;
+  shorter.edges.pop_back();
+  auto altered = l;
+  altered.edges[altered.size() / 2][1] = altered.edges[altered.size() / 2][1] + 1;
+  int thrown = 0;
+  for (const auto* bad : {&shorter, &altered}) {
+    try {
+      dualmesh::lumped_navs_dualfree(m, *bad);
+    } catch (const std::invalid_argument&) {
+      ++thrown;
+      continue;
+    } catch (...) {
+      return 2;
+    }
   }
-  return 0;
+  return thrown == 2 ? 1 : 0;
 }
 
 double probe_element_volume(int dim, const double* x, int64_t nv, const int32_t* el, int64_t ne,

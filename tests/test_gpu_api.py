@@ -194,3 +194,37 @@ def test_file_io_cpp_api(probe, tmp_path):
     bad = tmp_path / "bad.dm"
     bad.write_text("dualmesh v1\ndim 2\nnodes 1\n0 0\nelements 1\n1 1 2\n")
     assert probe.probe_io(str(bad).encode(), str(out).encode(), str(met).encode()) == -1
+
+
+def test_topology_cache_sequence(probe, oracle):
+    """The C++ API keeps one topology resident per thread: calls on the same
+    connectivity refresh coordinates only, any change of the element or
+    boundary arrays (same sizes included) is seen and rebuilds.  Every call of
+    a mixed sequence must equal the oracle on that call's mesh."""
+    p = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    base = meshgen.baseline_config("C2", 4)
+    rng = np.random.default_rng(3)
+    inner = (base.coords > 0) * (base.coords < 1)
+    moved = Mesh(3, base.coords + rng.uniform(-1e-3, 1e-3, base.coords.size) * inner,
+                 base.elements, base.boundary)
+    el = base.elements.reshape(-1, 4)
+    perm = rng.permutation(el.shape[0])
+    permuted = Mesh(3, base.coords, el[perm].ravel().copy(), base.boundary)
+    rot = el.copy()
+    rot[5] = rot[5][[1, 2, 0, 3]]  # even permutation: same orientation, other local order
+    rotated = Mesh(3, base.coords, rot.ravel().copy(), base.boundary)
+    for m in (base, moved, moved, permuted, base, rotated, rotated, base):
+        e, o = oracle.build_edges(m)
+        want = oracle.navs_dualfree(m, e, o)
+        navs, vols = np.empty(want.size), np.empty(m.num_nodes())
+        cl, tv = C.c_double(), C.c_double()
+        st = probe.probe_compute_metrics(*_a(m), p(m.boundary, C.c_int32), m.num_boundary(), 1,
+                                         0, p(navs, C.c_double), p(vols, C.c_double),
+                                         C.byref(cl), C.byref(tv))
+        assert st == 0
+        w = want.reshape(-1, 3)
+        den = np.maximum(np.abs(w).max(axis=1), 1e-300)
+        assert (np.abs(navs.reshape(-1, 3) - w).max(axis=1) / den).max() <= 1e-12
+        vw = oracle.volumes_edge(m, e, want)
+        assert np.abs(vols - vw).max() <= 1e-12 * np.abs(vw).max()
+    assert probe.probe_mismatch(*_a(base)) == 1  # a foreign EdgeList still throws
