@@ -64,7 +64,7 @@ class CopyPool {
 
  private:
   void slice(int i) {
-    const size_t per = (len_ / n_ + 63) & ~size_t(63);
+    const size_t per = ((len_ + n_ - 1) / n_ + 63) & ~size_t(63);  // n_ slices cover len_
     const size_t a = std::min(len_, per * static_cast<size_t>(i));
     const size_t b = std::min(len_, a + per);
     if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
