@@ -191,12 +191,19 @@ int64_t dm_kernel_launches(const dm_ctx* ctx);
 /* Which element-loop kernels the plan enables: info[0] ring path built (1: Morton
  * tiles, rings.cu; 2: row tiles, rowplan.cu),
  * [1] ring path usable, [2] row tables built, [3] row tables usable,
- * [4] max tile node count (ring path), [5] failure bits of the ring build (2: a tile
- * touches > 1536 nodes, 4: an edge has > 24 incident elements, 8: non-manifold fan,
- * 16: inconsistently oriented fan, 32: ring codes beyond 64 GB),
+ * [4] max tile node count (ring path), [5] ring-build bits (2: a Morton tile
+ * touches > 1536 nodes and 32: ring codes beyond 64 GB disable the ring path;
+ * 4: an edge has > 24 incident elements, 8: a non-manifold fan, 16: an
+ * inconsistently oriented fan send those edges to the side list),
  * [6] edge-volume pass walks nodes in Morton order (1) or id order (0),
  * [7] tile tables recoloured against bank conflicts (env DUALMESH_PLAN_COLOR=1). */
 int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
+/* Edges of the ring path's side list (*n): those the ring codes cannot
+ * describe -- more than 24 incident elements, a non-manifold or inconsistently
+ * oriented fan -- evaluated from their element list inside the same dm_navs
+ * call (0 when the ring path is not in use).  [5] of dm_plan_info gives the
+ * reasons (4 / 8 / 16). */
+int dm_plan_side_edges(dm_ctx* ctx, int64_t* n);
 /* SPEC cli_io file formats, host only (no device needed).
  * MeshFile: dm_mesh_file_read parses `path` (call with NULL arrays for the
  * sizes first); ids come back 0-based; *has_boundary = 0 when the file has no

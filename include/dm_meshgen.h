@@ -54,6 +54,16 @@ int dmg_permute(int dim, int64_t n_nodes, int64_t n_elements, int64_t n_boundary
 
 /* Returns the index of the first non-positive element (signed volume on the
  * generated coordinates) or -1: the post-hoc inversion check of SPEC.md:336. */
+/* Seeded random 2-3 flips of a valid tet mesh (n_nodes < 2^31): interior
+ * faces abc shared by (a,b,c,d) and (a,b,c,e) whose segment d-e pierces abc
+ * become (a,b,d,e), (b,c,d,e), (c,a,d,e); visited in splitmix64(seed)
+ * shuffled order, each tet in at most one flip, slivers (< 1e-3 of the mean
+ * new volume) skipped, at most max_flips flips.  out_elements (4 *
+ * (n_elements + max_flips) ids) gets the flipped mesh, positively oriented;
+ * returns the number of flips (elements: n_elements + flips), or -1. */
+int64_t dmg_flip23(int64_t n_nodes, const double* coords, int64_t n_elements,
+                   const int32_t* elements, int64_t max_flips, uint64_t seed,
+                   int32_t* out_elements);
 int64_t dmg_first_inverted(int dim, int64_t n_elements, const double* coords,
                            const int32_t* elements);
 

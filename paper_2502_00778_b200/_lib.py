@@ -94,6 +94,7 @@ CAPI = {
     "dm_get_timings": (C.c_int, [P, FP, C.c_int]),
     "dm_kernel_launches": (C.c_int64, [P]),
     "dm_plan_info": (C.c_int, [P, I64P]),
+    "dm_plan_side_edges": (C.c_int, [P, I64P]),
     "dm_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(P)]),
     "dm_mesh_file_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), I64P, I64P, I64P,
                                     C.POINTER(C.c_int), DP, I32P, I32P, C.c_char_p, C.c_int64]),
@@ -113,6 +114,7 @@ MESHGEN = {
     "dmg_bl_z": (C.c_int, [C.c_int, dbl, dbl, DP]),
     "dmg_permute": (C.c_int, [C.c_int, i64, i64, i64, u64, u64, DP, I32P, I32P]),
     "dmg_first_inverted": (C.c_int64, [C.c_int, i64, DP, I32P]),
+    "dmg_flip23": (C.c_int64, [i64, DP, i64, I32P, i64, u64, I32P]),
 }
 
 _cache: dict[str, C.CDLL] = {}

@@ -36,6 +36,7 @@ void drop_derived(dm_ctx* c) {
   c->ne = 0;
   c->n_bedge = 0;
   c->n_derived = 0;
+  c->n_side = 0;
 }
 
 // Writers of navs / volumes on the compute stream wait for the pipelined
@@ -384,6 +385,12 @@ int dm_plan_info(dm_ctx* c, int64_t info[8]) {
   info[5] = c->ring_fail;
   info[6] = c->vol_by_rank;
   info[7] = c->plan_colored;
+  return DM_OK;
+}
+
+int dm_plan_side_edges(dm_ctx* c, int64_t* n) {
+  if (!c || !n) return DM_ERR_INVALID_ARG;
+  *n = c->have_rings && c->ring_ok ? c->n_side : 0;
   return DM_OK;
 }
 

@@ -208,6 +208,12 @@ struct dm_ctx {
   dm::i64 n_bseg = 0;              // boundary edges (segments of bedge_p)
   dm::DevBuf<int4> bseg;           // per boundary edge {e, j, k, p}
   dm::DevBuf<dm::u32> bseg_start;  // its facets: bedge_p[bseg_start[i] .. bseg_start[i+1])
+  // side list of the ring path: edges the ring codes cannot describe (more
+  // than kRingMax incidences, a non-manifold or inconsistently oriented fan)
+  // as {edge id, position}; the ring kernels give them a zero row and
+  // k_navs_side recomputes them from the element list inside the same step
+  dm::DevBuf<int2> side;
+  dm::i64 n_side = 0;
   // row-tile plan (rowplan.cu), chosen over the Morton tiles for node
   // numberings whose id-contiguous edge ranges have small node tables
   bool row_plan = false;
@@ -306,6 +312,7 @@ constexpr int kTileNodeCap = 1536;
 constexpr int kTileFillRanks = 256;
 constexpr int kTileFillSlots = 512;
 constexpr int kRingMax = 24;
+constexpr int kSideCap = 1 << 20;  // side-list entries (more: the ring plan is not used)
 // Row-tile plan (rowplan.cu): tiles are contiguous edge-id ranges of at most
 // kRowTile edges (7 warps) whose node table -- node-id runs copied straight
 // from the caller's coordinates -- holds at most kRowSlots records.

@@ -45,7 +45,8 @@ struct Coords<2> {
 // Dual-free 3D: the
 // unscaled cross product 2*n_j^E of the face opposite the origin j, with the
 // face vertex order of tet_opposite_face (ref mesh.cpp:15,103-110).
-__device__ __forceinline__ void df3(const Coords<3>& X, int v0, int v1, int v2, int v3, int ij,
+template <typename CX>
+__device__ __forceinline__ void df3(const CX& X, int v0, int v1, int v2, int v3, int ij,
                                     double& c0, double& c1, double& c2) {
   const unsigned f = (kOppPacked >> (6 * ij)) & 63u;
   const d4 p0 = X[sel4(v0, v1, v2, v3, f & 3)];
@@ -96,7 +97,8 @@ __device__ __forceinline__ void tr3_core(const d4& x0, const d4& x1, const d4& x
   }
 }
 
-__device__ __forceinline__ void tr3(const Coords<3>& X, int v0, int v1, int v2, int v3, int ij,
+template <typename CX>
+__device__ __forceinline__ void tr3(const CX& X, int v0, int v1, int v2, int v3, int ij,
                                     int ik, double& c0, double& c1, double& c2) {
   const d4 x0 = X[v0], x1 = X[v1], x2 = X[v2], x3 = X[v3];
   const unsigned rest = 0xFu & ~((1u << ij) | (1u << ik));

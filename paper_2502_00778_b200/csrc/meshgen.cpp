@@ -5,6 +5,8 @@
 // libdm_meshgen.so so CPU-only tests can use it without touching CUDA.
 #include "dm_meshgen.h"
 
+#include <algorithm>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <utility>
@@ -234,6 +236,87 @@ int dmg_permute(int dim, int64_t n_nodes, int64_t n_elements, int64_t n_boundary
       for (int a = 0; a < npe; ++a) elements[npe * perm[e] + a] = el[npe * e + a];
   }
   return 0;
+}
+
+// Seeded random 2-3 flips: a generator of genuinely unstructured tetrahedral
+// topology (ring lengths 3..10+) from any valid tet mesh.  Two tets (a,b,c,d)
+// and (a,b,c,e) sharing the interior face abc become (a,b,d,e), (b,c,d,e),
+// (c,a,d,e) when the segment d-e pierces abc (the three new volumes have one
+// sign); conformity is kept (the union's boundary faces are unchanged).
+// Interior faces are visited in a splitmix64(seed) shuffled order and a tet
+// takes part in at most one flip; at most max_flips flips.  Writes
+// n_elements + flips tets to out_elements (first the originals in place,
+// flipped pairs rewritten, then the third tets appended), all positively
+// oriented; returns the number of flips.
+int64_t dmg_flip23(int64_t n_nodes, const double* x, int64_t n_elements, const int32_t* el,
+                   int64_t max_flips, uint64_t seed, int32_t* out) {
+  if (n_nodes < 0 || n_elements < 0 || !x || !el || !out || n_nodes >= (int64_t(1) << 31))
+    return -1;
+  // faces keyed by their sorted node triple (32 bits each)
+  using Key = unsigned __int128;
+  std::vector<std::pair<Key, int64_t>> f;
+  f.reserve(static_cast<std::size_t>(4 * n_elements));
+  for (int64_t e = 0; e < n_elements; ++e)
+    for (int o = 0; o < 4; ++o) {
+      int v[3], q = 0;
+      for (int a = 0; a < 4; ++a)
+        if (a != o) v[q++] = el[4 * e + a];
+      std::sort(v, v + 3);
+      const Key key = static_cast<Key>(static_cast<uint32_t>(v[0])) << 64 |
+                      static_cast<Key>(static_cast<uint32_t>(v[1])) << 32 |
+                      static_cast<Key>(static_cast<uint32_t>(v[2]));
+      f.push_back({key, 4 * e + o});
+    }
+  std::sort(f.begin(), f.end());
+  std::vector<std::pair<int64_t, int64_t>> inner;  // (tet*4+opposite local) pairs
+  for (std::size_t i = 0; i + 1 < f.size(); ++i)
+    if (f[i].first == f[i + 1].first) inner.push_back({f[i].second, f[i + 1].second});
+  SplitMix64 r(seed);
+  for (std::size_t i = inner.size(); i > 1; --i)
+    std::swap(inner[i - 1], inner[static_cast<std::size_t>(r.next() % i)]);
+  std::copy(el, el + 4 * n_elements, out);
+  std::vector<uint8_t> used(static_cast<std::size_t>(n_elements), 0);
+  auto vol = [&](int a, int b, int c, int d) {
+    const double* p = x + 3 * static_cast<int64_t>(a);
+    const double* q = x + 3 * static_cast<int64_t>(b);
+    const double* s = x + 3 * static_cast<int64_t>(c);
+    const double* t = x + 3 * static_cast<int64_t>(d);
+    const double u0 = q[0] - p[0], u1 = q[1] - p[1], u2 = q[2] - p[2];
+    const double v0 = s[0] - p[0], v1 = s[1] - p[1], v2 = s[2] - p[2];
+    const double w0 = t[0] - p[0], w1 = t[1] - p[1], w2 = t[2] - p[2];
+    return (u1 * v2 - u2 * v1) * w0 + (u2 * v0 - u0 * v2) * w1 + (u0 * v1 - u1 * v0) * w2;
+  };
+  int64_t flips = 0, next = n_elements;
+  for (const auto& [fa, fb] : inner) {
+    if (flips >= max_flips) break;
+    const int64_t t1 = fa >> 2, t2 = fb >> 2;
+    if (used[t1] || used[t2]) continue;
+    const int d = el[4 * t1 + (fa & 3)], e = el[4 * t2 + (fb & 3)];
+    int abc[3], q = 0;
+    for (int a = 0; a < 4; ++a)
+      if (a != (fa & 3)) abc[q++] = el[4 * t1 + a];
+    const int tri[3][2] = {{abc[0], abc[1]}, {abc[1], abc[2]}, {abc[2], abc[0]}};
+    double vs[3];
+    for (int k = 0; k < 3; ++k) vs[k] = vol(tri[k][0], tri[k][1], d, e);
+    const bool pos = vs[0] > 0 && vs[1] > 0 && vs[2] > 0;
+    const bool neg = vs[0] < 0 && vs[1] < 0 && vs[2] < 0;
+    if (!pos && !neg) continue;  // d-e misses the face: no valid 2-3 flip
+    // reject slivers: each new volume at least 1e-3 of the pair's mean
+    const double total = std::abs(vs[0]) + std::abs(vs[1]) + std::abs(vs[2]);
+    if (std::min({std::abs(vs[0]), std::abs(vs[1]), std::abs(vs[2])}) < 1e-3 * total / 3) continue;
+    used[t1] = used[t2] = 1;
+    int32_t* slots[3] = {out + 4 * t1, out + 4 * t2, out + 4 * next};
+    for (int k = 0; k < 3; ++k) {
+      int32_t* t = slots[k];
+      t[0] = tri[k][0];
+      t[1] = tri[k][1];
+      t[2] = pos ? d : e;
+      t[3] = pos ? e : d;
+    }
+    ++next;
+    ++flips;
+  }
+  return flips;
 }
 
 int64_t dmg_first_inverted(int dim, int64_t n_elements, const double* x, const int32_t* el) {

@@ -876,6 +876,47 @@ __global__ void __launch_bounds__(kRowTile, MINB)
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------------------------ side list of the ring path
+// Edges the ring codes cannot describe (rings.cu / rowplan.cu side list:
+// more than kRingMax incidences, non-manifold or inconsistently oriented
+// fans): one thread per edge folds its incident elements in ascending id --
+// the serial loop's order, so these rows are bitwise the oracle's -- and
+// overwrites the zero row the ring kernel wrote; the boundary pass follows.
+template <int ALGO>
+__global__ void __launch_bounds__(128)
+    k_navs_side(const int2* __restrict__ side, i64 n, const int2* __restrict__ edges,
+                const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+                const int32_t* __restrict__ el, Coords3R X, double* __restrict__ navs,
+                double* __restrict__ svals) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 sp = side[i];  // {edge id, s position}
+  const int e = sp.x;
+  const int2 jk = edges[e];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int q = inc_ptr[e]; q < inc_ptr[e + 1]; ++q) {
+    const int4 t = __ldg(reinterpret_cast<const int4*>(el) + inc[q]);
+    const int ij = t.x == jk.x ? 0 : (t.y == jk.x ? 1 : (t.z == jk.x ? 2 : 3));
+    double c0, c1, c2;
+    if constexpr (ALGO == kDualFree) {
+      df3(X, t.x, t.y, t.z, t.w, ij, c0, c1, c2);
+    } else {
+      const int ik = t.x == jk.y ? 0 : (t.y == jk.y ? 1 : (t.z == jk.y ? 2 : 3));
+      tr3(X, t.x, t.y, t.z, t.w, ij, ik, c0, c1, c2);
+    }
+    acc[0] += c0;
+    acc[1] += c1;
+    acc[2] += c2;
+  }
+  double nv[3], s;
+  edge_tail_values<3, ALGO>(Coords<3>{nullptr}, e, acc, X[jk.x], X[jk.y], nullptr, 0u, 0u, nullptr,
+                            nv, s);
+  navs[3 * static_cast<i64>(e)] = nv[0];
+  navs[3 * static_cast<i64>(e) + 1] = nv[1];
+  navs[3 * static_cast<i64>(e) + 2] = nv[2];
+  svals[sp.y] = s;
+}
+
 // ------------------------------------------------------------------ GATHER_FACES
 // One thread per edge.  x_j, x_k live in registers; the thread walks its own
 // slice of the face-list incidence in ascending element order, U entries at
@@ -1143,6 +1184,10 @@ int launch_navs(dm_ctx* c, int variant) {
       if (ALGO == kTraditional) st = launch(k_navs_row<kTraditional, 2>);
       else st = launch(k_navs_row<kDualFree, 5>);  // 56 registers, 5 x 35 KB shared
       if (st) return st;
+      if (c->n_side > 0)
+        DM_LAUNCH(c, k_navs_side<ALGO>, grid_for(c->n_side, 128), 128, 0, c->side.p, c->n_side,
+                  c->edges.p, c->inc_ptr.p, c->inc.p, c->elems.p, Coords3R{c->coords.p},
+                  c->navs.p, c->svals.p);
     }
     tmark(c, 1);
     if constexpr (D == 3 && ALGO == kDualFree) {
@@ -1188,6 +1233,10 @@ int launch_navs(dm_ctx* c, int variant) {
         st = launch(k_navs_ring_pipe<512, 4, 2, kDualFree, 1, 2>, sizeof(PipeSmem<512>));
       }
       if (st) return st;
+      if (c->n_side > 0)
+        DM_LAUNCH(c, k_navs_side<ALGO>, grid_for(c->n_side, 128), 128, 0, c->side.p, c->n_side,
+                  c->edges.p, c->inc_ptr.p, c->inc.p, c->elems.p, Coords3R{c->coords.p},
+                  c->navs.p, c->svals.p);
     }
     tmark(c, 1);
     if constexpr (D == 3 && ALGO == kDualFree) {

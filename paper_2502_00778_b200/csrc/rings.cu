@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kTileEdges)
     const int2 jk = edges[e];
     insert(rank[jk.x]);
     insert(rank[jk.y]);
-    for (int q = inc_ptr[e]; q < inc_ptr[e + 1]; ++q) {
+    const int nq = inc_ptr[e + 1] - inc_ptr[e];  // side-list edges need only j, k
+    for (int q = inc_ptr[e]; q < (nq > kRingMax ? inc_ptr[e] : inc_ptr[e + 1]); ++q) {
       const int4 v = reinterpret_cast<const int4*>(el)[inc[q]];
       const int vs[4] = {v.x, v.y, v.z, v.w};
       for (int a = 0; a < 4; ++a)
@@ -159,7 +160,8 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
                              const int32_t* __restrict__ rank, const uint8_t* __restrict__ bmark,
                              const int32_t* __restrict__ tnodes, const u32* __restrict__ tcnt,
                              const u32* __restrict__ wstart, i64 ne,
-                             uint8_t* __restrict__ rcodes, int* __restrict__ flag) {
+                             uint8_t* __restrict__ rcodes, int* __restrict__ flag,
+                             int2* __restrict__ side) {
   const i64 p = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= ne) return;
   const int e = eperm[p];
@@ -182,12 +184,24 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
     const int sl = tslot(list, nl, rank[v]);
     put(2 + step, (W == 2 && step == 0) ? (sl | (bmark[e] ? 0x8000u : 0u)) : sl);
   });
-  if (r.fail) {
-    atomicOr(flag, r.fail);
-    return;
-  }
   // closed: the last ring slot repeats slot(m_0) (word-0 bit 14 / header bit 7)
   const int sj = tslot(list, nl, rank[j]), sk = tslot(list, nl, rank[k]);
+  if (r.fail) {  // side list: an empty ring (m_0 := k), k_navs_side recomputes the edge
+    if constexpr (W == 2) {
+      put(0, sj);
+      put(1, sk);
+      put(2, sk | (bmark[e] ? 0x8000u : 0u));
+    } else {
+      put(0, sj);
+      put(1, sk);
+      put(2, sk);
+      blk[p & 31] = static_cast<uint8_t>(bmark[e] ? 64 : 0);
+    }
+    atomicOr(flag, r.fail);
+    const int q = atomicAdd(flag + 2, 1);
+    if (q < kSideCap) side[q] = make_int2(e, static_cast<int>(p));
+    return;
+  }
   if constexpr (W == 2) {
     put(0, sj | (r.sign < 0 ? 0x8000u : 0u) | (r.closed ? 0x4000u : 0u));
     put(1, sk | n << 11);
@@ -210,7 +224,8 @@ __global__ void k_ring_warpsize(const int32_t* __restrict__ eperm,
   int S = 3;
   for (i64 p = w * 32; p < w * 32 + 32 && p < ne; ++p) {
     const int e = eperm[p];
-    S = max(S, inc_ptr[e + 1] - inc_ptr[e] + 3);
+    const int n = inc_ptr[e + 1] - inc_ptr[e];
+    S = max(S, (n > kRingMax ? 0 : n) + 3);  // side-list edges: 3 steps
   }
   wsize[w] = static_cast<u32>(W == 2 ? 2 * S : S + 1);  // 32-byte units
 }
@@ -854,6 +869,8 @@ int ensure_rings(dm_ctx* c) {
   }
   // row tiles first (rowplan.cu): contiguous edge ranges whose tables fit
   c->row_plan = false;
+  c->n_side = 0;
+  c->ring_fail = 0;
   if (int sr = try_row_plan(c)) return sr;
   clk.mark("row plan");
   if (c->row_plan) {
@@ -862,7 +879,6 @@ int ensure_rings(dm_ctx* c) {
     c->vol_by_rank = false;
     c->plan_colored = false;
     c->ring_max_nodes = kRowSlots;
-    c->ring_fail = 0;
     c->have_rings = true;
     return DM_OK;
   }
@@ -885,7 +901,9 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, cudaMemsetAsync(c->tnode_cnt.p, 0, ntiles * sizeof(u32), c->stream));
   DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(2 * ntiles)));
   DM_CK(c, c->flag.ensure(4));
-  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 3 * sizeof(int), c->stream));
+  DM_CK(c, c->side.ensure(kSideCap));
+  c->n_side = 0;
   ScratchBuf<int32_t> rank(c->arena, arena_block(c));
   ScratchBuf<uint8_t> bmark(c->arena, arena_block(c));
   DM_CK(c, rank.ensure(c->nv));
@@ -936,11 +954,11 @@ int ensure_rings(dm_ctx* c) {
   if (c->code_width == 1)
     DM_LAUNCH(c, k_ring_codes<1>, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p,
               c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p,
-              wstart.p, ne, c->rcodes.p, c->flag.p);
+              wstart.p, ne, c->rcodes.p, c->flag.p, c->side.p);
   else
     DM_LAUNCH(c, k_ring_codes<2>, grid_for(ne, 128), 128, 0, c->edges.p, c->eperm.p,
               c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, bmark.p, c->tnodes.p, c->tnode_cnt.p,
-              wstart.p, ne, c->rcodes.p, c->flag.p);
+              wstart.p, ne, c->rcodes.p, c->flag.p, c->side.p);
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
             c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
   clk.mark("ring codes");
@@ -956,12 +974,15 @@ int ensure_rings(dm_ctx* c) {
       c->plan_colored = true;
     }
   }
-  int fl[2] = {0, 0};
+  int fl[3] = {0, 0, 0};
   DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
   c->ring_fail = fl[0];
   c->ring_max_nodes = fl[1];
-  c->ring_ok = (fl[0] == 0);
+  // edges the rings cannot describe ride the side list; only an oversized
+  // tile table (bit 2) or an overfull side list disables the ring path
+  c->n_side = fl[2];
+  c->ring_ok = (fl[0] & 2) == 0 && fl[2] <= kSideCap;
   c->have_rings = true;
   clk.mark("colouring");
   return DM_OK;  // the Morton-order coordinates are staged by every navs call

@@ -51,7 +51,6 @@ constexpr int kRTCodeUnits = kRowCodeCap / 32;
 constexpr int kRTTooManyNodes = 1;
 constexpr int kRTTooManyRuns = 2;
 constexpr int kRTTooManyCodes = 4;
-constexpr int kRTRingTooLong = 8;
 
 struct RTShared {
   int hs[kRTHash];
@@ -140,7 +139,9 @@ __global__ void __launch_bounds__(kRTThreads)
     const int pb = inc_ptr[e];
     n_inc = inc_ptr[e + 1] - pb;
     int last = -1;
-    for (int q = 0; q < n_inc; ++q) {  // the ring nodes: the two others of each element
+    // the ring nodes: the two others of each element (a side-list edge, more
+    // than kRingMax incidences, needs only j and k in the table)
+    for (int q = 0; q < (n_inc > kRingMax ? 0 : n_inc); ++q) {
       const int4 v = reinterpret_cast<const int4*>(el)[inc[pb + q]];
       const int vs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -157,7 +158,6 @@ __global__ void __launch_bounds__(kRTThreads)
   __syncthreads();
   const int nu = S.n_uniq;
   int badbits = nu > kRTUniqCap ? kRTTooManyNodes : 0;
-  if (__syncthreads_or(t < cnt && n_inc > kRingMax)) badbits |= kRTRingTooLong;
   if (badbits) {
     if (t == 0) bad[p] = static_cast<uint8_t>(badbits);
     return;
@@ -196,7 +196,10 @@ __global__ void __launch_bounds__(kRTThreads)
   const unsigned kq = S.key[t];
   const int q = static_cast<int>(kq & 0xffu);
   const int e = e0 + q;
-  if (t < cnt) atomicMax(&S.wmax[t >> 5], inc_ptr[e + 1] - inc_ptr[e] + 3);
+  if (t < cnt) {
+    const int n = inc_ptr[e + 1] - inc_ptr[e];
+    atomicMax(&S.wmax[t >> 5], (n > kRingMax ? 0 : n) + 3);  // side edges: 3 steps
+  }
   __syncthreads();
   if (S.nruns > kRowRuns) badbits |= kRTTooManyRuns;
   else if (S.nslots > kRowSlots) badbits |= kRTTooManyNodes;
@@ -231,12 +234,16 @@ __global__ void __launch_bounds__(kRTThreads)
 
 // Ring codes (k_rt_build has written the tile header and each lane's edge
 // offset): one CTA per tile, the runs in shared memory, one thread per lane.
+// An edge the walk cannot encode (more than kRingMax incidences, a
+// non-manifold or inconsistently oriented fan) gets an empty ring (header n =
+// 0, slots j, k, k: the kernel writes a zero row) and goes to the side list
+// {e, e}; flag[0] collects the kRing* reasons, flag[1] counts the list.
 __global__ void __launch_bounds__(kRowTile)
     k_rt_codes(const int* __restrict__ order, const int2* __restrict__ edges,
                const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
                const int32_t* __restrict__ el, const int2* __restrict__ runs,
                const int* __restrict__ nruns, uint8_t* __restrict__ codes,
-               int* __restrict__ flag) {
+               int* __restrict__ flag, int2* __restrict__ side) {
   __shared__ int2 R[kRowRuns];
   const int t = threadIdx.x, lane = t & 31;
   const i64 p = order[blockIdx.x];
@@ -264,12 +271,21 @@ __global__ void __launch_bounds__(kRowTile)
     miss |= sl < 0;
     blk[64 + (2 + step) * 32 + lane] = static_cast<uint8_t>(sl);
   });
-  if (rw.fail || miss) {
-    atomicOr(flag, rw.fail | (miss ? 1 : 0));
+  const int sj = slot(jk.x), sk = slot(jk.y);
+  if (sj < 0 || sk < 0) {  // cannot happen for a plan built from this edge list
+    atomicOr(flag, 1);
     return;
   }
-  blk[64 + lane] = static_cast<uint8_t>(slot(jk.x));
-  blk[64 + 32 + lane] = static_cast<uint8_t>(slot(jk.y));
+  blk[64 + lane] = static_cast<uint8_t>(sj);
+  blk[64 + 32 + lane] = static_cast<uint8_t>(sk);
+  if (rw.fail || miss) {
+    blk[64 + 64 + lane] = static_cast<uint8_t>(sk);  // m_0 := k, no ring steps
+    blk[lane] = 0;
+    atomicOr(flag, rw.fail | (miss ? 64 : 0));
+    const int q = atomicAdd(flag + 1, 1);
+    if (q < kSideCap) side[q] = make_int2(e, e);
+    return;
+  }
   blk[lane] = static_cast<uint8_t>(n | (rw.sign < 0 ? 32 : 0) | (rw.closed ? 128 : 0));
 }
 
@@ -359,7 +375,7 @@ int try_row_plan(dm_ctx* c) {
       if (!hb[static_cast<size_t>(i)]) continue;
       ++nbad;
       const int2 tl = all[static_cast<size_t>(base + i)];
-      if ((hb[static_cast<size_t>(i)] & kRTRingTooLong) || tl.y < 2) return DM_OK;  // Morton plan
+      if (tl.y < 2) return DM_OK;  // one edge does not fit: Morton plan
       const int h = tl.y >= 4 ? (tl.y / 2 + 1) & ~1 : 1;  // even splits keep e0 even
       child[static_cast<size_t>(base + i)] = static_cast<int>(all.size());
       all.push_back(make_int2(tl.x, h));
@@ -397,17 +413,19 @@ int try_row_plan(dm_ctx* c) {
   DM_CK(c, cudaMemcpyAsync(dorder.p, order.data(), nt * sizeof(int), cudaMemcpyHostToDevice,
                            c->stream));
   DM_CK(c, c->rt_meta.ensure(static_cast<size_t>(nt)));
+  DM_CK(c, c->side.ensure(kSideCap));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
   DM_LAUNCH(c, k_rt_codes, static_cast<unsigned>(nt), kRowTile, 0, dorder.p, c->edges.p,
-            c->inc_ptr.p, c->inc.p, c->elems.p, c->rt_runs.p, nruns.p, c->rcodes.p, c->flag.p);
+            c->inc_ptr.p, c->inc.p, c->elems.p, c->rt_runs.p, nruns.p, c->rcodes.p, c->flag.p,
+            c->side.p);
   DM_LAUNCH(c, k_rt_meta, grid_for(nt, 256), 256, 0, dorder.p, nruns.p, bytes.p, nt, c->rt_meta.p);
   {
-    int fl = 0;
-    DM_CK(c, cudaMemcpyAsync(&fl, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    int fl[2] = {0, 0};
+    DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
     DM_CK(c, cudaStreamSynchronize(c->stream));
-    if (fl) {  // a fan the walk cannot encode: the Morton plan reports it
-      c->ring_fail = fl;
-      return DM_OK;
-    }
+    if ((fl[0] & 1) || fl[1] > kSideCap) return DM_OK;  // not for this plan: Morton tiles
+    c->ring_fail = fl[0];  // reasons the side list exists (informational)
+    c->n_side = fl[1];
   }
   clk.mark("row tiles: codes");
   // boundary pass lists: positions are edge ids

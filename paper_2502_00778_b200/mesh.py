@@ -365,6 +365,12 @@ class Engine:
                 "volume_order": "morton" if info[6] else "node",
                 "colored": bool(info[7])}
 
+    def side_edges(self) -> int:
+        """Edges of the ring path's side list (dm_plan_side_edges)."""
+        n = C.c_int64()
+        self._ck(self._lib.dm_plan_side_edges(self._c, C.byref(n)), "dm_plan_side_edges")
+        return n.value
+
     def launches(self) -> int:
         return int(self._lib.dm_kernel_launches(self._c))
 

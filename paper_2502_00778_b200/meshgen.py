@@ -71,6 +71,53 @@ def permute(mesh: Mesh, node_seed: int = SEED_NODES, elem_seed: int = SEED_ELEMS
     return Mesh(mesh.dim, x, el, bd)
 
 
+SEED_FLIPS = 46
+
+
+def flip23(mesh: Mesh, fraction: float = 0.3, seed: int = SEED_FLIPS) -> Mesh:
+    """Seeded random 2-3 flips (dmg_flip23) of up to `fraction` * n_elements / 2
+    tet pairs: non-Kuhn, unstructured topology (ring lengths 3..10+) on the
+    same nodes and boundary, node numbering kept."""
+    assert mesh.dim == 3
+    ne = mesh.num_elements()
+    mx = int(fraction * ne / 2)
+    out = np.empty(4 * (ne + mx), np.int32)
+    nf = _lib.meshgen().dmg_flip23(mesh.num_nodes(), ptr(mesh.coords, C.c_double), ne,
+                                   ptr(mesh.elements, C.c_int32), mx, seed, ptr(out, C.c_int32))
+    if nf < 0:
+        raise ValueError("dmg_flip23: invalid mesh arrays")
+    return Mesh(3, mesh.coords, out[:4 * (ne + nf)].copy(), mesh.boundary)
+
+
+def fan_in(mesh: Mesh, n: int = 30) -> Mesh:
+    """`mesh` plus a disjoint fan of n tets around one edge (placed beside the
+    unit box): one edge with n incidences (n > 24 leaves the ring encoding)
+    inside an otherwise regular grid."""
+    th = 2 * np.pi * np.arange(n) / n
+    ring = np.stack([1.5 + 0.2 * np.cos(th), 0.5 + 0.2 * np.sin(th), np.full(n, 0.5)], 1)
+    xf = np.concatenate([[[1.5, 0.5, 0.3], [1.5, 0.5, 0.7]], ring])
+    b = mesh.num_nodes()
+    el, bd = [], []
+    for i in range(n):
+        t = [0, 1, 2 + i, 2 + (i + 1) % n]
+        p = xf[t]
+        if np.linalg.det(np.stack([p[1] - p[0], p[2] - p[0], p[3] - p[0]])) < 0:
+            t[2], t[3] = t[3], t[2]
+        el += [b + v for v in t]
+        # outward facets: the two faces of each tet not containing the edge (0,1)
+        for o in (0, 1):
+            f = [v for k, v in enumerate(t) if k != o]
+            q = xf[f]
+            nrm = np.cross(q[1] - q[0], q[2] - q[0])
+            cen = xf[t].mean(0)
+            if np.dot(nrm, q[0] - cen) < 0:
+                f[1], f[2] = f[2], f[1]
+            bd += [b + v for v in f]
+    return Mesh(3, np.concatenate([mesh.coords, xf.ravel()]),
+                np.concatenate([mesh.elements, np.array(el, np.int32)]),
+                np.concatenate([mesh.boundary, np.array(bd, np.int32)]))
+
+
 def first_inverted(mesh: Mesh) -> int:
     return int(_lib.meshgen().dmg_first_inverted(mesh.dim, mesh.num_elements(),
                                                  ptr(mesh.coords, C.c_double),

@@ -354,7 +354,7 @@ def _fan_mesh(n):
 
 @pytest.mark.parametrize("n", [12, 30, 50, 1500])
 def test_fan_fallback(engine, oracle, n):
-    """Fans around one edge: n > 24 incidences per edge leave the ring path;
+    """Fans around one edge: n > 24 incidences per edge go to the side list;
     n = 50 sorts node 0's 150 K1 keys in the CTA bitonic path, n = 1500 its
     4500 keys (> 4096) in the per-segment radix-sort path."""
     m0 = _fan_mesh(n)
@@ -364,7 +364,8 @@ def test_fan_fallback(engine, oracle, n):
     engine.build_edges()
     engine.navs(DF, GATHER)
     info = engine.plan_info()
-    assert info["ring_ok"] == (n <= 24)
+    # the fan's hub edge rides the ring path's side list; the ring path stays
+    assert info["ring_ok"] and engine.side_edges() == (1 if n > 24 else 0)
     e, o = oracle.build_edges(m)
     got = engine.edges()
     np.testing.assert_array_equal(got.edges, e)
@@ -703,3 +704,68 @@ def test_row_and_morton_plans_same_bits(name, scale, monkeypatch, oracle):
     e, o = oracle.build_edges(m)
     want = oracle.navs_dualfree(m, e, o)
     assert per_vector_rel(out[0][0], want, 3) <= 1e-12
+
+
+@pytest.mark.parametrize("name,scale,flag", [("C3", 4, "1"), ("C2", 2, "1"), ("C2", 2, "0")])
+def test_side_list_inside_grid(name, scale, flag, monkeypatch, oracle):
+    """One 30-tet fan beside a BASELINE grid (meshgen.fan_in): only its hub
+    edge leaves the ring codes (side list, evaluated in element order inside
+    the same step -- that row bitwise the serial oracle's); every other edge
+    stays on the ring path (row tiles, or Morton tiles for the randomly
+    numbered C3 / with DUALMESH_ROW_PLAN=0)."""
+    from paper_2502_00778_b200 import Engine
+    monkeypatch.setenv("DUALMESH_ROW_PLAN", flag)
+    m = meshgen.fan_in(meshgen.baseline_config(name, scale), 30)
+    eng = Engine(0)
+    try:
+        eng.set_mesh(m)
+        eng.build_edges()
+        eng.navs(DF, GATHER)
+        info = eng.plan_info()
+        assert info["ring_ok"] and eng.side_edges() == 1 and info["ring_fail_bits"] & 4
+        assert info["tiles"] == ("row" if flag == "1" and name != "C3" else "morton")
+        e, o = oracle.build_edges(m)
+        want = oracle.navs_dualfree(m, e, o)
+        got = eng.get_navs()
+        assert per_vector_rel(got, want, 3) <= 1e-12
+        hub = int(np.argmax(np.diff(oracle.edge_maps(m, e, o)[1])))
+        np.testing.assert_array_equal(got.reshape(-1, 3)[hub], want.reshape(-1, 3)[hub])
+        eng.volumes(EDGE)
+        vw = oracle.volumes_edge(m, e, want)
+        assert np.abs(eng.get_volumes() - vw).max() <= 1e-12 * np.abs(vw).max()
+        r, _ = eng.check_closure()
+        assert r <= 1e-13
+        eng.navs(TR, GATHER)
+        assert per_vector_rel(eng.get_navs(), oracle.navs_traditional(m, e, o), 3) <= 1e-12
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("permuted", [False, True])
+def test_flipped_unstructured_grid(engine, oracle, permuted):
+    """Non-Kuhn topology (meshgen.flip23: seeded 2-3 flips of C2, ring
+    lengths 1..11): the ring path (row tiles; Morton tiles when the numbering
+    is permuted) within 1e-12 of the oracle, the exact variant bitwise, the
+    SPEC identities."""
+    m = meshgen.flip23(meshgen.baseline_config("C2", 2), 0.3)
+    if permuted:
+        m = meshgen.permute(m)
+    engine.set_mesh(m)
+    engine.build_edges()
+    engine.navs(DF, GATHER)
+    info = engine.plan_info()
+    assert info["ring_ok"] and info["tiles"] == ("morton" if permuted else "row")
+    e, o = oracle.build_edges(m)
+    want = oracle.navs_dualfree(m, e, o)
+    assert per_vector_rel(engine.get_navs(), want, 3) <= 1e-12
+    engine.volumes(EDGE)
+    vw = oracle.volumes_edge(m, e, want)
+    assert np.abs(engine.get_volumes() - vw).max() <= 1e-12 * np.abs(vw).max()
+    r, ri = engine.check_closure()
+    assert r <= 1e-13 and ri <= 1e-13
+    rel, sv, _ = engine.check_total_volume()
+    assert rel <= 1e-12 and abs(sv - 1.0) <= 1e-12
+    engine.navs(DF, EXACT)
+    np.testing.assert_array_equal(engine.get_navs(), want)
+    engine.navs(TR, GATHER)
+    assert per_vector_rel(engine.get_navs(), oracle.navs_traditional(m, e, o), 3) <= 1e-12

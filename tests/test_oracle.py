@@ -275,3 +275,29 @@ def test_oracle_generator_equals_product_generator(oracle, n):
     assert np.array_equal(a.elements, b.elements)
     assert np.array_equal(a.boundary, b.boundary)
     assert oracle.max_element_volume(a) > 0
+
+
+def test_flip23_generator_is_valid(oracle):
+    """meshgen.flip23: a conforming, positively oriented non-Kuhn grid (the
+    reference's own validate_mesh when oracle/_ref is built), with ring
+    lengths spread well beyond the Kuhn 4 / 6, exact closure and volume."""
+    m = meshgen.flip23(meshgen.tet_cube(8, amp=0.15), 0.3)
+    assert m.num_elements() > 6 * 8 ** 3
+    assert meshgen.first_inverted(m) == -1
+    if ref_available():
+        n, msgs, _ = RefMesh(m).validate()
+        assert n == 0, msgs[:3]
+    e, o = oracle.build_edges(m)
+    ring = np.diff(oracle.edge_maps(m, e, o)[1])
+    assert ring.max() >= 8 and (ring == 3).sum() > 0
+    nv = oracle.navs_dualfree(m, e, o)
+    assert oracle.check_closure(m, e, nv)[0] <= 1e-13
+    assert oracle.check_total_volume(m, oracle.volumes_edge(m, e, nv))[0] <= 1e-12
+
+
+def test_fan_in_is_valid():
+    m = meshgen.fan_in(meshgen.tet_cube(4, amp=0.15), 30)
+    assert meshgen.first_inverted(m) == -1
+    if ref_available():
+        n, msgs, _ = RefMesh(m).validate()
+        assert n == 0, msgs[:3]
