@@ -882,39 +882,56 @@ __global__ void __launch_bounds__(kRowTile, MINB)
 // fans): one thread per edge folds its incident elements in ascending id --
 // the serial loop's order, so these rows are bitwise the oracle's -- and
 // overwrites the zero row the ring kernel wrote; the boundary pass follows.
+// A warp per edge: lane q evaluates incidences q, q + 32, ... (all loads in
+// flight at once), lane 0 then adds the terms in incidence order.
 template <int ALGO>
 __global__ void __launch_bounds__(128)
     k_navs_side(const int2* __restrict__ side, i64 n, const int2* __restrict__ edges,
                 const int32_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
-                const int32_t* __restrict__ el, Coords3R X, double* __restrict__ navs,
-                double* __restrict__ svals) {
-  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int2 sp = side[i];  // {edge id, s position}
+                const int32_t* __restrict__ el, Coords3R X, bool pos_s,
+                double* __restrict__ navs, double* __restrict__ svals) {
+  __shared__ double term[4][32][3];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const i64 i = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;  // warp-uniform
+  const int2 sp = side[i];  // {edge id, position}
   const int e = sp.x;
   const int2 jk = edges[e];
+  const int q0 = inc_ptr[e], q1 = inc_ptr[e + 1];
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int q = inc_ptr[e]; q < inc_ptr[e + 1]; ++q) {
-    const int4 t = __ldg(reinterpret_cast<const int4*>(el) + inc[q]);
-    const int ij = t.x == jk.x ? 0 : (t.y == jk.x ? 1 : (t.z == jk.x ? 2 : 3));
-    double c0, c1, c2;
-    if constexpr (ALGO == kDualFree) {
-      df3(X, t.x, t.y, t.z, t.w, ij, c0, c1, c2);
-    } else {
-      const int ik = t.x == jk.y ? 0 : (t.y == jk.y ? 1 : (t.z == jk.y ? 2 : 3));
-      tr3(X, t.x, t.y, t.z, t.w, ij, ik, c0, c1, c2);
+  for (int b = q0; b < q1; b += 32) {
+    const int q = b + lane;
+    if (q < q1) {
+      const int4 t = __ldg(reinterpret_cast<const int4*>(el) + inc[q]);
+      const int ij = t.x == jk.x ? 0 : (t.y == jk.x ? 1 : (t.z == jk.x ? 2 : 3));
+      double c0, c1, c2;
+      if constexpr (ALGO == kDualFree) {
+        df3(X, t.x, t.y, t.z, t.w, ij, c0, c1, c2);
+      } else {
+        const int ik = t.x == jk.y ? 0 : (t.y == jk.y ? 1 : (t.z == jk.y ? 2 : 3));
+        tr3(X, t.x, t.y, t.z, t.w, ij, ik, c0, c1, c2);
+      }
+      term[w][lane][0] = c0;
+      term[w][lane][1] = c1;
+      term[w][lane][2] = c2;
     }
-    acc[0] += c0;
-    acc[1] += c1;
-    acc[2] += c2;
+    __syncwarp();
+    if (lane == 0)
+      for (int r = 0; r < 32 && b + r < q1; ++r) {
+        acc[0] += term[w][r][0];
+        acc[1] += term[w][r][1];
+        acc[2] += term[w][r][2];
+      }
+    __syncwarp();
   }
+  if (lane != 0) return;
   double nv[3], s;
   edge_tail_values<3, ALGO>(Coords<3>{nullptr}, e, acc, X[jk.x], X[jk.y], nullptr, 0u, 0u, nullptr,
                             nv, s);
   navs[3 * static_cast<i64>(e)] = nv[0];
   navs[3 * static_cast<i64>(e) + 1] = nv[1];
   navs[3 * static_cast<i64>(e) + 2] = nv[2];
-  svals[sp.y] = s;
+  svals[pos_s ? static_cast<i64>(sp.y) : static_cast<i64>(e)] = s;
 }
 
 // ------------------------------------------------------------------ GATHER_FACES
@@ -1184,10 +1201,11 @@ int launch_navs(dm_ctx* c, int variant) {
       if (ALGO == kTraditional) st = launch(k_navs_row<kTraditional, 2>);
       else st = launch(k_navs_row<kDualFree, 5>);  // 56 registers, 5 x 35 KB shared
       if (st) return st;
-      if (c->n_side > 0)
-        DM_LAUNCH(c, k_navs_side<ALGO>, grid_for(c->n_side, 128), 128, 0, c->side.p, c->n_side,
-                  c->edges.p, c->inc_ptr.p, c->inc.p, c->elems.p, Coords3R{c->coords.p},
-                  c->navs.p, c->svals.p);
+      if (c->n_side > 0)  // one warp per side-list edge
+        DM_LAUNCH(c, k_navs_side<ALGO>, grid_for(32 * c->n_side, 128), 128, 0, c->side.p,
+                  c->n_side, c->edges.p, c->inc_ptr.p, c->inc.p, c->elems.p,
+                  Coords3R{c->coords.p}, c->row_plan ? false : c->vol_by_rank, c->navs.p,
+                  c->svals.p);
     }
     tmark(c, 1);
     if constexpr (D == 3 && ALGO == kDualFree) {
@@ -1233,10 +1251,11 @@ int launch_navs(dm_ctx* c, int variant) {
         st = launch(k_navs_ring_pipe<512, 4, 2, kDualFree, 1, 2>, sizeof(PipeSmem<512>));
       }
       if (st) return st;
-      if (c->n_side > 0)
-        DM_LAUNCH(c, k_navs_side<ALGO>, grid_for(c->n_side, 128), 128, 0, c->side.p, c->n_side,
-                  c->edges.p, c->inc_ptr.p, c->inc.p, c->elems.p, Coords3R{c->coords.p},
-                  c->navs.p, c->svals.p);
+      if (c->n_side > 0)  // one warp per side-list edge
+        DM_LAUNCH(c, k_navs_side<ALGO>, grid_for(32 * c->n_side, 128), 128, 0, c->side.p,
+                  c->n_side, c->edges.p, c->inc_ptr.p, c->inc.p, c->elems.p,
+                  Coords3R{c->coords.p}, c->row_plan ? false : c->vol_by_rank, c->navs.p,
+                  c->svals.p);
     }
     tmark(c, 1);
     if constexpr (D == 3 && ALGO == kDualFree) {

@@ -340,7 +340,9 @@ int try_row_plan(dm_ctx* c) {
   const i64 n0 = (ne + kRowTile - 1) / kRowTile;
   // provisional tiles: the level-0 ranges p < n0, then the halves of tiles
   // that did not fit, appended level by level (about 2 % of tiles at C5)
-  const i64 cap = n0 + n0 / 4 + 1024;
+  double split_max = 1.25;  // tiles after splitting / (ne / kRowTile), env DUALMESH_ROW_SPLIT_MAX
+  if (const char* sm = std::getenv("DUALMESH_ROW_SPLIT_MAX")) split_max = std::atof(sm);
+  const i64 cap = static_cast<i64>(split_max * static_cast<double>(n0)) + 1024;
   ScratchBuf<int2> cand(c->arena, rt_block(c));
   ScratchBuf<uint8_t> bad(c->arena, rt_block(c));
   ScratchBuf<int> nruns(c->arena, rt_block(c)), bytes(c->arena, rt_block(c));
@@ -383,8 +385,9 @@ int try_row_plan(dm_ctx* c) {
       child.push_back(-1);
       child.push_back(-1);
     }
-    if (level == 0 && nbad * 4 > n0) return DM_OK;  // tables too large: Morton plan
-    if (static_cast<i64>(all.size()) > cap) return DM_OK;
+    if (level == 0 && static_cast<double>(nbad) > (split_max - 1.0) * static_cast<double>(n0))
+      return DM_OK;  // tables too large: Morton plan
+    if (static_cast<i64>(all.size()) > cap) return DM_OK;  // (cap: the split budget below)
     base = next;
     np = static_cast<i64>(all.size()) - next;
     DM_CK(c, cand.ensure(np > 0 ? np : 1));
@@ -407,7 +410,7 @@ int try_row_plan(dm_ctx* c) {
     }
   }
   const i64 nt = static_cast<i64>(order.size());
-  if (nt * 4 > n0 * 5) return DM_OK;
+  if (static_cast<double>(nt) > split_max * static_cast<double>(n0)) return DM_OK;
   ScratchBuf<int> dorder(c->arena, rt_block(c));
   DM_CK(c, dorder.ensure(nt));
   DM_CK(c, cudaMemcpyAsync(dorder.p, order.data(), nt * sizeof(int), cudaMemcpyHostToDevice,
