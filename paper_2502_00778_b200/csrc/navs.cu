@@ -20,9 +20,11 @@
 //   GATHER_ELEM: the same fold through the element-id CSR (inc) and a
 //       dependent connectivity gather per incidence (kept for comparison).
 //   SCATTER: one thread per element, fp64 atomics (REDG.E.ADD.F64) through
-//       e2l into zeroed navs, then the same per-edge tail; summation order
-//       varies run to run (<=1e-12 parity, not deterministic).
+//       e2l into zeroed navs, aggregated per warp over lanes hitting the same
+//       edge, then the same per-edge tail; summation order varies run to run
+//       (<=1e-12 parity, not deterministic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "geometry.cuh"
 
@@ -1081,6 +1083,55 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Warp-aggregated form (north_star (b)): for each local edge slot l the 32
+// lanes (consecutive elements, which share many edges: the six Kuhn tets of a
+// hex all hold its diagonal) group by edge id with __match_any_sync; the
+// lowest lane of a group adds the group's terms (lane order) and issues one
+// REDG.E.ADD.F64 per component for all of them.
+template <int D, int ALGO>
+__global__ void __launch_bounds__(256)
+    k_navs_scatter_agg(const int32_t* __restrict__ el, Coords<D> X, i64 nE,
+                       const int32_t* __restrict__ e2l, double* __restrict__ navs) {
+  __shared__ double term[8][32][D];
+  const i64 E = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool valid = E < nE;
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  constexpr int L = D == 3 ? 6 : 3;
+  int v[4];
+  if constexpr (D == 3) {
+    const int4 t4 = ld_i4(reinterpret_cast<const int4*>(el) + E);
+    v[0] = t4.x; v[1] = t4.y; v[2] = t4.z; v[3] = t4.w;
+  } else {
+    v[0] = __ldg(el + 3 * E); v[1] = __ldg(el + 3 * E + 1); v[2] = __ldg(el + 3 * E + 2); v[3] = 0;
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const unsigned pk = D == 3 ? (kTetEdgePacked >> (4 * l)) : (kTriEdgePacked >> (4 * l));
+    const int a = v[pk & 3], b = v[(pk >> 2) & 3];
+    const int j = a < b ? a : b, k = a < b ? b : a;
+    double c[3];
+    contribution<D, ALGO>(X, el, static_cast<int>(E), j, k, c);
+    const int id = __ldg(e2l + L * E + l);
+    const unsigned grp = __match_any_sync(act, id);
+#pragma unroll
+    for (int d = 0; d < D; ++d) term[w][lane][d] = c[d];
+    __syncwarp(act);
+    if ((grp & ((1u << lane) - 1)) == 0) {  // group leader
+      double s[3] = {0.0, 0.0, 0.0};
+      for (unsigned g = grp; g; g &= g - 1) {
+        const int r = __ffs(g) - 1;
+#pragma unroll
+        for (int d = 0; d < D; ++d) s[d] += term[w][r][d];
+      }
+#pragma unroll
+      for (int d = 0; d < D; ++d) atomicAdd(navs + D * static_cast<i64>(id) + d, s[d]);
+    }
+    __syncwarp(act);
+  }
+}
+
 template <int D, int ALGO>
 __global__ void __launch_bounds__(kEB)
     k_edge_finalize(const int2* __restrict__ edges, Coords<D> X, i64 ne,
@@ -1169,8 +1220,18 @@ int launch_navs(dm_ctx* c, int variant) {
   if (variant == DM_VARIANT_SCATTER) {
     tmark(c, 0);
     DM_CK(c, cudaMemsetAsync(c->navs.p, 0, sizeof(double) * D * ne, c->stream));
-    DM_LAUNCH(c, (k_navs_scatter<D, ALGO>), grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE,
-              c->e2l.p, c->navs.p);
+    // warp-aggregated atomics by default; DUALMESH_SCATTER_PLAIN=1: one
+    // atomic per term (the ncu comparison in profiles/)
+    static const bool plain = [] {
+      const char* e = std::getenv("DUALMESH_SCATTER_PLAIN");
+      return e && e[0] == '1';
+    }();
+    if (plain)
+      DM_LAUNCH(c, (k_navs_scatter<D, ALGO>), grid_for(c->nE, 256), 256, 0, c->elems.p, X, c->nE,
+                c->e2l.p, c->navs.p);
+    else
+      DM_LAUNCH(c, (k_navs_scatter_agg<D, ALGO>), grid_for(c->nE, 256), 256, 0, c->elems.p, X,
+                c->nE, c->e2l.p, c->navs.p);
     tmark(c, 1);
     DM_LAUNCH(c, (k_edge_finalize<D, ALGO>), tiles, kEB, 0, c->edges.p, X, ne, c->bedge.p,
               c->tile_bptr.p, c->bnd.p, c->navs.p, c->svals.p);
