@@ -450,6 +450,23 @@ def run_ours(args, world, rank, local, dist):
     kernel_bytes = B["elem"]
     achieved = kernel_bytes / (elem_ms / 1e3) / 1e9
     step_achieved = B["metrics"] / (ms_step / 1e3) / 1e9
+    # each kernel against the bytes its own design moves,
+    # beside the canonical SURVEY 8(d) bytes above
+    D, nv = mesh.dim, mesh.num_nodes()
+    pb = eng.plan_bytes()
+    design = {}
+    if pb["tiles"]:
+        d_elem = (pb["codes"] + pb["meta_runs"] + 8 * D * nv + 8 * D * ne + 8 * ne)
+        design["element_loop"] = {
+            "bytes": d_elem, "ms": elem_ms, "frac": d_elem / (elem_ms / 1e3) / 1e9 / peak,
+            "parts": {"ring_codes": pb["codes"], "tile_meta_runs": pb["meta_runs"],
+                      "coords_once": 8 * D * nv, "navs_rows": 8 * D * ne, "s_terms": 8 * ne},
+            "table_fill_from_l2_or_hbm": pb["table_fill"],
+            "note": "row tiles: codes + run descriptors + coordinates once + navs + s"}
+    d_vol = 4 * (nv + 1) + 4 * ne + 4 * (nv + 1) + 8 * ne + 8 * nv
+    design["volumes"] = {"bytes": d_vol, "ms": kvol_ms,
+                         "frac": d_vol / (kvol_ms / 1e3) / 1e9 / peak,
+                         "note": "in_ptr + in_list + origin CSR + s once + V"}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "latest_traffic.json")
     if os.path.exists(prof):
@@ -505,10 +522,13 @@ def run_ours(args, world, rank, local, dist):
                              f"{B['metrics'] / 1e9:.2f} GB algorithmic per step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_navs_ring_pipe (K2 dual-free element loop, scale pass "
-                                   "and s_e fused)",
+                         "kernel": ("k_navs_row (K2 dual-free element loop on row tiles, "
+                                    "scale pass and s_e fused)" if pb["tiles"] else
+                                    "k_navs_ring_pipe (K2 dual-free element loop on Morton "
+                                    "tiles, scale pass and s_e fused)"),
                          "bytes_per_launch": kernel_bytes, "ms_per_launch": elem_ms,
                          "peak_source": peak_kind},
+            "design_roofline": design,
             "step_roofline": {"achieved": step_achieved, "frac": step_achieved / peak,
                               "bytes_per_step": B["metrics"], "unit": "GB/s",
                               "nav_ms": nav_ms, "vol_ms": vol_ms,

@@ -204,6 +204,12 @@ int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
  * call (0 when the ring path is not in use).  [5] of dm_plan_info gives the
  * reasons (4 / 8 / 16). */
 int dm_plan_side_edges(dm_ctx* ctx, int64_t* n);
+/* Per-step streams of the row-tile element loop (zeros for other plans):
+ * out[0] ring-code bytes, [1] node-table fill bytes (24 B per table slot, from
+ * L2 or HBM), [2] tile metadata + run descriptor bytes, [3] tiles.  With the
+ * navs / s rows written and the coordinates read once, these are the bytes
+ * the kernel's design moves (bench.py design_roofline). */
+int dm_plan_bytes(dm_ctx* ctx, int64_t out[4]);
 /* SPEC cli_io file formats, host only (no device needed).
  * MeshFile: dm_mesh_file_read parses `path` (call with NULL arrays for the
  * sizes first); ids come back 0-based; *has_boundary = 0 when the file has no

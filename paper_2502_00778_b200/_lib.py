@@ -95,6 +95,7 @@ CAPI = {
     "dm_kernel_launches": (C.c_int64, [P]),
     "dm_plan_info": (C.c_int, [P, I64P]),
     "dm_plan_side_edges": (C.c_int, [P, I64P]),
+    "dm_plan_bytes": (C.c_int, [P, I64P]),
     "dm_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(P)]),
     "dm_mesh_file_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), I64P, I64P, I64P,
                                     C.POINTER(C.c_int), DP, I32P, I32P, C.c_char_p, C.c_int64]),

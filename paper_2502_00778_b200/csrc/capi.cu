@@ -388,6 +388,17 @@ int dm_plan_info(dm_ctx* c, int64_t info[8]) {
   return DM_OK;
 }
 
+int dm_plan_bytes(dm_ctx* c, int64_t out[4]) {
+  if (!c || !out) return DM_ERR_INVALID_ARG;
+  for (int i = 0; i < 4; ++i) out[i] = 0;
+  if (!(c->have_rings && c->ring_ok && c->row_plan)) return DM_OK;
+  out[0] = static_cast<int64_t>(c->rt_bytes[0]);
+  out[1] = static_cast<int64_t>(c->rt_bytes[1]);
+  out[2] = static_cast<int64_t>(c->rt_bytes[2]);
+  out[3] = c->rt_ntiles;
+  return DM_OK;
+}
+
 int dm_plan_side_edges(dm_ctx* c, int64_t* n) {
   if (!c || !n) return DM_ERR_INVALID_ARG;
   *n = c->have_rings && c->ring_ok ? c->n_side : 0;

@@ -220,6 +220,7 @@ struct dm_ctx {
   dm::i64 rt_ntiles = 0;
   dm::DevBuf<int4> rt_meta;         // per tile {code offset (32 B units), code bytes, runs, run block}
   dm::DevBuf<int2> rt_runs;         // kRowRuns per tile {first node, nodes | slot << 16}
+  unsigned long long rt_bytes[3] = {0, 0, 0};  // per step: codes, table fill, meta + runs
   bool have_n2e = false;
   dm::DevBuf<dm::u32> n2e_ptr;
   dm::DevBuf<int32_t> n2e;

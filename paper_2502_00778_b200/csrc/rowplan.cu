@@ -291,12 +291,31 @@ __global__ void __launch_bounds__(kRowTile)
 
 // meta[f] = {code offset (32 B units), code bytes, runs, provisional index}
 // for the tiles in ascending e0 order
+// (+ the plan's per-step stream sizes in sums[0..2]: code bytes, node-table
+// fill bytes, metadata + run bytes -- the element loop's design bytes)
 __global__ void k_rt_meta(const int* __restrict__ order, const int* __restrict__ nruns,
-                          const int* __restrict__ bytes, i64 ntiles, int4* __restrict__ meta) {
+                          const int* __restrict__ bytes, const int2* __restrict__ runs, i64 ntiles,
+                          int4* __restrict__ meta, unsigned long long* __restrict__ sums) {
   const i64 f = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (f >= ntiles) return;
-  const int p = order[f];
-  meta[f] = make_int4(p * (kRowCodeCap / 32), bytes[p], nruns[p], p);
+  unsigned long long cb = 0, fb = 0, mb = 0;
+  if (f < ntiles) {
+    const int p = order[f];
+    meta[f] = make_int4(p * (kRowCodeCap / 32), bytes[p], nruns[p], p);
+    cb = static_cast<unsigned long long>(bytes[p]);
+    for (int r = 0; r < nruns[p]; ++r)
+      fb += 24ull * static_cast<unsigned long long>(runs[static_cast<i64>(p) * kRowRuns + r].y & 0xffff);
+    mb = 16ull + 8ull * static_cast<unsigned long long>(nruns[p]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    mb += __shfl_xor_sync(0xffffffffu, mb, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(sums, cb);
+    atomicAdd(sums + 1, fb);
+    atomicAdd(sums + 2, mb);
+  }
 }
 
 __global__ void k_rt_cand(i64 ne, i64 n, int2* __restrict__ cand) {
@@ -421,7 +440,13 @@ int try_row_plan(dm_ctx* c) {
   DM_LAUNCH(c, k_rt_codes, static_cast<unsigned>(nt), kRowTile, 0, dorder.p, c->edges.p,
             c->inc_ptr.p, c->inc.p, c->elems.p, c->rt_runs.p, nruns.p, c->rcodes.p, c->flag.p,
             c->side.p);
-  DM_LAUNCH(c, k_rt_meta, grid_for(nt, 256), 256, 0, dorder.p, nruns.p, bytes.p, nt, c->rt_meta.p);
+  ScratchBuf<unsigned long long> sums(c->arena, rt_block(c));
+  DM_CK(c, sums.ensure(3));
+  DM_CK(c, cudaMemsetAsync(sums.p, 0, 3 * sizeof(unsigned long long), c->stream));
+  DM_LAUNCH(c, k_rt_meta, grid_for(nt, 256), 256, 0, dorder.p, nruns.p, bytes.p, c->rt_runs.p, nt,
+            c->rt_meta.p, sums.p);
+  DM_CK(c, cudaMemcpyAsync(c->rt_bytes, sums.p, sizeof(c->rt_bytes), cudaMemcpyDeviceToHost,
+                           c->stream));
   {
     int fl[2] = {0, 0};
     DM_CK(c, cudaMemcpyAsync(fl, c->flag.p, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));

@@ -365,6 +365,13 @@ class Engine:
                 "volume_order": "morton" if info[6] else "node",
                 "colored": bool(info[7])}
 
+    def plan_bytes(self) -> dict:
+        """Per-step streams of the row-tile element loop (dm_plan_bytes)."""
+        out = np.zeros(4, np.int64)
+        self._ck(self._lib.dm_plan_bytes(self._c, ptr(out, C.c_int64)), "dm_plan_bytes")
+        return {"codes": int(out[0]), "table_fill": int(out[1]), "meta_runs": int(out[2]),
+                "tiles": int(out[3])}
+
     def side_edges(self) -> int:
         """Edges of the ring path's side list (dm_plan_side_edges)."""
         n = C.c_int64()
