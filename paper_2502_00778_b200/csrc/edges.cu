@@ -94,31 +94,39 @@ __device__ __forceinline__ int2 make_ifl(const int32_t* el, int E, int l) {
   return make_int2(v[im] | (ij << 30), ik << 30);
 }
 
-// Warp per bucket: emit edges, inc_ptr, inc and e2l.
+// Warp per bucket: emit edges, inc_ptr, inc and e2l.  Each chunk's items
+// are loaded before the previous chunk is stored, and each item's
+// predecessor comes by shuffle.
 template <int L>
-__global__ void k_emit(const u64* items, const u32* bstart, const u32* os, i64 nv,
-                       int2* edges, int32_t* inc_ptr, int32_t* inc, int32_t* e2l) {
+__global__ void k_emit(const u64* __restrict__ items, const u32* __restrict__ bstart,
+                       const u32* __restrict__ os, i64 nv, int2* __restrict__ edges,
+                       int32_t* __restrict__ inc_ptr, int32_t* __restrict__ inc,
+                       int32_t* __restrict__ e2l) {
+  constexpr unsigned F = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const i64 j = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (j >= nv) return;
   const u32 b = bstart[j], n = bstart[j + 1] - b;
   u32 id_base = os[j];  // edge id of the first head in this chunk
+  u64 nxt = lane < n ? items[b + lane] : 0;
+  u32 prev_hi = ~0u;  // high word of the item before this chunk
   for (u32 i0 = 0; i0 < n; i0 += 32) {
     const u32 i = i0 + lane;
-    u64 it = 0;
-    bool head = false;
-    if (i < n) {
-      it = items[b + i];
-      head = (i == 0) || ((it >> 32) != (items[b + i - 1] >> 32));
-    }
-    const unsigned hm = __ballot_sync(0xffffffffu, head);
+    const u64 it = nxt;
+    if (i0 + 32 < n) nxt = i + 32 < n ? items[b + i + 32] : 0;
+    const u32 hi = static_cast<u32>(it >> 32);
+    u32 up = __shfl_up_sync(F, hi, 1);
+    if (lane == 0) up = prev_hi;
+    prev_hi = __shfl_sync(F, hi, 31);
+    const bool head = i < n && (i == 0 || hi != up);
+    const unsigned hm = __ballot_sync(F, head);
     if (i < n) {
       // heads at or before this lane within the chunk
       const int before = __popc(hm & (0xffffffffu >> (31 - lane)));
       const int32_t id = static_cast<int32_t>(id_base + before - 1);
       const u32 val = static_cast<u32>(it);
       if (head) {
-        edges[id] = make_int2(static_cast<int>(j), static_cast<int>(it >> 32));
+        edges[id] = make_int2(static_cast<int>(j), static_cast<int>(hi));
         inc_ptr[id] = static_cast<int32_t>(b + i);
       }
       inc[b + i] = static_cast<int32_t>(val / L);

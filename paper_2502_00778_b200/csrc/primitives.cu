@@ -4,6 +4,8 @@
 // more than ~1300 incident tets), one call per such segment.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "dm_internal.cuh"
@@ -195,6 +197,177 @@ __global__ void __launch_bounds__(256)
   for (int i = lane; i < n; i += 32) data[b + i] = buf[i];
 }
 
+// Unique u64 keys (K1's (k << 32 | e*L + l) items, the boundary-edge keys):
+// warp per segment of <= kWarpSeg keys with compressed ranks.  The distinct
+// high words are enumerated smallest first (a warp min-reduction per
+// distinct value: ~7 rounds for a K1 origin bucket of ~36 items), giving
+// every key its group g = rank of its high word among the distinct ones and
+// the segment's distinct count (K1's edges per origin) on the way.  When the
+// low words span < 2^24 and g < 127, g << 24 | (lo - lo_min) is an
+// order-preserving 31-bit key, and a rank costs two integer ops per
+// comparison (the sign bit of v - key accumulates "v < key") against four
+// for the 64-bit compare-and-select; otherwise the 64-bit rank.  Keys are
+// stored straight to their ranks (one segment spans a few sectors).
+// Grid-stride over segments: most calls have ~nv short segments.
+template <int R>
+__device__ __forceinline__ void sort_unique_u64_segment(u64* data, u32 b, int n, int lane,
+                                                        const u64 (&pre)[2], u32* b32, u64* b64,
+                                                        u32* ucnt) {
+  constexpr unsigned F = 0xffffffffu;
+  u64 it[R];
+  u32 lmin = ~0u, lmax = 0u;
+  bool odd = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    it[r] = R <= 2 ? pre[r] : (i < n ? data[b + i] : ~0ull);  // pre: ~0 past n
+    if (i < n) {
+      const u32 lo = static_cast<u32>(it[r]);
+      lmin = min(lmin, lo);
+      lmax = max(lmax, lo);
+      odd |= (it[r] >> 32) == ~0u;  // a high word of ~0 reads as an empty slot below
+    }
+  }
+  lmin = __reduce_min_sync(F, lmin);
+  lmax = __reduce_max_sync(F, lmax);
+  int cnt[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) cnt[r] = 0;
+  u32 d = 0;
+  bool ranked = false;
+  if (lmax - lmin < (1u << 24) && !__any_sync(F, odd)) {
+    u32 g[R], rem[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      g[r] = 0;
+      rem[r] = static_cast<u32>(it[r] >> 32);
+    }
+    for (;;) {
+      u32 m = rem[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) m = min(m, rem[r]);
+      m = __reduce_min_sync(F, m);
+      if (m == ~0u) break;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (rem[r] == m) {
+          g[r] = d;
+          rem[r] = ~0u;
+        }
+      ++d;
+    }
+    if (d < 127) {
+      u32 key[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        key[r] = lane + 32 * r < n ? (g[r] << 24 | (static_cast<u32>(it[r]) - lmin)) : 0x7fffffffu;
+        b32[lane + 32 * r] = key[r];  // slots >= n hold 0x7fffffff: never below a key
+      }
+      __syncwarp();
+      const uint4* q = reinterpret_cast<const uint4*>(b32);
+      for (int i = 0, n4 = (n + 3) >> 2; i < n4; ++i) {
+        const uint4 v = q[i];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          cnt[r] += static_cast<int>(((v.x - key[r]) >> 31) + ((v.y - key[r]) >> 31) +
+                                     ((v.z - key[r]) >> 31) + ((v.w - key[r]) >> 31));
+      }
+      ranked = true;
+    }
+  }
+  if (!ranked) {  // 64-bit rank; distinct high words counted on the sorted run
+#pragma unroll
+    for (int r = 0; r < R; ++r) b64[lane + 32 * r] = it[r];
+    __syncwarp();
+    for (int i = 0; i < n; i += 2) {  // b64[n] is an empty slot (~0) when n is odd
+      const u64 v0 = b64[i], v1 = b64[i + 1];
+#pragma unroll
+      for (int r = 0; r < R; ++r) cnt[r] += (v0 < it[r]) + (v1 < it[r]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (lane + 32 * r < n) b64[cnt[r]] = it[r];
+    __syncwarp();
+    d = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = lane + 32 * r;
+      if (i < n) data[b + i] = b64[i];  // coalesced
+      const bool h = i < n && (i == 0 || (b64[i] >> 32) != (b64[i - 1] >> 32));
+      d += __popc(__ballot_sync(F, h));
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (lane + 32 * r < n) data[b + cnt[r]] = it[r];
+  }
+  if (ucnt && lane == 0) *ucnt = d;
+}
+
+// Grid-stride over chunks of 32 consecutive segments per warp: the bounds
+// of a chunk are read coalesced, empty and single-key segments are finished
+// there (most boundary-edge buckets), and the next segment's (up to 64)
+// keys are loaded before the current one is ranked, so the global-load
+// latency overlaps the rank arithmetic.
+__global__ void __launch_bounds__(256)
+    k_segsort_u64u_warp(u64* data, const u32* seg, i64 nseg, u32* big, int* nbig, u32* ucnt) {
+  constexpr unsigned F = 0xffffffffu;
+  __shared__ __align__(16) u32 s32[8][kWarpSeg];
+  __shared__ __align__(16) u64 s64[8][kWarpSeg + 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 stride = static_cast<i64>(gridDim.x) * 8 * 32;
+  for (i64 s0 = (static_cast<i64>(blockIdx.x) * 8 + warp) * 32; s0 < nseg; s0 += stride) {
+    const i64 s = s0 + lane;
+    u32 sb = 0, sn = 0;
+    if (s < nseg) {
+      sb = seg[s];
+      sn = seg[s + 1] - sb;
+      if (ucnt && sn <= 1) ucnt[s] = sn;
+      if (sn > static_cast<u32>(kWarpSeg)) big[atomicAdd(nbig, 1)] = static_cast<u32>(s);
+    }
+    unsigned work = __ballot_sync(F, s < nseg && sn > 1 && sn <= static_cast<u32>(kWarpSeg));
+    if (!work) continue;
+    auto fetch = [&](int t, u32& b, int& n, u64 (&pre)[2]) {
+      b = __shfl_sync(F, sb, t);
+      n = static_cast<int>(__shfl_sync(F, sn, t));
+      pre[0] = lane < n ? data[b + lane] : ~0ull;
+      pre[1] = n <= 64 && lane + 32 < n ? data[b + lane + 32] : ~0ull;
+    };
+    int t = __ffs(work) - 1;
+    work &= work - 1;
+    u32 b;
+    int n;
+    u64 pre[2];
+    fetch(t, b, n, pre);
+    for (;;) {
+      const int tn = work ? __ffs(work) - 1 : -1;
+      u32 nb = 0;
+      int nn = 0;
+      u64 npre[2] = {~0ull, ~0ull};
+      if (tn >= 0) {
+        work &= work - 1;
+        fetch(tn, nb, nn, npre);
+      }
+      u32* uc = ucnt ? ucnt + s0 + t : nullptr;
+      if (n <= 32) {
+        sort_unique_u64_segment<1>(data, b, n, lane, pre, s32[warp], s64[warp], uc);
+      } else if (n <= 64) {
+        sort_unique_u64_segment<2>(data, b, n, lane, pre, s32[warp], s64[warp], uc);
+      } else {
+        sort_unique_u64_segment<4>(data, b, n, lane, pre, s32[warp], s64[warp], uc);
+      }
+      __syncwarp();
+      if (tn < 0) break;
+      t = tn;
+      b = nb;
+      n = nn;
+      pre[0] = npre[0];
+      pre[1] = npre[1];
+    }
+  }
+}
+
 template <typename K>
 __global__ void __launch_bounds__(512)
     k_segsort_block(K* data, const u32* seg, const u32* big, const int* nbig, int* flag,
@@ -290,8 +463,20 @@ int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg, u32* ucnt) {
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
   int* nbig = c->flag.p + 1;
-  DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg, big.p,
-            nbig, ucnt);
+  if constexpr (sizeof(K) == 8 && kUnique) {
+    static const char* r64 = std::getenv("DUALMESH_SEGSORT_RANK64");  // A/B switch
+    const bool rank64 = r64 && *r64 == '1';
+    if (!rank64) {
+      const unsigned grid = static_cast<unsigned>(std::min<i64>(grid_for(nseg, 256), 148 * 8));
+      DM_LAUNCH(c, k_segsort_u64u_warp, grid, 256, 0, data, seg, nseg, big.p, nbig, ucnt);
+    } else {
+      DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg,
+                big.p, nbig, ucnt);
+    }
+  } else {
+    DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg, big.p,
+              nbig, ucnt);
+  }
   const size_t smem = kBlockSeg * sizeof(K);
   DM_CK(c, cudaFuncSetAttribute(k_segsort_block<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
