@@ -14,11 +14,12 @@
 //     from the caller's coordinate array (24-byte records; runs are padded to
 //     even node ids so every copy is 16-byte aligned) -- no coordinate copy
 //     per call, no per-node fill instructions;
-//   * the lanes of the tile take its edges in direction-major order (sorted
-//     by the edge's index inside its origin row, then by origin): for a
-//     structured grid the 32 lanes of a warp hold the same edge direction of
-//     32 consecutive origins, so a ring step reads 32 consecutive table slots
-//     (no bank conflicts, uniform ring length in the warp);
+//   * the lanes of the tile take its edges sorted by ring length, then by
+//     the edge's index inside its origin row, then by origin: a warp's lanes
+//     walk rings of one length (a Kuhn grid's even and odd cubes give one
+//     edge direction 4- and 6-rings), and for a structured grid they hold
+//     the same edge direction of consecutive origins, so a ring step reads
+//     consecutive table slots (few bank conflicts);
 //   * the rows are staged in shared memory and leave as two TMA bulk stores
 //     per tile (navs rows, s terms) -- contiguous, no per-lane stores.
 // The plan is used when the tiles split little (<= 25 % more tiles than
@@ -99,7 +100,7 @@ __device__ __forceinline__ void bitonic_sort_u32(unsigned* a, int t) {
 // the tile's node set (shared-memory hash set), sorted; its runs of node-id
 // pairs (a run covers pairs [a, b], i.e. nodes [2a, 2b + 2): every copy is
 // 16-byte aligned; consecutive or equal pairs extend a run); the
-// direction-major lane order; and, if the tile fits (<= kRowRuns runs,
+// lane order (ring length, then direction); and, if the tile fits (<= kRowRuns runs,
 // <= kRowSlots slots, <= kRowCodeCap code bytes), its runs and its code block
 // at codes + p * kRowCodeCap.  Otherwise bad[p] says why (the host splits it).
 __global__ void __launch_bounds__(kRTThreads)
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kRTThreads)
                const u32* __restrict__ os, const int32_t* __restrict__ inc_ptr,
                const int32_t* __restrict__ inc, const int32_t* __restrict__ el,
                uint8_t* __restrict__ bad, int2* __restrict__ runs_out, int* __restrict__ nruns_out,
-               int* __restrict__ bytes_out, uint8_t* __restrict__ codes) {
+               int* __restrict__ bytes_out, uint8_t* __restrict__ codes, int by_len) {
   __shared__ RTShared S;
   const int t = threadIdx.x, lane = t & 31;
   const i64 p = static_cast<i64>(base) + blockIdx.x;
@@ -153,6 +154,11 @@ __global__ void __launch_bounds__(kRTThreads)
     }
     // direction-major: index of the edge inside its origin row, then origin
     key = (static_cast<unsigned>(e - static_cast<int>(os[jk.x])) << 8) | static_cast<unsigned>(t);
+    if (by_len)  // ring length first (warps of equal trip counts: on the Kuhn grids the
+                 // even/odd cube orientation splits a direction into 4- and 6-rings)
+      key = static_cast<unsigned>(min(n_inc, 31)) << 27 |
+            min(static_cast<unsigned>(e - static_cast<int>(os[jk.x])), (1u << 19) - 1u) << 8 |
+            static_cast<unsigned>(t);
   }
   S.key[t] = key;
   __syncthreads();
@@ -318,11 +324,11 @@ __global__ void k_rt_meta(const int* __restrict__ order, const int* __restrict__
   }
 }
 
-__global__ void k_rt_cand(i64 ne, i64 n, int2* __restrict__ cand) {
+__global__ void k_rt_cand(i64 ne, i64 n, int ct, int2* __restrict__ cand) {
   const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const i64 e0 = i * kRowTile;
-  cand[i] = make_int2(static_cast<int>(e0), static_cast<int>(ne - e0 < kRowTile ? ne - e0 : kRowTile));
+  const i64 e0 = i * ct;
+  cand[i] = make_int2(static_cast<int>(e0), static_cast<int>(ne - e0 < ct ? ne - e0 : ct));
 }
 
 // boundary segments with positions = edge ids
@@ -356,11 +362,15 @@ int try_row_plan(dm_ctx* c) {
   ArenaScope scratch(c->arena);
   PlanClock clk(c);
   const i64 ne = c->ne;
-  const i64 n0 = (ne + kRowTile - 1) / kRowTile;
+  int ct = kRowTile;  // candidate tile (edges), env DUALMESH_ROW_CAND
+  if (const char* cs = std::getenv("DUALMESH_ROW_CAND")) ct = std::max(2, std::min(kRowTile, std::atoi(cs) & ~1));
+  const i64 n0 = (ne + ct - 1) / ct;
   // provisional tiles: the level-0 ranges p < n0, then the halves of tiles
   // that did not fit, appended level by level (about 2 % of tiles at C5)
   double split_max = 1.25;  // tiles after splitting / (ne / kRowTile), env DUALMESH_ROW_SPLIT_MAX
   if (const char* sm = std::getenv("DUALMESH_ROW_SPLIT_MAX")) split_max = std::atof(sm);
+  int by_len = 1;  // lane order: ring length first; env DUALMESH_ROW_BYLEN=0: direction only
+  if (const char* bl = std::getenv("DUALMESH_ROW_BYLEN")) by_len = std::atoi(bl);
   const i64 cap = static_cast<i64>(split_max * static_cast<double>(n0)) + 1024;
   ScratchBuf<int2> cand(c->arena, rt_block(c));
   ScratchBuf<uint8_t> bad(c->arena, rt_block(c));
@@ -373,7 +383,7 @@ int try_row_plan(dm_ctx* c) {
   DM_CK(c, c->rcodes.ensure(static_cast<size_t>(cap) * kRowCodeCap));
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
-  DM_LAUNCH(c, k_rt_cand, grid_for(n0, 256), 256, 0, ne, n0, cand.p);
+  DM_LAUNCH(c, k_rt_cand, grid_for(n0, 256), 256, 0, ne, n0, ct, cand.p);
   std::vector<int2> all(static_cast<size_t>(n0));  // provisional tiles, host copy
   DM_CK(c, cudaMemcpyAsync(all.data(), cand.p, n0 * sizeof(int2), cudaMemcpyDeviceToHost,
                            c->stream));
@@ -386,7 +396,7 @@ int try_row_plan(dm_ctx* c) {
                                cudaMemcpyHostToDevice, c->stream));
     DM_LAUNCH(c, k_rt_build, static_cast<unsigned>(np), kRTThreads, 0, cand.p,
               static_cast<int>(base), c->edges.p, c->os.p, c->inc_ptr.p, c->inc.p, c->elems.p,
-              bad.p, c->rt_runs.p, nruns.p, bytes.p, c->rcodes.p);
+              bad.p, c->rt_runs.p, nruns.p, bytes.p, c->rcodes.p, by_len);
     hb.resize(static_cast<size_t>(np));
     DM_CK(c, cudaMemcpyAsync(hb.data(), bad.p + base, np, cudaMemcpyDeviceToHost, c->stream));
     DM_CK(c, cudaStreamSynchronize(c->stream));

@@ -40,7 +40,7 @@ def run(m, steps=10, env=None):
             t.append(eng.timings())
         t = np.array(t[2:])
         out = {"n_elements": m.num_elements(), "n_edges": ne, "plan": eng.plan_info(),
-               "side_edges": eng.side_edges(),
+               "side_edges": eng.side_edges(), "plan_bytes": eng.plan_bytes(),
                "element_loop_ms": float(t[:, 0].mean()), "boundary_ms": float(t[:, 1].mean()),
                "volumes_ms": float(t[:, 2].mean()), "step_ms": float(t[:, 3].mean())}
         eng.close()
