@@ -14,7 +14,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -Iinclu
            -Xptxas -warn-spills --expt-relaxed-constexpr
 CXXFLAGS := -O2 -fPIC -std=c++20 -ffp-contract=off -Iinclude
 
-CU_SRCS := $(CSRC)/capi.cu $(CSRC)/primitives.cu $(CSRC)/edges.cu $(CSRC)/navs.cu \
+CU_SRCS := $(CSRC)/capi.cu $(CSRC)/primitives.cu $(CSRC)/edges.cu $(CSRC)/edge_extract.cu $(CSRC)/navs.cu \
            $(CSRC)/volumes.cu $(CSRC)/verify.cu $(CSRC)/validate.cu $(CSRC)/tables.cu \
            $(CSRC)/rings.cu $(CSRC)/rowplan.cu $(CSRC)/devgen.cu $(CSRC)/devmem.cu $(CSRC)/hostio.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))

@@ -241,6 +241,15 @@ struct dm_ctx {
   dm::DevBuf<dm::u32> seg_big;  // segment_sort: ids of segments longer than a warp's
   dm::Arena arena;              // plan temporaries (rings.cu)
   dm::DevBuf<dm::u32> scan_tmp;
+  dm::DevBuf<dm::u64> scan_tmp64;
+  // K1 (edge_extract.cu): packed per-origin counts -> exclusive scan
+  // (items << 32 | entries), entries (element ids bucketed by origin node),
+  // look-back status per warp chunk, and the long-bucket side path
+  dm::DevBuf<dm::u64> k1_cs;
+  dm::DevBuf<dm::u32> k1_ent;
+  dm::DevBuf<dm::u64> k1_status;
+  dm::DevBuf<dm::u32> k1_bscan, k1_blist, k1_bseg, k1_bd;
+  dm::DevBuf<dm::u64> k1_bitems;
   dm::DevBuf<int> flag;
 
   // derived boundary / validation
@@ -471,6 +480,7 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // Exclusive scan of n u32 counts into out[0..n] (out[n] = total) on the ctx
 // stream.  in and out may alias.  Returns DM_OK or an error code.
 int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n);
+int scan_exclusive_u64(dm_ctx* c, const u64* in, u64* out, i64 n);
 
 // Sort each segment [seg[s], seg[s+1]) of data ascending; segments up to
 // 4096 keys (larger ones set *flag = 1).  Keys are u32 or u64.
@@ -496,6 +506,11 @@ int ensure_rings(dm_ctx* c);
 // (sets c->row_plan); called by ensure_rings before the Morton plan.
 int try_row_plan(dm_ctx* c);
 int build_edges_impl(dm_ctx* c);
+// edge_extract.cu: the entry-bucket K1; returns DM_OK, an error, or
+// kK1Unsupported when the mesh needs the generic item-sort path
+// (repeated nodes in an element, more than 2^25 nodes).
+constexpr int kK1Unsupported = -1000;
+int build_edges_buckets(dm_ctx* c);
 int navs_impl(dm_ctx* c, int algo, int variant);
 int volumes_impl(dm_ctx* c, int algo);
 // Coordinate-derived layouts.  coords_changed marks them stale (set-time

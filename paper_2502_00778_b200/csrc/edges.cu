@@ -14,6 +14,8 @@
 // lexicographic edge order of the reference with, per edge, its incident
 // elements in ascending id.  Atomic placement order is erased by the sort
 // (payloads are unique), so every output is deterministic.
+#include <cstdlib>
+
 #include "dm_internal.cuh"
 
 namespace dm {
@@ -180,6 +182,15 @@ int build_edges_impl(dm_ctx* c) {
   c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_ifl = c->have_tables =
       c->have_rings = false;
   c->have_navs = c->have_vols = false;
+  // DUALMESH_K1_LEGACY=1: the item-sort path for every mesh (A/B and tests)
+  const char* legacy = std::getenv("DUALMESH_K1_LEGACY");
+  if (!(legacy && *legacy == '1')) {
+    const int sb = build_edges_buckets(c);
+    if (sb != kK1Unsupported) {
+      c->have_edges = sb == DM_OK;
+      return sb;
+    }
+  }
   const i64 nv = c->nv;
 
   DM_CK(c, c->cnt.ensure(static_cast<size_t>(nv + 1)));

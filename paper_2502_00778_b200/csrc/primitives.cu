@@ -19,40 +19,43 @@ constexpr int kScanPerThread = 8;
 constexpr int kScanBlock = kScanThreads * kScanPerThread;
 
 // Block-local exclusive scan; writes the block total to bsum[blockIdx.x].
+// T = u32 (bucket counts) or u64 (K1's packed (items << 32 | entries) counts:
+// one scan gives both prefix sums while the low word cannot overflow).
+template <typename T>
 __global__ void __launch_bounds__(kScanThreads)
-    k_scan_blocks(const u32* in, u32* out, u32* bsum, i64 n) {
-  __shared__ u32 wsum[kScanThreads / 32];
+    k_scan_blocks(const T* in, T* out, T* bsum, i64 n) {
+  __shared__ T wsum[kScanThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 base = static_cast<i64>(blockIdx.x) * kScanBlock + threadIdx.x * kScanPerThread;
-  u32 v[kScanPerThread];
-  u32 tot = 0;
+  T v[kScanPerThread];
+  T tot = 0;
 #pragma unroll
   for (int q = 0; q < kScanPerThread; ++q) {
     const i64 i = base + q;
-    v[q] = i < n ? in[i] : 0u;
+    v[q] = i < n ? in[i] : T(0);
     tot += v[q];
   }
-  u32 incl = tot;
+  T incl = tot;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    u32 t = __shfl_up_sync(0xffffffffu, incl, o);
+    T t = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += t;
   }
   if (lane == 31) wsum[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    u32 w = lane < kScanThreads / 32 ? wsum[lane] : 0u;
-    u32 wi = w;
+    T w = lane < kScanThreads / 32 ? wsum[lane] : T(0);
+    T wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      u32 t = __shfl_up_sync(0xffffffffu, wi, o);
+      T t = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += t;
     }
     if (lane < kScanThreads / 32) wsum[lane] = wi - w;  // exclusive warp offsets
     if (lane == kScanThreads / 32 - 1) bsum[blockIdx.x] = wi;
   }
   __syncthreads();
-  u32 run = incl - tot + wsum[warp];
+  T run = incl - tot + wsum[warp];
 #pragma unroll
   for (int q = 0; q < kScanPerThread; ++q) {
     const i64 i = base + q;
@@ -61,30 +64,43 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
-__global__ void k_scan_add(u32* out, const u32* boff, i64 n) {
+template <typename T>
+__global__ void k_scan_add(T* out, const T* boff, i64 n) {
   const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] += boff[i / kScanBlock];
 }
 
-__global__ void k_copy_one(u32* dst, const u32* src) { *dst = *src; }
+template <typename T>
+__global__ void k_copy_one(T* dst, const T* src) { *dst = *src; }
 
-int scan_rec(dm_ctx* c, const u32* in, u32* out, i64 n, u32* tmp) {
+template <typename T>
+int scan_rec(dm_ctx* c, const T* in, T* out, i64 n, T* tmp) {
   const i64 nb = (n + kScanBlock - 1) / kScanBlock;
   if (n == 0) {
-    DM_CK(c, cudaMemsetAsync(out, 0, sizeof(u32), c->stream));
+    DM_CK(c, cudaMemsetAsync(out, 0, sizeof(T), c->stream));
     return DM_OK;
   }
-  u32* lvl = tmp;  // nb + 1 entries
-  DM_LAUNCH(c, k_scan_blocks, static_cast<unsigned>(nb), kScanThreads, 0, in, out, lvl, n);
+  T* lvl = tmp;  // nb + 1 entries
+  DM_LAUNCH(c, k_scan_blocks<T>, static_cast<unsigned>(nb), kScanThreads, 0, in, out, lvl, n);
   if (nb > 1) {
-    int st = scan_rec(c, lvl, lvl, nb, tmp + nb + 1);
+    int st = scan_rec<T>(c, lvl, lvl, nb, tmp + nb + 1);
     if (st) return st;
-    DM_LAUNCH(c, k_scan_add, grid_for(n, 256), 256, 0, out, lvl, n);
-    DM_LAUNCH(c, k_copy_one, 1, 1, 0, out + n, lvl + nb);
+    DM_LAUNCH(c, k_scan_add<T>, grid_for(n, 256), 256, 0, out, lvl, n);
+    DM_LAUNCH(c, k_copy_one<T>, 1, 1, 0, out + n, lvl + nb);
   } else {
-    DM_LAUNCH(c, k_copy_one, 1, 1, 0, out + n, lvl);
+    DM_LAUNCH(c, k_copy_one<T>, 1, 1, 0, out + n, lvl);
   }
   return DM_OK;
+}
+
+i64 scan_tmp_need(i64 n) {
+  i64 need = 0, m = n;
+  do {
+    const i64 nb = (m + kScanBlock - 1) / kScanBlock;
+    need += nb + 1;
+    m = nb;
+  } while (m > 1);
+  return need + 4;
 }
 
 // ------------------------------------------------------------ segment sort
@@ -625,15 +641,13 @@ int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg) {
 }
 
 int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n) {
-  // temp: sum over levels of (nb+1)
-  i64 need = 0, m = n;
-  do {
-    const i64 nb = (m + kScanBlock - 1) / kScanBlock;
-    need += nb + 1;
-    m = nb;
-  } while (m > 1);
-  DM_CK(c, c->scan_tmp.ensure(static_cast<size_t>(need + 4)));
-  return scan_rec(c, in, out, n, c->scan_tmp.p);
+  DM_CK(c, c->scan_tmp.ensure(static_cast<size_t>(scan_tmp_need(n))));
+  return scan_rec<u32>(c, in, out, n, c->scan_tmp.p);
+}
+
+int scan_exclusive_u64(dm_ctx* c, const u64* in, u64* out, i64 n) {
+  DM_CK(c, c->scan_tmp64.ensure(static_cast<size_t>(scan_tmp_need(n))));
+  return scan_rec<u64>(c, in, out, n, c->scan_tmp64.p);
 }
 
 int segment_sort_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg) {

@@ -1,0 +1,118 @@
+"""K1 edge extraction on origin buckets (csrc/edge_extract.cu) against the
+generic item-sort path (csrc/edges.cu, DUALMESH_K1_LEGACY=1), the oracle and
+the reference's own build_edges (oracle/_ref, mesh.cpp:256-285).
+
+Every output of north_star (a) is compared bit for bit: the edge list, the
+origin CSR, the element->local-edge map and the edge->element incidence.
+The topologies exercise the register path (Kuhn, 2D), the wide kernel
+(permuted numbering: up to 24 entries per origin), the side path (a 30-tet
+fan, 2-3 flips), the repeated-node fallback and the edge-capacity re-run."""
+import numpy as np
+import pytest
+
+from paper_2502_00778_b200 import Engine, Mesh, meshgen
+
+pytestmark = pytest.mark.gpu
+
+
+def extract(eng, m):
+    eng.set_mesh(m)
+    eng.build_edges()
+    el = eng.edges()
+    ip, inc = eng.incidence()
+    return el.edges.copy(), el.origin_start.copy(), eng.e2l().copy(), ip.copy(), inc.copy()
+
+
+def assert_same(a, b):
+    for x, y, what in zip(a, b, ("edges", "origin_start", "e2l", "inc_ptr", "inc")):
+        np.testing.assert_array_equal(x, y, err_msg=what)
+
+
+def grids():
+    return {
+        "kuhn": meshgen.tet_cube(14, amp=0.15),
+        "kuhn_perm": meshgen.permute(meshgen.tet_cube(14, amp=0.15)),
+        "fan": meshgen.fan_in(meshgen.tet_cube(10, amp=0.1), 30),
+        "flip": meshgen.flip23(meshgen.tet_cube(12, amp=0.1)),
+        "flip_perm": meshgen.permute(meshgen.flip23(meshgen.tet_cube(12, amp=0.1))),
+        "tri": meshgen.tri_square(40, diag_seed=3, amp=0.2),
+        "tri_perm": meshgen.permute(meshgen.tri_square(40, diag_seed=3, amp=0.2)),
+        "bl": meshgen.baseline_config("C4", 8),
+    }
+
+
+@pytest.mark.parametrize("name", list(grids()))
+def test_buckets_equal_item_sort_and_oracle(engine, oracle, monkeypatch, name):
+    m = grids()[name]
+    got = extract(engine, m)
+    monkeypatch.setenv("DUALMESH_K1_LEGACY", "1")
+    legacy = extract(engine, m)
+    monkeypatch.delenv("DUALMESH_K1_LEGACY")
+    assert_same(got, legacy)
+    e, o = oracle.build_edges(m)
+    np.testing.assert_array_equal(got[0], e)
+    np.testing.assert_array_equal(got[1], o)
+    e2l, ip, inc = oracle.edge_maps(m, e, o)
+    assert_same(got, (e, o, e2l, ip, inc))
+
+
+def test_full_size_c3_buckets_equal_item_sort(monkeypatch):
+    """Permuted 160^3 grid (wide kernel + side buckets) against the item sort."""
+    eng = Engine(0)
+    try:
+        meshgen.baseline_config_device(eng, "C3")
+        eng.build_edges()
+        el = eng.edges()
+        got = (el.edges.copy(), el.origin_start.copy(), eng.e2l().copy(), *eng.incidence())
+        monkeypatch.setenv("DUALMESH_K1_LEGACY", "1")
+        eng.build_edges()
+        el = eng.edges()
+        want = (el.edges.copy(), el.origin_start.copy(), eng.e2l().copy(), *eng.incidence())
+        assert_same(got, want)
+    finally:
+        eng.close()
+
+
+def test_repeated_node_falls_back_to_reference_pairs(engine, oracle):
+    """A repeated node inside an element: the reference packs the (a, a)
+    pair (mesh.cpp:260-270); the bucket path hands the mesh to the item
+    sort, whose output equals the reference's own build_edges."""
+    m = meshgen.tet_cube(3, amp=0.0)
+    el = m.elements.reshape(-1, 4).copy()
+    el[5, 2] = el[5, 1]
+    bad = Mesh(3, m.coords, el.reshape(-1), m.boundary)
+    engine.set_mesh(bad)
+    engine.build_edges()
+    got = engine.edges()
+    from oracle.oracle import RefMesh, ref_available
+    if ref_available():
+        want_e, want_o = RefMesh(bad).build_edges()
+    else:
+        want_e, want_o = oracle.build_edges(bad)
+    np.testing.assert_array_equal(got.edges, want_e)
+    np.testing.assert_array_equal(got.origin_start, want_o)
+    assert (got.edges[:, 0] == got.edges[:, 1]).any()
+
+
+def test_out_of_range_node_is_an_error(engine):
+    m = meshgen.tet_cube(3, amp=0.0)
+    el = m.elements.copy()
+    el[7] = m.num_nodes() + 5
+    engine.set_mesh(Mesh(3, m.coords, el, m.boundary))
+    with pytest.raises(ValueError, match="outside"):  # DM_ERR_INVALID_ARG
+        engine.build_edges()
+
+
+def test_edge_capacity_rerun(monkeypatch, oracle):
+    """An edge-count estimate below the real count re-runs P3 at the exact
+    size (fresh context: no capacity left over from earlier calls)."""
+    monkeypatch.setenv("DUALMESH_K1_EDGE_EST", "16")
+    m = meshgen.tet_cube(9, amp=0.1)
+    eng = Engine(0)
+    try:
+        got = extract(eng, m)
+    finally:
+        eng.close()
+    e, o = oracle.build_edges(m)
+    e2l, ip, inc = oracle.edge_maps(m, e, o)
+    assert_same(got, (e, o, e2l, ip, inc))
