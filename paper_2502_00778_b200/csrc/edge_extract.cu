@@ -55,6 +55,7 @@ constexpr unsigned F = 0xffffffffu;
 constexpr u32 kInf = 0xffffffffu;
 constexpr int kChunk = 32;  // buckets per warp chunk (a lane each)
 constexpr int kWarps = 8;   // warp chunks per CTA tile of k_edge_chunks
+constexpr int kCtasPerSm = 16 / kWarps;  // 16 warps per SM at ~128 registers
 constexpr u64 kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 // look-back values pack (edges << 31 | items): both stay below 2^31
 constexpr u64 kItemMask = (1ull << 31) - 1;
@@ -188,7 +189,12 @@ __global__ void k_ent_fill(const int32_t* __restrict__ el, i64 nE, i64 nv, u32* 
     if (bad) atomicOr(flag, bad);
   }
   const bool live = e < nE && !bad;
-  int over = 0;
+  // per role r: the origin, its run of adjacent lanes with the same origin
+  // (consecutive elements sharing a node, e.g. the tets of one hex) and
+  // the run's first lane, which takes the run's slots with one atomic; the
+  // D atomics are issued back to back (predicated, no branches between)
+  int jr[D], lead[D];
+  u32 base[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) {
     int j = -1;
@@ -196,15 +202,30 @@ __global__ void k_ent_fill(const int32_t* __restrict__ el, i64 nE, i64 nv, u32* 
     for (int p = 0; p <= D; ++p)
       if (rk[p] == r) j = v[p];
     if (!live) j = -1;
-    // lanes with the same origin take consecutive slots with one atomic
-    const unsigned m = __match_any_sync(F, j);
-    const int leader = __ffs(m) - 1;
-    u32 base = 0;
-    if (lane == leader && j >= 0) base = atomicAdd(cnt + j, static_cast<u32>(__popc(m)));
-    base = __shfl_sync(F, base, leader);
-    if (j >= 0) {
-      const u32 slot = base + __popc(m & ((1u << lane) - 1));
-      if (slot < static_cast<u32>(CAP)) ent[static_cast<i64>(j) * CAP + slot] = static_cast<u32>(e);
+    const int up = __shfl_up_sync(F, j, 1);
+    const unsigned heads = __ballot_sync(F, lane == 0 || up != j);
+    const int leader = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+    const unsigned after = heads & ~(0xffffffffu >> (31 - lane));
+    const u32 run = static_cast<u32>((after ? __ffs(after) - 1 : 32) - lane);
+    const u32 go = lane == leader && j >= 0;
+    u32* addr = cnt + (j >= 0 ? j : 0);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+        "@p atom.global.add.u32 %0, [%1], %2;\n\t}"
+        : "=r"(base[r])
+        : "l"(addr), "r"(run), "r"(go)
+        : "memory");
+    jr[r] = j;
+    lead[r] = leader;
+  }
+  int over = 0;
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    const u32 b = __shfl_sync(F, base[r], lead[r]);
+    if (jr[r] >= 0) {
+      const u32 slot = b + static_cast<u32>(lane - lead[r]);
+      if (slot < static_cast<u32>(CAP))
+        ent[static_cast<i64>(jr[r]) * CAP + slot] = static_cast<u32>(e);
       else over |= 4;
       if (slot >= static_cast<u32>(Caps<D>::kNarrow)) over |= 8;
     }
@@ -410,24 +431,43 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
   // items: key = (k - j) << 7 | entry rank << 2 | t, t = the node's place
   // among the element's other nodes; kInf for nodes below j / empty slots
   u32 key[S];
+  constexpr int GB = 6;  // element rows gathered per batch (loads in flight; 4-12 measured equal)
 #pragma unroll
-  for (int s = 0; s < NE; ++s) {
-    int v[4] = {0, 0, 0, 0};
-    const bool live = es[s] != kInf;
-    K1_CHECK(!live || es[s] < A.n_elems, "entry", es[s]);
-    if (live) load_nodes<D>(A.el, es[s], v);
-    const int pj = v[0] == j ? 0 : v[1] == j ? 1 : (D == 3 && v[2] == j) ? 2 : D;
-    u32 ls = 0;
+  for (int s0 = 0; s0 < NE; s0 += GB) {
+    int4 row[GB];
 #pragma unroll
-    for (int t = 0; t < D; ++t) {
-      const int q = t + (t >= pj);  // the element's other local nodes, in order
-      const int a = sel4(v[0], v[1], v[2], v[3], q);
-      key[D * s + t] = live && a > j
-                           ? (static_cast<u32>(a - j) << 7) | (static_cast<u32>(s) << 2) | t
-                           : kInf;
-      ls |= ledge<D>(pj, q) << (3 * t);
+    for (int u = 0; u < GB; ++u) {
+      const int s = s0 + u;
+      row[u] = make_int4(0, 0, 0, 0);
+      if (s < NE && es[s] != kInf) {
+        K1_CHECK(es[s] < A.n_elems, "entry", es[s]);
+        if (D == 3) {
+          row[u] = ld_i4(reinterpret_cast<const int4*>(A.el) + es[s]);
+        } else {
+          const int32_t* r = A.el + 3 * static_cast<i64>(es[s]);
+          row[u] = make_int4(__ldg(r), __ldg(r + 1), __ldg(r + 2), 0);
+        }
+      }
     }
-    if (live) s_info[s][lane] = (static_cast<u64>(ls) << 32) | es[s];
+#pragma unroll
+    for (int u = 0; u < GB; ++u) {
+      const int s = s0 + u;
+      if (s >= NE) break;
+      const bool live = es[s] != kInf;
+      const int v[4] = {row[u].x, row[u].y, row[u].z, row[u].w};
+      const int pj = v[0] == j ? 0 : v[1] == j ? 1 : (D == 3 && v[2] == j) ? 2 : D;
+      u32 ls = 0;
+#pragma unroll
+      for (int t = 0; t < D; ++t) {
+        const int q = t + (t >= pj);  // the element's other local nodes, in order
+        const int a = sel4(v[0], v[1], v[2], v[3], q);
+        key[D * s + t] = live && a > j
+                             ? (static_cast<u32>(a - j) << 7) | (static_cast<u32>(s) << 2) | t
+                             : kInf;
+        ls |= ledge<D>(pj, q) << (3 * t);
+      }
+      if (live) s_info[s][lane] = (static_cast<u64>(ls) << 32) | es[s];
+    }
   }
   oem_sort<S>(key);
 
@@ -566,7 +606,7 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
 
 // Shared memory per warp of k_edge_chunks<D, NEMAX>: entry info [NEMAX][32]
 // (element id | local edges << 32); the chunk's staged rows, then inc;
-// staged edges and inc_ptr.  Sized for two CTAs per SM.
+// staged edges and inc_ptr.  Sized for kCtasPerSm CTAs per SM.
 template <int D, int NEMAX>
 struct ChunkSmem {
   static constexpr int kInfo = NEMAX * 32 * 8;
@@ -574,11 +614,11 @@ struct ChunkSmem {
   static constexpr int kHead = Caps<D>::kHeadStage;
   static constexpr int kWarpBytes = kInfo + kInc * 4 + kHead * 12;
   static_assert(kInc >= Caps<D>::kNe * 32, "the chunk's rows are staged inside the inc stage");
-  static_assert(2 * (kWarps * kWarpBytes + 2048) <= 228 * 1024, "two CTAs per SM");
+  static_assert(kCtasPerSm * (kWarps * kWarpBytes + 1024 + 128) <= 228 * 1024, "CTAs per SM");
 };
 
 template <int D, int NEMAX>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_edge_chunks(ChunkArgs A) {
+__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) k_edge_chunks(ChunkArgs A) {
   constexpr int NE = Caps<D>::kNe;  // row stride
   using SM = ChunkSmem<D, NEMAX>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -645,7 +685,7 @@ int run_chunks(dm_ctx* c, ChunkArgs A, int* flags_host) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = static_cast<unsigned>(std::min<i64>(sms * 2, A.ntiles));
+  const unsigned grid = static_cast<unsigned>(std::min<i64>(sms * kCtasPerSm, A.ntiles));
   constexpr size_t smem = kWarps * ChunkSmem<D, NEMAX>::kWarpBytes;
   DM_CK(c, cudaFuncSetAttribute(k_edge_chunks<D, NEMAX>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
