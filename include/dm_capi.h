@@ -99,7 +99,9 @@ int dm_mesh_sizes(dm_ctx* ctx, int* dim, int64_t* n_nodes, int64_t* n_elements,
 
 /* Edge extraction: ref build_edges, proj/src/mesh.cpp:256-285.  Also builds
  * the element-to-local-edge map e2l[e*L+l] (local order mesh.cpp:17,263-265)
- * and the edge-to-element CSR incidence (ascending element ids per edge). */
+ * and the edge-to-element CSR incidence (ascending element ids per edge).
+ * DM_ERR_INVALID_ARG if an element references a node id outside
+ * [0, n_nodes) (the reference's behaviour there is undefined). */
 int dm_build_edges(dm_ctx* ctx, int64_t* n_edges);
 /* edges: 2*n_edges ids; origin_start: n_nodes+1 (size_t in the reference,
  * mesh.hpp:50).  Either pointer may be NULL. */
