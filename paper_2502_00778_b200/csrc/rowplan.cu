@@ -44,7 +44,7 @@ namespace dm {
 namespace {
 
 constexpr int kRTThreads = 256;   // plan kernel: one CTA per tile
-constexpr int kRTHash = 4096;
+constexpr int kRTHash = 2048;  // <= 512 unique nodes: load factor <= 1/4
 constexpr int kRTUniqCap = 512;
 constexpr int kRTCodeUnits = kRowCodeCap / 32;
 
@@ -56,7 +56,8 @@ constexpr int kRTTooManyCodes = 4;
 struct RTShared {
   int hs[kRTHash];
   int uq[kRTUniqCap];
-  unsigned key[kRTThreads];
+  unsigned key[kRTThreads], ktmp[kRTThreads];
+  int2 heads[kRowRuns];  // run heads {first pair, pairs}, unsorted
   int n_uniq;
   int nruns, nslots;
   int2 runs[kRowRuns];
@@ -64,36 +65,37 @@ struct RTShared {
   int woff[8];
 };
 
-__device__ __forceinline__ void bitonic_sort_int(int* a, int P, int t) {
-  for (int k = 2; k <= P; k <<= 1)
+// Sorts the kRTThreads unique keys a[t] ascending in place: each warp sorts
+// its 32 keys with a shuffle bitonic network (no block barriers), then every
+// key's rank is its rank in its warp plus, per other warp, the number of
+// that warp's keys below it (binary search in the warp's sorted run).
+__device__ __forceinline__ void warp_merge_sort_u32(unsigned* a, unsigned* tmp, int t) {
+  const int lane = t & 31, w = t >> 5;
+  unsigned x = a[t];
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = t; i < P; i += kRTThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const int x = a[i], y = a[ixj];
-          if ((x > y) == ((i & k) == 0)) {
-            a[i] = y;
-            a[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
+      const unsigned y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      x = (lower == up) ? min(x, y) : max(x, y);
     }
-}
-
-__device__ __forceinline__ void bitonic_sort_u32(unsigned* a, int t) {
-  for (int k = 2; k <= kRTThreads; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int i = t, ixj = i ^ j;
-      if (ixj > i) {
-        const unsigned x = a[i], y = a[ixj];
-        if ((x > y) == ((i & k) == 0)) {
-          a[i] = y;
-          a[ixj] = x;
-        }
-      }
-      __syncthreads();
-    }
+  tmp[t] = x;  // warp w's sorted run at tmp[32w .. 32w + 32)
+  __syncthreads();
+  int r = lane;
+#pragma unroll
+  for (int v = 0; v < kRTThreads / 32; ++v) {
+    if (v == w) continue;
+    const unsigned* run = tmp + 32 * v;
+    int lo = 0;  // keys of run v below x
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (run[lo + step - 1] < x) lo += step;
+    r += lo + (run[31] < x && lo == 31 ? 1 : 0);
+  }
+  __syncthreads();
+  a[r] = x;
+  __syncthreads();
 }
 
 // One CTA per candidate tile {e0, cnt} (tile index p = base + blockIdx.x):
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kRTThreads)
   if (t < 8) S.wmax[t] = 0;
   __syncthreads();
   auto insert = [&](int v) {
-    unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 20;  // 12 bits
+    unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 21;  // 11 bits
     for (int probe = 0; probe < kRTHash; ++probe, h = (h + 1) & (kRTHash - 1)) {
       const int old = atomicCAS(&S.hs[h], -1, v);
       if (old == -1) {
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(kRTThreads)
     }
   };
   int n_inc = 0;
-  unsigned key = 0xffffffffu;
+  unsigned key = 0xffffff00u | static_cast<unsigned>(t);  // idle lanes: unique, after every edge
   if (t < cnt) {
     const int e = e0 + t;
     const int2 jk = edges[e];
@@ -141,16 +143,29 @@ __global__ void __launch_bounds__(kRTThreads)
     n_inc = inc_ptr[e + 1] - pb;
     int last = -1;
     // the ring nodes: the two others of each element (a side-list edge, more
-    // than kRingMax incidences, needs only j and k in the table)
-    for (int q = 0; q < (n_inc > kRingMax ? 0 : n_inc); ++q) {
-      const int4 v = reinterpret_cast<const int4*>(el)[inc[pb + q]];
-      const int vs[4] = {v.x, v.y, v.z, v.w};
+    // than kRingMax incidences, needs only j and k in the table); element
+    // ids and rows are loaded eight at a time (two round trips per batch
+    // instead of two per element)
+    const int nq = n_inc > kRingMax ? 0 : n_inc;
+    for (int q0 = 0; q0 < nq; q0 += 8) {
+      int id[8];
+      int4 rows[8];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-        if (vs[a] != jk.x && vs[a] != jk.y && vs[a] != last) {
-          insert(vs[a]);
-          last = vs[a];
-        }
+      for (int u = 0; u < 8; ++u) id[u] = q0 + u < nq ? __ldg(inc + pb + q0 + u) : -1;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        rows[u] = id[u] >= 0 ? __ldg(reinterpret_cast<const int4*>(el) + id[u])
+                             : make_int4(jk.x, jk.x, jk.x, jk.x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int vs[4] = {rows[u].x, rows[u].y, rows[u].z, rows[u].w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if (vs[a] != jk.x && vs[a] != jk.y && vs[a] != last) {
+            insert(vs[a]);
+            last = vs[a];
+          }
+      }
     }
     // direction-major: index of the edge inside its origin row, then origin
     key = (static_cast<unsigned>(e - static_cast<int>(os[jk.x])) << 8) | static_cast<unsigned>(t);
@@ -168,37 +183,51 @@ __global__ void __launch_bounds__(kRTThreads)
     if (t == 0) bad[p] = static_cast<uint8_t>(badbits);
     return;
   }
-  int P = 2;
-  while (P < nu) P <<= 1;
-  for (int i = nu + t; i < P; i += kRTThreads) S.uq[i] = 0x7fffffff;
+  // runs of node pairs straight from the hash set (no sorted node list): a
+  // present pair p (node 2p or 2p + 1 in the tile) opens a run iff pair
+  // p - 1 is absent; the run extends while the next pairs are present.  The
+  // <= kRowRuns heads are then ordered by pair and take their table slots.
+  auto present = [&](int v) -> bool {
+    if (v < 0) return false;
+    unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 21;
+    for (int probe = 0; probe < kRTHash; ++probe, h = (h + 1) & (kRTHash - 1)) {
+      const int x = S.hs[h];
+      if (x == v) return true;
+      if (x == -1) return false;
+    }
+    return false;
+  };
+  if (t == 0) S.nruns = 0;
   __syncthreads();
-  bitonic_sort_int(S.uq, P, t);
-  // runs of node pairs: a node whose pair exceeds the previous node's pair
-  // by more than one opens a run (thread 0; ~240 sorted nodes)
-  if (t == 0) {
-    int nr = 0, slots = 0, a = 0, last = -2;
-    for (int i = 0; i < nu; ++i) {
-      const int pr = S.uq[i] >> 1;
-      if (pr > last + 1) {
-        if (i > 0) {
-          if (nr < kRowRuns) S.runs[nr] = make_int2(2 * a, (2 * (last - a + 1)) | slots << 16);
-          slots += 2 * (last - a + 1);
-          ++nr;
-        }
-        a = pr;
-      }
-      last = pr;
+  for (int i = t; i < nu; i += kRTThreads) {
+    const int v = S.uq[i], pr = v >> 1;
+    const bool rep = !(v & 1) || !present(v - 1);  // one representative per pair
+    if (rep && !present(2 * pr - 2) && !present(2 * pr - 1)) {
+      int len = 1;
+      while (present(2 * (pr + len)) || present(2 * (pr + len) + 1)) ++len;
+      const int r = atomicAdd(&S.nruns, 1);
+      if (r < kRowRuns) S.heads[r] = make_int2(pr, len);
     }
-    if (nu > 0) {
-      if (nr < kRowRuns) S.runs[nr] = make_int2(2 * a, (2 * (last - a + 1)) | slots << 16);
-      slots += 2 * (last - a + 1);
-      ++nr;
-    }
-    S.nruns = nr;
-    S.nslots = slots;
   }
-  // lane order
-  bitonic_sort_u32(S.key, t);
+  warp_merge_sort_u32(S.key, S.ktmp, t);  // lane order (its barriers also publish the heads)
+  if (t < 32) {  // order the heads by pair, then slot offsets
+    const int nr = min(S.nruns, kRowRuns);
+    const int2 hd = t < nr ? S.heads[t] : make_int2(0x7fffffff, 0);
+    int rank = 0;
+    for (int q = 0; q < nr; ++q) rank += __shfl_sync(0xffffffffu, hd.x, q) < hd.x;
+    int x = t < nr ? 2 * hd.y : 0;  // exclusive scan in pair order: by rank
+    int off = 0;
+    for (int q = 0; q < nr; ++q) {
+      const int rq = __shfl_sync(0xffffffffu, rank, q);
+      const int lq = __shfl_sync(0xffffffffu, x, q);
+      off += rq < rank ? lq : 0;
+    }
+    const int tot = __reduce_add_sync(0xffffffffu, x);
+    __syncwarp();
+    if (t < nr) S.runs[rank] = make_int2(2 * hd.x, (2 * hd.y) | off << 16);
+    if (t == 0) S.nslots = tot;
+  }
+  __syncthreads();
   const unsigned kq = S.key[t];
   const int q = static_cast<int>(kq & 0xffu);
   const int e = e0 + q;
