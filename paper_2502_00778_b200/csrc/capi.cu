@@ -10,6 +10,12 @@ using namespace dm;
 
 namespace {
 
+// origin CSR widened to the reference's size_t (mesh.hpp:50) on the device
+__global__ void k_widen_u32(const u32* __restrict__ in, i64 n, u64* __restrict__ out) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
 const char* kStatus[] = {"ok",           "invalid argument", "mesh/edge mismatch",
                          "boundary edge absent from EdgeList", "CUDA error", "out of device memory",
                          "call order",   "unsupported size"};
@@ -181,10 +187,11 @@ int dm_get_edges(dm_ctx* c, int32_t* edges, uint64_t* origin_start) {
     if (int st = copy_d2h(c, edges, c->edges.p, sizeof(int2) * c->ne)) return st;
   if (origin_start) {
     // widen the 32-bit device CSR to the reference's size_t (mesh.hpp:50)
-    std::vector<std::uint32_t> tmp(static_cast<size_t>(c->nv + 1));
-    if (int st = copy_d2h(c, tmp.data(), c->os.p, sizeof(std::uint32_t) * (c->nv + 1)))
-      return st;
-    for (int64_t v = 0; v <= c->nv; ++v) origin_start[v] = tmp[static_cast<size_t>(v)];
+    DevBuf<u64> wide;
+    DM_CK(c, wide.ensure(static_cast<size_t>(c->nv + 1)));
+    DM_LAUNCH(c, k_widen_u32, grid_for(c->nv + 1, 256), 256, 0, c->os.p, c->nv + 1, wide.p);
+    if (int st = copy_d2h(c, origin_start, wide.p, sizeof(u64) * (c->nv + 1))) return st;
+    DM_CK(c, cudaStreamSynchronize(c->stream));  // before the scratch is freed
   }
   DM_CK(c, cudaStreamSynchronize(c->stream));
   return DM_OK;
