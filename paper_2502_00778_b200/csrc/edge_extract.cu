@@ -150,6 +150,17 @@ __device__ __forceinline__ void oem_sort(u32 (&a)[N]) {
   run_net<N>(a, std::make_integer_sequence<int, NetOf<N>::net.n>{});
 }
 
+// Compile-time loop: f(std::integral_constant<int, B>) for B in [B0, B1)
+// (nvcc stops fully unrolling large loop nests, which would leave register
+// arrays dynamically indexed, i.e. in local memory).
+template <int B0, int B1, typename Fn>
+__device__ __forceinline__ void static_for(Fn&& f) {
+  if constexpr (B0 < B1) {
+    f(std::integral_constant<int, B0>{});
+    static_for<B0 + 1, B1>(f);
+  }
+}
+
 // ---------------------------------------------------------------- P1
 // Node v[p] ranks above r other nodes of its element; with r < D it is the
 // origin of D - r of the element's pairs.  Flags: 1 = node id out of range,
@@ -432,8 +443,8 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
   // among the element's other nodes; kInf for nodes below j / empty slots
   u32 key[S];
   constexpr int GB = 6;  // element rows gathered per batch (loads in flight; 4-12 measured equal)
-#pragma unroll
-  for (int s0 = 0; s0 < NE; s0 += GB) {
+  static_for<0, (NE + GB - 1) / GB>([&](auto batch) {
+    constexpr int s0 = decltype(batch)::value * GB;
     int4 row[GB];
 #pragma unroll
     for (int u = 0; u < GB; ++u) {
@@ -452,23 +463,24 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
 #pragma unroll
     for (int u = 0; u < GB; ++u) {
       const int s = s0 + u;
-      if (s >= NE) break;
-      const bool live = es[s] != kInf;
-      const int v[4] = {row[u].x, row[u].y, row[u].z, row[u].w};
-      const int pj = v[0] == j ? 0 : v[1] == j ? 1 : (D == 3 && v[2] == j) ? 2 : D;
-      u32 ls = 0;
+      if (s < NE) {
+        const bool live = es[s] != kInf;
+        const int v[4] = {row[u].x, row[u].y, row[u].z, row[u].w};
+        const int pj = v[0] == j ? 0 : v[1] == j ? 1 : (D == 3 && v[2] == j) ? 2 : D;
+        u32 ls = 0;
 #pragma unroll
-      for (int t = 0; t < D; ++t) {
-        const int q = t + (t >= pj);  // the element's other local nodes, in order
-        const int a = sel4(v[0], v[1], v[2], v[3], q);
-        key[D * s + t] = live && a > j
-                             ? (static_cast<u32>(a - j) << 7) | (static_cast<u32>(s) << 2) | t
-                             : kInf;
-        ls |= ledge<D>(pj, q) << (3 * t);
+        for (int t = 0; t < D; ++t) {
+          const int q = t + (t >= pj);  // the element's other local nodes, in order
+          const int a = sel4(v[0], v[1], v[2], v[3], q);
+          key[D * s + t] = live && a > j
+                               ? (static_cast<u32>(a - j) << 7) | (static_cast<u32>(s) << 2) | t
+                               : kInf;
+          ls |= ledge<D>(pj, q) << (3 * t);
+        }
+        if (live) s_info[s][lane] = (static_cast<u64>(ls) << 32) | es[s];
       }
-      if (live) s_info[s][lane] = (static_cast<u64>(ls) << 32) | es[s];
     }
-  }
+  });
   oem_sort<S>(key);
 
   // edges and items of the bucket; slots past the warp's fullest bucket are
@@ -476,13 +488,24 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
   u32 d = 0, nit = 0;
   if (reg) {
     u32 prev = kInf;
+    if constexpr (S <= 64) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      if (key[s] == kInf) break;
-      const u32 kd = key[s] >> 7;
-      d += kd != prev;
-      prev = kd;
-      ++nit;
+      for (int s = 0; s < S; ++s) {
+        if (key[s] == kInf) break;
+        const u32 kd = key[s] >> 7;
+        d += kd != prev;
+        prev = kd;
+        ++nit;
+      }
+    } else {  // the wide kernel: a compile-time loop keeps key[] in registers
+      static_for<0, S>([&](auto si) {
+        constexpr int s = decltype(si)::value;
+        const u32 kd = key[s] >> 7;
+        const bool v = key[s] != kInf;
+        d += v && kd != prev;
+        prev = kd;
+        nit += v;
+      });
     }
   } else if (Ln.big) {
     const u32 b = A.bscan[Ln.j];
@@ -530,9 +553,7 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
   const bool st_head = !anybig && ne_w <= static_cast<u32>(Caps<D>::kHeadStage);
   if (reg) {
     u32 prev = kInf, g = 0;
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      if (static_cast<u32>(s) >= nmax) break;
+    auto emit = [&](const int s) {
       if (key[s] != kInf) {
         const u32 kd = key[s] >> 7, se = (key[s] >> 2) & 31, t = key[s] & 3;
         const bool head = kd != prev;
@@ -557,6 +578,17 @@ __device__ __forceinline__ void process_chunk(const ChunkArgs& A, u32 tile, u32 
           }
         }
       }
+    };
+    if constexpr (S <= 64) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (static_cast<u32>(s) >= nmax) break;
+        emit(s);
+      }
+    } else {
+      static_for<0, S>([&](auto si) {
+        if (static_cast<u32>(decltype(si)::value) < nmax) emit(decltype(si)::value);
+      });
     }
   }
   // side buckets: the warp emits each from its sorted item list
