@@ -88,7 +88,9 @@ def cpu_rows(m, reps, ref_reps, threads):
     plan = O.plan(m, e, o)
     buf = (np.empty(m.dim * e.shape[0]), np.empty(e.shape[0]), np.empty(m.num_nodes()))
     try:
-        out["mt_dualfree_step_ms"] = best(lambda: O.metrics_mt(plan, m.coords, threads, buf), reps)
+        O.metrics_mt(plan, m.coords, threads, buf)  # warm-up: first touch of the result buffers
+        out["mt_dualfree_step_ms"] = best(lambda: O.metrics_mt(plan, m.coords, threads, buf),
+                                          max(reps, 3))
     finally:
         O.plan_free(plan)
     out["mt_threads"] = threads
