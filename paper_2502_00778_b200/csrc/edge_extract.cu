@@ -798,7 +798,11 @@ static int build_buckets(dm_ctx* c) {
     DM_LAUNCH(c, k_big_items<D>, gb, 256, 0, c->elems.p, c->k1_blist.p, bent_seg, bent.p, nbig,
               nullptr, bseg, c->k1_bitems.p);
     st = segment_sort_unique_u64(c, c->k1_bitems.p, bseg, nbig, c->k1_bd.p);
+    // the entry lists (bent) are freed at the end of this block: the stream
+    // must be past their readers on every path
+    const cudaError_t sync = cudaStreamSynchronize(c->stream);
     if (st) return st;
+    DM_CK(c, sync);
     A.bscan = c->k1_bscan.p;
     A.bseg = bseg;
     A.bd = c->k1_bd.p;
