@@ -116,3 +116,36 @@ def test_edge_capacity_rerun(monkeypatch, oracle):
     e, o = oracle.build_edges(m)
     e2l, ip, inc = oracle.edge_maps(m, e, o)
     assert_same(got, (e, o, e2l, ip, inc))
+
+
+def tri_fan(n):
+    """n triangles around node 0 (the hub is the smallest id of each: n entries
+    in one 2D origin bucket, beyond a row's 23)."""
+    th = 2 * np.pi * np.arange(n) / n
+    coords = np.concatenate([[0.0, 0.0], np.stack([np.cos(th), np.sin(th)], 1).reshape(-1)])
+    el = np.stack([np.zeros(n, np.int32), 1 + np.arange(n), 1 + (np.arange(n) + 1) % n], 1)
+    bnd = np.stack([1 + np.arange(n), 1 + (np.arange(n) + 1) % n], 1)
+    return Mesh(2, coords.astype(np.float64), el.astype(np.int32).reshape(-1),
+                bnd.astype(np.int32).reshape(-1))
+
+
+@pytest.mark.parametrize("n", [5, 23, 24, 40, 300])
+def test_2d_fan_side_path(engine, oracle, monkeypatch, n):
+    m = tri_fan(n)
+    got = extract(engine, m)
+    e, o = oracle.build_edges(m)
+    e2l, ip, inc = oracle.edge_maps(m, e, o)
+    assert_same(got, (e, o, e2l, ip, inc))
+    monkeypatch.setenv("DUALMESH_K1_LEGACY", "1")
+    assert_same(got, extract(engine, m))
+
+
+def test_single_element(engine, oracle):
+    for m in (Mesh(3, np.array([0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0, 1], np.float64),
+                   np.array([0, 1, 2, 3], np.int32), np.zeros(0, np.int32)),
+              Mesh(2, np.array([0, 0, 1, 0, 0, 1], np.float64), np.array([2, 0, 1], np.int32),
+                   np.zeros(0, np.int32))):
+        got = extract(engine, m)
+        e, o = oracle.build_edges(m)
+        e2l, ip, inc = oracle.edge_maps(m, e, o)
+        assert_same(got, (e, o, e2l, ip, inc))
