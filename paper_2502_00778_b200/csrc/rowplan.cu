@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "dm_internal.cuh"
@@ -413,15 +414,21 @@ int try_row_plan(dm_ctx* c) {
   DM_CK(c, c->flag.ensure(4));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
   DM_LAUNCH(c, k_rt_cand, grid_for(n0, 256), 256, 0, ne, n0, ct, cand.p);
-  std::vector<int2> all(static_cast<size_t>(n0));  // provisional tiles, host copy
-  DM_CK(c, cudaMemcpyAsync(all.data(), cand.p, n0 * sizeof(int2), cudaMemcpyDeviceToHost,
-                           c->stream));
+  // provisional tiles: p < n0 the level-0 ranges (by formula, as k_rt_cand
+  // writes them), then the halves of tiles that did not fit (host list)
+  std::vector<int2> extra;
+  auto tile_of = [&](i64 p) -> int2 {
+    if (p >= n0) return extra[static_cast<size_t>(p - n0)];
+    const i64 e0 = p * ct;
+    return make_int2(static_cast<int>(e0), static_cast<int>(ne - e0 < ct ? ne - e0 : ct));
+  };
+  clk.mark("row tiles: setup");
   std::vector<uint8_t> hb;
   std::vector<int> child(static_cast<size_t>(n0), -1);  // first of the two halves
   i64 base = 0, np = n0;
   for (int level = 0; np > 0; ++level) {
     if (level > 0)
-      DM_CK(c, cudaMemcpyAsync(cand.p, all.data() + base, np * sizeof(int2),
+      DM_CK(c, cudaMemcpyAsync(cand.p, extra.data() + (base - n0), np * sizeof(int2),
                                cudaMemcpyHostToDevice, c->stream));
     DM_LAUNCH(c, k_rt_build, static_cast<unsigned>(np), kRTThreads, 0, cand.p,
               static_cast<int>(base), c->edges.p, c->os.p, c->inc_ptr.p, c->inc.p, c->elems.p,
@@ -429,45 +436,66 @@ int try_row_plan(dm_ctx* c) {
     hb.resize(static_cast<size_t>(np));
     DM_CK(c, cudaMemcpyAsync(hb.data(), bad.p + base, np, cudaMemcpyDeviceToHost, c->stream));
     DM_CK(c, cudaStreamSynchronize(c->stream));
+    clk.mark(level == 0 ? "row tiles: build level 0" : "row tiles: build level >0");
     i64 nbad = 0;
     const i64 next = base + np;
-    for (i64 i = 0; i < np; ++i) {
-      if (!hb[static_cast<size_t>(i)]) continue;
+    if (static_cast<i64>(child.size()) < next) child.resize(static_cast<size_t>(next), -1);
+    // the flagged tiles (mostly none: the scan skips eight zero flags at a time)
+    const uint8_t* q = hb.data();
+    const uint8_t* const end = q + np;
+    for (;;) {
+      while (q + 8 <= end) {
+        std::uint64_t w;
+        std::memcpy(&w, q, 8);
+        if (w) break;
+        q += 8;
+      }
+      while (q < end && !*q) ++q;
+      if (q >= end) break;
+      const i64 i = q - hb.data();
+      ++q;
       ++nbad;
-      const int2 tl = all[static_cast<size_t>(base + i)];
+      const int2 tl = tile_of(base + i);
       if (tl.y < 2) return DM_OK;  // one edge does not fit: Morton plan
       const int h = tl.y >= 4 ? (tl.y / 2 + 1) & ~1 : 1;  // even splits keep e0 even
-      child[static_cast<size_t>(base + i)] = static_cast<int>(all.size());
-      all.push_back(make_int2(tl.x, h));
-      all.push_back(make_int2(tl.x + h, tl.y - h));
-      child.push_back(-1);
-      child.push_back(-1);
+      child[static_cast<size_t>(base + i)] = static_cast<int>(n0 + static_cast<i64>(extra.size()));
+      extra.push_back(make_int2(tl.x, h));
+      extra.push_back(make_int2(tl.x + h, tl.y - h));
     }
     if (level == 0 && static_cast<double>(nbad) > (split_max - 1.0) * static_cast<double>(n0))
       return DM_OK;  // tables too large: Morton plan
-    if (static_cast<i64>(all.size()) > cap) return DM_OK;  // (cap: the split budget below)
+    if (n0 + static_cast<i64>(extra.size()) > cap) return DM_OK;  // (cap: the split budget below)
     base = next;
-    np = static_cast<i64>(all.size()) - next;
+    np = n0 + static_cast<i64>(extra.size()) - next;
     DM_CK(c, cand.ensure(np > 0 ? np : 1));
   }
   clk.mark("row tiles: build + split");
+  child.resize(static_cast<size_t>(n0) + extra.size(), -1);
   // final order: every level-0 tile, or its halves in place, depth first
+  // (only split tiles need the stack)
   std::vector<int> order;
-  order.reserve(all.size());
+  order.reserve(static_cast<size_t>(n0) + extra.size());
   std::vector<int> stack;
-  for (i64 i = n0 - 1; i >= 0; --i) stack.push_back(static_cast<int>(i));
-  while (!stack.empty()) {
-    const int pv = stack.back();
-    stack.pop_back();
-    const int ch = child[static_cast<size_t>(pv)];
-    if (ch < 0) {
-      order.push_back(pv);
-    } else {
-      stack.push_back(ch + 1);
-      stack.push_back(ch);
+  for (i64 i = 0; i < n0; ++i) {
+    if (child[static_cast<size_t>(i)] < 0) {
+      order.push_back(static_cast<int>(i));
+      continue;
+    }
+    stack.push_back(static_cast<int>(i));
+    while (!stack.empty()) {
+      const int pv = stack.back();
+      stack.pop_back();
+      const int ch = child[static_cast<size_t>(pv)];
+      if (ch < 0) {
+        order.push_back(pv);
+      } else {
+        stack.push_back(ch + 1);
+        stack.push_back(ch);
+      }
     }
   }
   const i64 nt = static_cast<i64>(order.size());
+  clk.mark("row tiles: host order");
   if (static_cast<double>(nt) > split_max * static_cast<double>(n0)) return DM_OK;
   ScratchBuf<int> dorder(c->arena, rt_block(c));
   DM_CK(c, dorder.ensure(nt));
@@ -476,6 +504,7 @@ int try_row_plan(dm_ctx* c) {
   DM_CK(c, c->rt_meta.ensure(static_cast<size_t>(nt)));
   DM_CK(c, c->side.ensure(kSideCap));
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 2 * sizeof(int), c->stream));
+  clk.mark("row tiles: order upload");
   DM_LAUNCH(c, k_rt_codes, static_cast<unsigned>(nt), kRowTile, 0, dorder.p, c->edges.p,
             c->inc_ptr.p, c->inc.p, c->elems.p, c->rt_runs.p, nruns.p, c->rcodes.p, c->flag.p,
             c->side.p);
@@ -520,7 +549,7 @@ int try_row_plan(dm_ctx* c) {
   if (const char* ck = std::getenv("DUALMESH_PLAN_CHECK")) {  // debugging aid: host audit
     if (std::atoi(ck) == 1) {
       std::vector<int4> hm(static_cast<size_t>(nt));
-      std::vector<int2> hr(static_cast<size_t>(all.size()) * kRowRuns);
+      std::vector<int2> hr((static_cast<size_t>(n0) + extra.size()) * kRowRuns);
       DM_CK(c, cudaMemcpy(hm.data(), c->rt_meta.p, nt * sizeof(int4), cudaMemcpyDeviceToHost));
       DM_CK(c, cudaMemcpy(hr.data(), c->rt_runs.p, hr.size() * sizeof(int2),
                           cudaMemcpyDeviceToHost));
