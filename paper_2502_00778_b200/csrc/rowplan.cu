@@ -36,6 +36,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
 #include <vector>
 
 #include "dm_internal.cuh"
@@ -425,6 +426,7 @@ int try_row_plan(dm_ctx* c) {
   clk.mark("row tiles: setup");
   std::vector<uint8_t> hb;
   std::vector<int> child(static_cast<size_t>(n0), -1);  // first of the two halves
+  std::vector<int> split0;                               // split level-0 tiles, ascending
   i64 base = 0, np = n0;
   for (int level = 0; np > 0; ++level) {
     if (level > 0)
@@ -459,6 +461,7 @@ int try_row_plan(dm_ctx* c) {
       if (tl.y < 2) return DM_OK;  // one edge does not fit: Morton plan
       const int h = tl.y >= 4 ? (tl.y / 2 + 1) & ~1 : 1;  // even splits keep e0 even
       child[static_cast<size_t>(base + i)] = static_cast<int>(n0 + static_cast<i64>(extra.size()));
+      if (level == 0) split0.push_back(static_cast<int>(i));
       extra.push_back(make_int2(tl.x, h));
       extra.push_back(make_int2(tl.x + h, tl.y - h));
     }
@@ -471,29 +474,38 @@ int try_row_plan(dm_ctx* c) {
   }
   clk.mark("row tiles: build + split");
   child.resize(static_cast<size_t>(n0) + extra.size(), -1);
-  // final order: every level-0 tile, or its halves in place, depth first
-  // (only split tiles need the stack)
-  std::vector<int> order;
-  order.reserve(static_cast<size_t>(n0) + extra.size());
+  // final order: every level-0 tile, or its halves in place, depth first;
+  // runs of unsplit level-0 tiles are written as ranges, only the split
+  // tiles (their ids are ascending in split0) walk the stack
+  std::vector<int> order(static_cast<size_t>(n0) + extra.size());
+  size_t w = 0;
   std::vector<int> stack;
-  for (i64 i = 0; i < n0; ++i) {
-    if (child[static_cast<size_t>(i)] < 0) {
-      order.push_back(static_cast<int>(i));
-      continue;
-    }
-    stack.push_back(static_cast<int>(i));
+  i64 prev = 0;
+  auto expand = [&](int root) {
+    stack.push_back(root);
     while (!stack.empty()) {
       const int pv = stack.back();
       stack.pop_back();
       const int ch = child[static_cast<size_t>(pv)];
       if (ch < 0) {
-        order.push_back(pv);
+        order[w++] = pv;
       } else {
         stack.push_back(ch + 1);
         stack.push_back(ch);
       }
     }
+  };
+  for (const int sp : split0) {
+    std::iota(order.begin() + static_cast<std::ptrdiff_t>(w),
+              order.begin() + static_cast<std::ptrdiff_t>(w + (sp - prev)), static_cast<int>(prev));
+    w += static_cast<size_t>(sp - prev);
+    expand(sp);
+    prev = sp + 1;
   }
+  std::iota(order.begin() + static_cast<std::ptrdiff_t>(w),
+            order.begin() + static_cast<std::ptrdiff_t>(w + (n0 - prev)), static_cast<int>(prev));
+  w += static_cast<size_t>(n0 - prev);
+  order.resize(w);
   const i64 nt = static_cast<i64>(order.size());
   clk.mark("row tiles: host order");
   if (static_cast<double>(nt) > split_max * static_cast<double>(n0)) return DM_OK;
