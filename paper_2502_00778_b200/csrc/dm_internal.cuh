@@ -239,6 +239,7 @@ struct dm_ctx {
   dm::DevBuf<dm::u32> cnt, fill;
   dm::DevBuf<dm::u64> tmp64;
   dm::DevBuf<dm::u32> seg_big;  // segment_sort: ids of segments longer than a warp's
+  dm::DevBuf<dm::u32> seg_med;  // segment_sort (u32): ids of segments longer than a lane's
   dm::Arena arena;              // plan temporaries (rings.cu)
   dm::DevBuf<dm::u32> scan_tmp;
   dm::DevBuf<dm::u64> scan_tmp64;

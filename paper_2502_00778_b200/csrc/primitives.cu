@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "dm_internal.cuh"
+#include "sortnet.cuh"
 
 namespace dm {
 
@@ -211,6 +212,97 @@ __global__ void __launch_bounds__(256)
     }
   }
   for (int i = lane; i < n; i += 32) data[b + i] = buf[i];
+}
+
+// ---- small segments of unique u32 keys (the incoming-edge and node-element
+// CSRs: ~7 and ~24 keys per node): a lane sorts a whole segment in
+// registers with a sorting network (sortnet.cuh) instead of a warp per
+// segment.  A warp takes 32 consecutive segments; their contiguous key range
+// is staged in shared memory when it fits.  Longer segments are listed for
+// the warp rank sort (<= kWarpSeg keys) or the block sort.
+constexpr int kSmallSeg = 32;
+constexpr int kSmallStage = 1024;
+
+template <int N>
+__device__ __forceinline__ void lane_sort_segment(u32* p, int n) {  // p: shared or global
+  u32 a[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = i < n ? p[i] : 0xffffffffu;
+  oem_sort<N>(a);
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (i < n) p[i] = a[i];
+}
+
+__global__ void __launch_bounds__(256)
+    k_segsort_small_u32(u32* data, const u32* seg, i64 nseg, u32* med, int* nmed, u32* big,
+                        int* nbig) {
+  constexpr unsigned F = 0xffffffffu;
+  __shared__ u32 stage[8][kSmallStage];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 s0 = (static_cast<i64>(blockIdx.x) * 8 + warp) * 32;
+  if (s0 >= nseg) return;
+  const i64 s = s0 + lane;
+  const bool valid = s < nseg;
+  const u32 b = valid ? seg[s] : 0u, e = valid ? seg[s + 1] : 0u;
+  const int n = static_cast<int>(e - b);
+  if (valid && n > kSmallSeg) {
+    if (n > kWarpSeg) big[atomicAdd(nbig, 1)] = static_cast<u32>(s);
+    else med[atomicAdd(nmed, 1)] = static_cast<u32>(s);
+  }
+  const int nl = valid && n <= kSmallSeg ? n : 0;
+  const int nmax = __reduce_max_sync(F, static_cast<unsigned>(nl));
+  if (nmax <= 1) return;
+  const int last = 31 - __clz(__ballot_sync(F, valid));
+  const u32 b0 = __shfl_sync(F, b, 0), bend = __shfl_sync(F, e, last);
+  const bool staged = bend - b0 <= static_cast<u32>(kSmallStage);
+  u32* buf = stage[warp];
+  if (staged)
+    for (u32 i = lane; i < bend - b0; i += 32) buf[i] = data[b0 + i];
+  __syncwarp();
+  u32* p = staged ? buf + (b - b0) : data + b;
+  if (nmax <= 8) lane_sort_segment<8>(p, nl);
+  else if (nmax <= 16) lane_sort_segment<16>(p, nl);
+  else lane_sort_segment<32>(p, nl);
+  __syncwarp();
+  if (staged)
+    for (u32 i = lane; i < bend - b0; i += 32) data[b0 + i] = buf[i];
+}
+
+// Warp rank sort of the listed segments (kSmallSeg < n <= kWarpSeg unique
+// u32 keys), grid-stride over the list.
+__global__ void __launch_bounds__(256)
+    k_segsort_warp_list_u32(u32* data, const u32* seg, const u32* list, const int* nlist) {
+  __shared__ __align__(16) u32 sbuf[8][kWarpSeg + 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cnt = *nlist;
+  for (int q = blockIdx.x * 8 + warp; q < cnt; q += gridDim.x * 8) {
+    const u32 s = list[q];
+    const u32 b = seg[s];
+    const int n = static_cast<int>(seg[s + 1] - b);
+    u32* buf = sbuf[warp];
+    u32 key[4];
+    int rk[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      key[r] = i < n ? data[b + i] : 0xffffffffu;
+      buf[i] = key[r];
+    }
+    if (lane < 2) buf[kWarpSeg + lane] = 0xffffffffu;
+    __syncwarp();
+    const int nr = (n + 31) >> 5;
+    if (nr == 2) rank_keys<u32, true, 2>(buf, n, key, lane, rk);
+    else if (nr == 3) rank_keys<u32, true, 3>(buf, n, key, lane, rk);
+    else rank_keys<u32, true, 4>(buf, n, key, lane, rk);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (lane + 32 * r < n) buf[rk[r]] = key[r];
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) data[b + i] = buf[i];
+    __syncwarp();
+  }
 }
 
 // Unique u64 keys (K1's (k << 32 | e*L + l) items, the boundary-edge keys):
@@ -489,6 +581,13 @@ int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg, u32* ucnt) {
       DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg,
                 big.p, nbig, ucnt);
     }
+  } else if constexpr (sizeof(K) == 4 && kUnique) {
+    DevBuf<u32>& med = c->seg_med;
+    DM_CK(c, med.ensure(static_cast<size_t>(nseg)));
+    int* nmed = c->flag.p + 2;
+    DM_LAUNCH(c, k_segsort_small_u32, grid_for(nseg, 256), 256, 0, data, seg, nseg, med.p, nmed,
+              big.p, nbig);
+    DM_LAUNCH(c, k_segsort_warp_list_u32, 148 * 8, 256, 0, data, seg, med.p, nmed);
   } else {
     DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg, big.p,
               nbig, ucnt);
