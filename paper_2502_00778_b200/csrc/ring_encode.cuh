@@ -62,6 +62,47 @@ __device__ RingWalk ring_walk_encode(int j, int k, int pb, int n, const int32_t*
     a[i] = o[0];
     b[i] = o[1];
   }
+  // The walk from `start`: the next element is the first unused one holding
+  // the current node.  Emits m_0 .. m_n; `end` is the last node.
+  auto walk = [&](int start, int& end) -> int {
+    emit(0, start);
+    unsigned used = 0;
+    int cur = start, sg0 = 0;
+    for (int step = 0; step < n; ++step) {
+      int pick = -1;
+      for (int i = 0; i < n; ++i)
+        if (!(used >> i & 1u) && (a[i] == cur || b[i] == cur)) {
+          pick = i;
+          break;
+        }
+      if (pick < 0) return kRingNonManifold;
+      used |= 1u << pick;
+      const int nxt = a[pick] == cur ? b[pick] : a[pick];
+      const int sg = perm_sign(k, cur, nxt, p0[pick], p1[pick], p2[pick]);
+      if (step == 0) sg0 = sg;
+      else if (sg != sg0) return kRingMixedSign;
+      emit(1 + step, nxt);
+      cur = nxt;
+    }
+    r.sign = sg0 < 0 ? -1 : 1;
+    end = cur;
+    return 0;
+  };
+  // A closed ring (every node in exactly two elements: the interior edges)
+  // starts at a[0].  The XOR of all nodes is 0 then; try that walk first and
+  // keep it if it closes -- the same start and codes as the full search
+  // below, without its n^2 node counts.
+  int x = 0;
+  for (int i = 0; i < n; ++i) x ^= a[i] ^ b[i];
+  if (x == 0 && n >= 3) {
+    int end = -1;
+    if (walk(a[0], end) == 0 && end == a[0]) {
+      r.start = a[0];
+      r.closed = true;
+      return r;
+    }
+  }
+  // open chain (or not a fan): the start is the smallest node seen once
   int start = -1;
   for (int i = 0; i < n; ++i)
     for (int s = 0; s < 2; ++s) {
@@ -73,33 +114,10 @@ __device__ RingWalk ring_walk_encode(int j, int k, int pb, int n, const int32_t*
   const bool open = start >= 0;
   if (start < 0) start = a[0];
   r.start = start;
-  emit(0, start);
-  unsigned used = 0;
-  int cur = start, sg0 = 0;
-  for (int step = 0; step < n; ++step) {
-    int pick = -1;
-    for (int i = 0; i < n; ++i)
-      if (!(used >> i & 1u) && (a[i] == cur || b[i] == cur)) {
-        pick = i;
-        break;
-      }
-    if (pick < 0) {
-      r.fail = kRingNonManifold;
-      return r;
-    }
-    used |= 1u << pick;
-    const int nxt = a[pick] == cur ? b[pick] : a[pick];
-    const int sg = perm_sign(k, cur, nxt, p0[pick], p1[pick], p2[pick]);
-    if (step == 0) sg0 = sg;
-    else if (sg != sg0) {
-      r.fail = kRingMixedSign;
-      return r;
-    }
-    emit(1 + step, nxt);
-    cur = nxt;
-  }
-  r.sign = sg0 < 0 ? -1 : 1;
-  r.closed = !open && cur == start && n >= 3;
+  int end = -1;
+  r.fail = walk(start, end);
+  if (r.fail) return r;
+  r.closed = !open && end == start && n >= 3;
   return r;
 }
 

@@ -291,12 +291,16 @@ __global__ void __launch_bounds__(kRowTile)
   const int* h = reinterpret_cast<const int*>(tb);
   const int e0 = h[0], cnt = h[1];
   if (t >= cnt) return;
-  auto slot = [&](int v) -> int {
-    for (int r = 0; r < nr; ++r) {
-      const int2 x = R[r];
-      if (v >= x.x && v < x.x + (x.y & 0xffff)) return (x.y >> 16) + (v - x.x);
+  auto slot = [&](int v) -> int {  // the runs ascend by first node: binary search
+    if (nr == 0 || v < R[0].x) return -1;
+    int lo = 0, hi = nr - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (R[mid].x <= v) lo = mid;
+      else hi = mid - 1;
     }
-    return -1;
+    const int2 x = R[lo];
+    return v < x.x + (x.y & 0xffff) ? (x.y >> 16) + (v - x.x) : -1;
   };
   uint8_t* blk = tb + reinterpret_cast<const uint16_t*>(h + 2)[t >> 5];
   const int e = e0 + blk[32 + lane];
