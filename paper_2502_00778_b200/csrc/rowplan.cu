@@ -55,10 +55,18 @@ constexpr int kRTTooManyNodes = 1;
 constexpr int kRTTooManyRuns = 2;
 constexpr int kRTTooManyCodes = 4;
 
+constexpr int kBitPairs = 4096 * 32;  // pair bitmap: a tile's node-pair span up to 131072
+
 struct RTShared {
-  int hs[kRTHash];
-  int uq[kRTUniqCap];
+  union {
+    struct {
+      int hs[kRTHash];
+      int uq[kRTUniqCap];
+    } h;                       // node set as a hash set (wide node spans)
+    unsigned bm[kBitPairs / 32];  // node pairs as a bitmap over the tile's span
+  } u;
   unsigned key[kRTThreads], ktmp[kRTThreads];
+  int vmin[8], vmax[8], hcount[8];
   int2 heads[kRowRuns];  // run heads {first pair, pairs}, unsorted
   int n_uniq;
   int nruns, nslots;
@@ -118,37 +126,50 @@ __global__ void __launch_bounds__(kRTThreads)
   const i64 p = static_cast<i64>(base) + blockIdx.x;
   const int2 cd = cand[blockIdx.x];
   const int e0 = cd.x, cnt = cd.y;
-  for (int i = t; i < kRTHash; i += kRTThreads) S.hs[i] = -1;
-  if (t == 0) S.n_uniq = 0;
+  if (t == 0) {
+    S.n_uniq = 0;
+    S.nruns = 0;
+  }
   if (t < 8) S.wmax[t] = 0;
-  __syncthreads();
   auto insert = [&](int v) {
     unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 21;  // 11 bits
     for (int probe = 0; probe < kRTHash; ++probe, h = (h + 1) & (kRTHash - 1)) {
-      const int old = atomicCAS(&S.hs[h], -1, v);
+      const int old = atomicCAS(&S.u.h.hs[h], -1, v);
       if (old == -1) {
         const int q = atomicAdd(&S.n_uniq, 1);
-        if (q < kRTUniqCap) S.uq[q] = v;
+        if (q < kRTUniqCap) S.u.h.uq[q] = v;
         return;
       }
       if (old == v) return;
     }
   };
-  int n_inc = 0;
+  int n_inc = 0, pb = 0, nq = 0;
+  int2 jk = make_int2(0, 0);
   unsigned key = 0xffffff00u | static_cast<unsigned>(t);  // idle lanes: unique, after every edge
   if (t < cnt) {
     const int e = e0 + t;
-    const int2 jk = edges[e];
-    insert(jk.x);
-    insert(jk.y);
-    const int pb = inc_ptr[e];
+    jk = edges[e];
+    pb = inc_ptr[e];
     n_inc = inc_ptr[e + 1] - pb;
-    int last = -1;
     // the ring nodes: the two others of each element (a side-list edge, more
-    // than kRingMax incidences, needs only j and k in the table); element
-    // ids and rows are loaded eight at a time (two round trips per batch
-    // instead of two per element)
-    const int nq = n_inc > kRingMax ? 0 : n_inc;
+    // than kRingMax incidences, needs only j and k in the table)
+    nq = n_inc > kRingMax ? 0 : n_inc;
+    // direction-major: index of the edge inside its origin row, then origin
+    key = (static_cast<unsigned>(e - static_cast<int>(os[jk.x])) << 8) | static_cast<unsigned>(t);
+    if (by_len)  // ring length first (warps of equal trip counts: on the Kuhn grids the
+                 // even/odd cube orientation splits a direction into 4- and 6-rings)
+      key = static_cast<unsigned>(min(n_inc, 31)) << 27 |
+            min(static_cast<unsigned>(e - static_cast<int>(os[jk.x])), (1u << 19) - 1u) << 8 |
+            static_cast<unsigned>(t);
+  }
+  S.key[t] = key;
+  // this edge's table nodes: j, k and its ring's nodes (element ids and rows
+  // loaded eight at a time: two round trips per batch)
+  auto for_nodes = [&](auto&& fn) {
+    if (t >= cnt) return;
+    fn(jk.x);
+    fn(jk.y);
+    int last = -1;
     for (int q0 = 0; q0 < nq; q0 += 8) {
       int id[8];
       int4 rows[8];
@@ -164,52 +185,123 @@ __global__ void __launch_bounds__(kRTThreads)
 #pragma unroll
         for (int a = 0; a < 4; ++a)
           if (vs[a] != jk.x && vs[a] != jk.y && vs[a] != last) {
-            insert(vs[a]);
+            fn(vs[a]);
             last = vs[a];
           }
       }
     }
-    // direction-major: index of the edge inside its origin row, then origin
-    key = (static_cast<unsigned>(e - static_cast<int>(os[jk.x])) << 8) | static_cast<unsigned>(t);
-    if (by_len)  // ring length first (warps of equal trip counts: on the Kuhn grids the
-                 // even/odd cube orientation splits a direction into 4- and 6-rings)
-      key = static_cast<unsigned>(min(n_inc, 31)) << 27 |
-            min(static_cast<unsigned>(e - static_cast<int>(os[jk.x])), (1u << 19) - 1u) << 8 |
-            static_cast<unsigned>(t);
-  }
-  S.key[t] = key;
-  __syncthreads();
-  const int nu = S.n_uniq;
-  int badbits = nu > kRTUniqCap ? kRTTooManyNodes : 0;
-  if (badbits) {
-    if (t == 0) bad[p] = static_cast<uint8_t>(badbits);
-    return;
-  }
-  // runs of node pairs straight from the hash set (no sorted node list): a
-  // present pair p (node 2p or 2p + 1 in the tile) opens a run iff pair
-  // p - 1 is absent; the run extends while the next pairs are present.  The
-  // <= kRowRuns heads are then ordered by pair and take their table slots.
-  auto present = [&](int v) -> bool {
-    if (v < 0) return false;
-    unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 21;
-    for (int probe = 0; probe < kRTHash; ++probe, h = (h + 1) & (kRTHash - 1)) {
-      const int x = S.hs[h];
-      if (x == v) return true;
-      if (x == -1) return false;
-    }
-    return false;
   };
-  if (t == 0) S.nruns = 0;
-  __syncthreads();
-  for (int i = t; i < nu; i += kRTThreads) {
-    const int v = S.uq[i], pr = v >> 1;
-    const bool rep = !(v & 1) || !present(v - 1);  // one representative per pair
-    if (rep && !present(2 * pr - 2) && !present(2 * pr - 1)) {
-      int len = 1;
-      while (present(2 * (pr + len)) || present(2 * (pr + len) + 1)) ++len;
-      const int r = atomicAdd(&S.nruns, 1);
-      if (r < kRowRuns) S.heads[r] = make_int2(pr, len);
+  // the tile's node-pair span: a bitmap when it fits, else the hash set
+  {
+    int lo = 0x7fffffff, hi = -1;
+    for_nodes([&](int v) {
+      lo = min(lo, v);
+      hi = max(hi, v);
+    });
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) {
+      S.vmin[t >> 5] = lo;
+      S.vmax[t >> 5] = hi;
     }
+  }
+  __syncthreads();
+  int vlo = 0x7fffffff, vhi = -1;
+#pragma unroll
+  for (int w = 0; w < kRTThreads / 32; ++w) {
+    vlo = min(vlo, S.vmin[w]);
+    vhi = max(vhi, S.vmax[w]);
+  }
+  const int pmin = vlo >> 1;
+  const int npairs = vhi >= vlo ? (vhi >> 1) - pmin + 1 : 0;
+  const bool bits = npairs <= kBitPairs;
+  const int nw = (npairs + 31) >> 5;
+  if (bits) {
+    for (int i = t; i < nw; i += kRTThreads) S.u.bm[i] = 0u;
+  } else {
+    for (int i = t; i < kRTHash; i += kRTThreads) S.u.h.hs[i] = -1;
+  }
+  __syncthreads();
+  if (bits) {
+    for_nodes([&](int v) {
+      const int q = (v >> 1) - pmin;
+      atomicOr(&S.u.bm[q >> 5], 1u << (q & 31));
+    });
+  } else {
+    for_nodes(insert);
+  }
+  __syncthreads();
+  int badbits = 0;
+  if (bits) {
+    // runs: a set pair after a clear one opens a run; a thread scans a slice
+    // of words, runs are numbered in pair order by a block scan of the heads
+    const int W = (nw + kRTThreads - 1) / kRTThreads;
+    const int w0 = min(nw, t * W), w1 = min(nw, w0 + W);
+    auto heads_of = [&](int i) -> unsigned {
+      const unsigned x = S.u.bm[i], prev = i > 0 ? S.u.bm[i - 1] >> 31 : 0u;
+      return x & ~((x << 1) | prev);
+    };
+    int c = 0;
+    for (int i = w0; i < w1; ++i) c += __popc(heads_of(i));
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) S.hcount[t >> 5] = incl;
+    __syncthreads();
+    int r = incl - c;
+    for (int w = 0; w < (t >> 5); ++w) r += S.hcount[w];
+    if (t == kRTThreads - 1) S.nruns = r + c;
+    for (int i = w0; i < w1; ++i) {
+      unsigned h = heads_of(i);
+      while (h) {
+        const int b = __ffs(h) - 1;
+        h &= h - 1;
+        if (r < kRowRuns) {
+          // the run ends at the next clear pair
+          int wi = i;
+          unsigned z = ~S.u.bm[wi] & (0xffffffffu << b);
+          while (!z && ++wi < nw) z = ~S.u.bm[wi];
+          const int end = z ? 32 * wi + __ffs(z) - 1 : 32 * nw;
+          S.heads[r] = make_int2(pmin + 32 * i + b, end - (32 * i + b));
+        }
+        ++r;
+      }
+    }
+  } else {
+    const int nu = S.n_uniq;
+    if (nu > kRTUniqCap) badbits = kRTTooManyNodes;
+    if (!badbits) {
+      // runs of node pairs straight from the hash set (no sorted node list): a
+      // present pair p (node 2p or 2p + 1 in the tile) opens a run iff pair
+      // p - 1 is absent; the run extends while the next pairs are present.
+      auto present = [&](int v) -> bool {
+        if (v < 0) return false;
+        unsigned h = (static_cast<unsigned>(v) * 2654435761u) >> 21;
+        for (int probe = 0; probe < kRTHash; ++probe, h = (h + 1) & (kRTHash - 1)) {
+          const int x = S.u.h.hs[h];
+          if (x == v) return true;
+          if (x == -1) return false;
+        }
+        return false;
+      };
+      for (int i = t; i < nu; i += kRTThreads) {
+        const int v = S.u.h.uq[i], pr = v >> 1;
+        const bool rep = !(v & 1) || !present(v - 1);  // one representative per pair
+        if (rep && !present(2 * pr - 2) && !present(2 * pr - 1)) {
+          int len = 1;
+          while (present(2 * (pr + len)) || present(2 * (pr + len) + 1)) ++len;
+          const int r = atomicAdd(&S.nruns, 1);
+          if (r < kRowRuns) S.heads[r] = make_int2(pr, len);
+        }
+      }
+    }
+  }
+  if (__syncthreads_or(badbits)) {
+    if (t == 0) bad[p] = static_cast<uint8_t>(kRTTooManyNodes);
+    return;
   }
   warp_merge_sort_u32(S.key, S.ktmp, t);  // lane order (its barriers also publish the heads)
   if (t < 32) {  // order the heads by pair, then slot offsets
