@@ -539,7 +539,12 @@ def run_ours(args, world, rank, local, dist):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
-            "extra": {"edges_ms": edges_ms, "edges_ms_first_call": edges_ms_first,
+            "extra": {"throughput": {
+                          "step_tets_per_s": value, "step_edges_per_s": world * K * ne / (total_ms / 1e3),
+                          "element_loop_edges_per_s": ne / (elem_ms / 1e3),
+                          "edge_extraction_tets_per_s": mesh.num_elements() / (edges_ms / 1e3),
+                          "edge_extraction_edges_per_s": ne / (edges_ms / 1e3)},
+                      "edges_ms": edges_ms, "edges_ms_first_call": edges_ms_first,
                       "plan_ms_first_call": plan_ms, "plan_ms_rebuild": replan_ms,
                       "plan": eng.plan_info(), "edges_bytes": B["edges"],
                       "edges_GBps": B["edges"] / (edges_ms / 1e3) / 1e9,
