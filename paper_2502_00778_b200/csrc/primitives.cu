@@ -572,15 +572,8 @@ int segment_sort(dm_ctx* c, K* data, const u32* seg, i64 nseg, u32* ucnt) {
   DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
   int* nbig = c->flag.p + 1;
   if constexpr (sizeof(K) == 8 && kUnique) {
-    static const char* r64 = std::getenv("DUALMESH_SEGSORT_RANK64");  // A/B switch
-    const bool rank64 = r64 && *r64 == '1';
-    if (!rank64) {
-      const unsigned grid = static_cast<unsigned>(std::min<i64>(grid_for(nseg, 256), 148 * 8));
-      DM_LAUNCH(c, k_segsort_u64u_warp, grid, 256, 0, data, seg, nseg, big.p, nbig, ucnt);
-    } else {
-      DM_LAUNCH(c, (k_segsort_warp<K, kUnique>), grid_for(nseg, 8), 256, 0, data, seg, nseg,
-                big.p, nbig, ucnt);
-    }
+    const unsigned grid = static_cast<unsigned>(std::min<i64>(grid_for(nseg, 256), 148 * 8));
+    DM_LAUNCH(c, k_segsort_u64u_warp, grid, 256, 0, data, seg, nseg, big.p, nbig, ucnt);
   } else if constexpr (sizeof(K) == 4 && kUnique) {
     DevBuf<u32>& med = c->seg_med;
     DM_CK(c, med.ensure(static_cast<size_t>(nseg)));
