@@ -493,6 +493,10 @@ int segment_sort_unique_u64(dm_ctx* c, u64* data, const u32* seg, i64 nseg, u32*
 int segment_sort_u32(dm_ctx* c, u32* data, const u32* seg, i64 nseg);
 // (key, value) pairs sorted lexicographically within each segment.
 int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg);
+// Global sort of n u64 keys into keys_out; with vals, (key, value) pairs
+// lexicographically (stable-sort order for values entering ascending);
+// without, the keys must be unique.
+int sort_u64(dm_ctx* c, const u64* keys, const u32* vals, i64 n, u64* keys_out, u32* vals_out);
 
 __global__ void k_tile_bptr(const u64* bedge, u32 n, i64 ne, i64 ntiles, u32* tile_bptr);
 

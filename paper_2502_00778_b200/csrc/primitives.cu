@@ -732,6 +732,68 @@ int segment_sort_kv(dm_ctx* c, u64* keys, u32* vals, const u32* seg, i64 nseg) {
   return f ? sort_huge_segments_kv(c, keys, vals, seg) : DM_OK;
 }
 
+// ---- global sort of u64 keys (with optional u32 values): buckets on the
+// top 16 significant key bits (count, scan, atomic placement), then the
+// segmented sort orders each bucket -- (key, value) lexicographically, which
+// is a stable sort's order when the values enter in ascending order.  The
+// Morton orders of the ring plan (rings.cu) and its boundary lists use it.
+namespace {
+__global__ void k_umax64(const u64* __restrict__ k, i64 n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    m = max(m, static_cast<unsigned long long>(k[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+__global__ void k_bkt_count(const u64* __restrict__ k, i64 n, int shift, u32* __restrict__ cnt) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(cnt + (k[i] >> shift), 1u);
+}
+__global__ void k_bkt_place(const u64* __restrict__ k, const u32* __restrict__ v, i64 n,
+                            int shift, const u32* __restrict__ start, u32* __restrict__ fill,
+                            u64* __restrict__ ko, u32* __restrict__ vo) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 key = k[i];
+  const u64 b = key >> shift;
+  const u32 pos = start[b] + atomicAdd(fill + b, 1u);
+  ko[pos] = key;
+  if (vo) vo[pos] = v[i];
+}
+}  // namespace
+
+int sort_u64(dm_ctx* c, const u64* keys, const u32* vals, i64 n, u64* keys_out, u32* vals_out) {
+  if (n <= 0) return DM_OK;
+  DevBuf<unsigned long long> mx;
+  DM_CK(c, mx.ensure(1));
+  DM_CK(c, cudaMemsetAsync(mx.p, 0, sizeof(unsigned long long), c->stream));
+  DM_LAUNCH(c, k_umax64, static_cast<unsigned>(std::min<i64>(grid_for(n, 256), 1184)), 256, 0,
+            keys, n, mx.p);
+  unsigned long long hmax = 0;
+  DM_CK(c, cudaMemcpyAsync(&hmax, mx.p, sizeof(hmax), cudaMemcpyDeviceToHost, c->stream));
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  const int bits = hmax ? 64 - __builtin_clzll(hmax) : 1;
+  const int shift = bits > 16 ? bits - 16 : 0;
+  const i64 nb = static_cast<i64>(hmax >> shift) + 1;
+  DevBuf<u32> start, fill;
+  DM_CK(c, start.ensure(static_cast<size_t>(nb + 1)));
+  DM_CK(c, fill.ensure(static_cast<size_t>(nb + 1)));
+  DM_CK(c, cudaMemsetAsync(start.p, 0, (nb + 1) * sizeof(u32), c->stream));
+  DM_CK(c, cudaMemsetAsync(fill.p, 0, (nb + 1) * sizeof(u32), c->stream));
+  DM_LAUNCH(c, k_bkt_count, grid_for(n, 256), 256, 0, keys, n, shift, start.p);
+  int st = scan_exclusive(c, start.p, start.p, nb);
+  if (st) return st;
+  DM_LAUNCH(c, k_bkt_place, grid_for(n, 256), 256, 0, keys, vals, n, shift, start.p, fill.p,
+            keys_out, vals_out);
+  st = vals_out ? segment_sort_kv(c, keys_out, vals_out, start.p, nb)
+                : segment_sort_unique_u64(c, keys_out, start.p, nb, nullptr);
+  if (st) return st;
+  DM_CK(c, cudaStreamSynchronize(c->stream));  // the bucket scratch dies here
+  return DM_OK;
+}
+
 int scan_exclusive(dm_ctx* c, const u32* in, u32* out, i64 n) {
   DM_CK(c, c->scan_tmp.ensure(static_cast<size_t>(scan_tmp_need(n))));
   return scan_rec<u32>(c, in, out, n, c->scan_tmp.p);

@@ -53,7 +53,6 @@
 // incidences or a non-manifold fan (the walk does not consume every incident
 // element) sets ring_ok = false and the GATHER path falls back to the
 // bit-exact row-table kernel.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <cmath>
 #include <cstdlib>
@@ -549,14 +548,17 @@ __global__ void k_morton(const d4* __restrict__ x4, i64 nv, double lx, double ly
 // in that coordinate (sorted) scaled to `cells` -- equal node counts per slab,
 // so graded / stretched grids (boundary layers) get cells of ~cell_nodes
 // nodes like uniform ones.
-__global__ void k_axis_key(const d4* __restrict__ x4, i64 nv, int axis, u64* __restrict__ key,
-                           int32_t* __restrict__ id) {
+// Axis order key: the coordinate quantised to 32 bits over the bounding box
+// (uniform buckets for the bucketed sort), then the node id.  The cells only
+// shape the plan's layout (performance), never the results.
+__global__ void k_axis_key(const d4* __restrict__ x4, i64 nv, int axis, double lo, double sc,
+                           u64* __restrict__ key, int32_t* __restrict__ id) {
   const i64 v = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const d4 r = x4[v];
-  const double x = axis == 0 ? r.x : (axis == 1 ? r.y : r.z);
-  const u64 b = static_cast<u64>(__double_as_longlong(x));
-  key[v] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // order-preserving
+  const double f = ((axis == 0 ? r.x : (axis == 1 ? r.y : r.z)) - lo) * sc;
+  const u64 q = f <= 0.0 ? 0ull : (f >= 4294967295.0 ? 4294967295ull : static_cast<u64>(f));
+  key[v] = q << 32 | static_cast<u64>(v);
   id[v] = static_cast<int32_t>(v);
 }
 
@@ -729,19 +731,9 @@ int build_edge_order(dm_ctx* c) {
   DM_CK(c, i0.ensure(nv));
   DM_CK(c, c->morder.ensure(nv));
   int32_t* i1p = c->morder.p;
-  ScratchBuf<unsigned char> tmp(c->arena, arena_block(c));
-  size_t tb = 0;
-  auto radix = [&]() -> int {  // (k0, i0) -> sorted ids in i1p
-    size_t need = 0;
-    DM_CK(c, cub::DeviceRadixSort::SortPairs(nullptr, need, k0.p, k1.p, i0.p, i1p, nv, 0, 63,
-                                             c->stream));
-    if (need > tb) {
-      DM_CK(c, tmp.ensure(need));
-      tb = need;
-    }
-    DM_CK(c, cub::DeviceRadixSort::SortPairs(tmp.p, need, k0.p, k1.p, i0.p, i1p, nv, 0, 64,
-                                             c->stream));
-    return DM_OK;
+  auto radix = [&]() -> int {  // (k0, i0) -> ids in key order (ties: ascending id) in i1p
+    return sort_u64(c, k0.p, reinterpret_cast<const u32*>(i0.p), nv, k1.p,
+                    reinterpret_cast<u32*>(i1p));
   };
   auto sort_nodes = [&](int cells) -> int {
     DM_LAUNCH(c, k_morton, grid_for(nv, 256), 256, 0, c->x4.p, nv, lo[0], lo[1], lo[2], sc,
@@ -776,7 +768,10 @@ int build_edge_order(dm_ctx* c) {
     ScratchBuf<u32> cellpack(c->arena, arena_block(c));
     DM_CK(c, cellpack.ensure(nv));
     for (int axis = 0; axis < 3; ++axis) {
-      DM_LAUNCH(c, k_axis_key, grid_for(nv, 256), 256, 0, c->x4.p, nv, axis, k0.p, i0.p);
+      const double ax_ext = hi[axis] - lo[axis];
+      const double ax_sc = ax_ext > 0.0 && std::isfinite(ax_ext) ? 4294967295.0 / ax_ext : 0.0;
+      DM_LAUNCH(c, k_axis_key, grid_for(nv, 256), 256, 0, c->x4.p, nv, axis, lo[axis], ax_sc,
+                k0.p, i0.p);
       st = radix();
       if (st) return st;
       DM_LAUNCH(c, k_axis_cell, grid_for(nv, 256), 256, 0, i1p, nv, axis, cells, cellpack.p);
@@ -826,13 +821,8 @@ int build_edge_order(dm_ctx* c) {
     ScratchBuf<u64> bk(c->arena, arena_block(c));
     DM_CK(c, bk.ensure(nb));
     DM_LAUNCH(c, k_bkey, grid_for(nb, 256), 256, 0, c->bedge.p, nb, pinv.p, bk.p);
-    const int hb = 32 + bits_for(static_cast<u64>(ne));
-    tb = 0;
-    DM_CK(c, cub::DeviceRadixSort::SortKeys(nullptr, tb, bk.p, c->bedge_p.p, nb, 0, hb,
-                                            c->stream));
-    DM_CK(c, tmp.ensure(tb));
-    DM_CK(c, cub::DeviceRadixSort::SortKeys(tmp.p, tb, bk.p, c->bedge_p.p, nb, 0, hb,
-                                            c->stream));
+    st = sort_u64(c, bk.p, nullptr, nb, c->bedge_p.p, nullptr);  // (position, facet): unique
+    if (st) return st;
   }
   DM_LAUNCH(c, k_tile_bptr, grid_for(ntiles + 1, 256), 256, 0, c->bedge_p.p,
             static_cast<u32>(nb), ne, ntiles, c->tile_bptr_p.p);
