@@ -955,12 +955,15 @@ int ensure_rings(dm_ctx* c) {
   DM_LAUNCH(c, k_ring_meta, grid_for(ntiles, 256), 256, 0, wstart.p, c->tnode_cnt.p,
             c->tile_bptr_p.p, nwarps, ntiles, c->ring_meta.p);
   clk.mark("ring codes");
-  // bank-conflict-aware slots for 8-bit plans (env DUALMESH_PLAN_COLOR=0 turns
-  // it off): C5 element loop 2.36 -> 2.25 ms for ~0.1 s more plan time
+  // bank-conflict-aware slots for 8-bit plans: by default only for coherent
+  // numberings (the 2-3-flipped grid: element loop 0.712 -> 0.694 ms); on a
+  // randomly numbered grid it no longer pays (C3: 0.562 ms without, 0.568-
+  // 0.573 ms with 1-8 rounds, plus ~20 ms of plan; tools/color_rounds_sweep.py).
+  // env DUALMESH_PLAN_COLOR=0 / 1 forces it off / on.
   c->plan_colored = false;
   if (c->code_width == 1) {
     const char* pc = std::getenv("DUALMESH_PLAN_COLOR");
-    if (!pc || std::atoi(pc) != 0) {
+    if (pc ? std::atoi(pc) != 0 : !c->vol_by_rank) {
       DM_LAUNCH(c, k_tile_color_warp, static_cast<unsigned>(ntiles), kTileEdges, 0,
                 c->rcodes.p, c->ring_meta.p, c->tnodes.p, static_cast<int>(ntiles), ne,
                 color_rounds());
