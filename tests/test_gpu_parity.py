@@ -784,3 +784,38 @@ def test_flipped_unstructured_grid(engine, oracle, permuted):
     np.testing.assert_array_equal(engine.get_navs(), want)
     engine.navs(TR, GATHER)
     assert per_vector_rel(engine.get_navs(), oracle.navs_traditional(m, e, o), 3) <= 1e-12
+
+
+def test_row_plan_wide_span_hash_path(monkeypatch, oracle):
+    """Row tiles whose node-pair span exceeds the builder's bitmap (131072
+    pairs) take its hash-set path: a Kuhn grid whose upper half of node ids
+    is shifted past 300000 unused ids (isolated nodes) keeps its topology and
+    id order, so its navs are bitwise those of the unshifted grid (the ring
+    encodings, fixed by the element list, are the same), and the plan audit
+    (DUALMESH_PLAN_CHECK=1) accepts the tiles."""
+    from paper_2502_00778_b200 import Engine
+    m = meshgen.tet_cube(24, amp=0.15)
+    nv = m.num_nodes()
+    gap, half = 300_000, nv // 2
+    newid = np.arange(nv, dtype=np.int64)
+    newid[half:] += gap
+    coords = np.zeros((nv + gap, 3))
+    coords[newid] = m.coords.reshape(-1, 3)
+    coords[half:half + gap] = 5.0  # isolated nodes, away from the grid
+    ms = Mesh(3, coords.ravel(), newid[m.elements].astype(np.int32),
+              newid[m.boundary].astype(np.int32))
+    monkeypatch.setenv("DUALMESH_PLAN_CHECK", "1")
+    out = []
+    for mesh in (m, ms):
+        eng = Engine(0)
+        try:
+            eng.set_mesh(mesh)
+            eng.build_edges()
+            eng.navs(DF, GATHER)
+            assert eng.plan_info()["tiles"] == "row"
+            out.append(eng.get_navs())
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(out[0], out[1])
+    e, o = oracle.build_edges(ms)
+    assert per_vector_rel(out[1], oracle.navs_dualfree(ms, e, o), 3) <= 1e-12
