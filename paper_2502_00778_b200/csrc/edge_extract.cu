@@ -10,25 +10,29 @@
 // elements in which j is not the largest node (an "entry" per such element,
 // D per element), each contributing the pairs (j, k) for its nodes k > j.
 //
-//   P1 k_ent_fill    per element: each entry node takes a slot in its
-//                    fixed-capacity bucket row (warp-aggregated atomics) and
-//                    the element id goes there; flags repeated or
-//                    out-of-range nodes and rows that overflow
-//   P3 k_edge_chunks a warp per chunk of 32 consecutive buckets, a lane per
-//                    bucket: the chunk's rows are staged coalesced, each lane
-//                    sorts its entries by element id and its items by
-//                    (k - j, entry rank) with register sorting networks and
-//                    counts its edges and items; a decoupled look-back over
-//                    CTA tiles (8 chunks) gives the first edge id and item
-//                    position; the lanes emit e2l directly and stage inc,
-//                    edges and inc_ptr in shared memory for coalesced
-//                    stores.
+//   k_ent_fill     per element: each entry node takes a slot in its fixed-
+//                  capacity bucket row (runs of adjacent lanes with the same
+//                  node -- a hex's tets share a corner -- take their slots
+//                  with one atomic) and the element id goes there; flags
+//                  repeated or out-of-range nodes and rows that overflow
+//   k_edge_chunks  a warp per chunk of 32 consecutive buckets, a lane per
+//                  bucket: the chunk's rows are staged coalesced, each lane
+//                  sorts its entries by element id and its items by
+//                  (k - j, entry rank) with register sorting networks
+//                  (sortnet.cuh) and counts its edges and items; a
+//                  decoupled look-back over CTA tiles (8 chunks) gives the
+//                  first edge id and item position; the lanes emit e2l
+//                  directly and stage inc, edges and inc_ptr in shared
+//                  memory for coalesced stores.  A narrow variant holds
+//                  rows of <= 21 entries in registers, a wide one <= 25
+//                  (chosen by a k_ent_fill flag).
 //
 // Buckets with more entries than a row holds (Caps::kNe) take a side path
-// before P3: their entries are collected into exact lists, expanded into
-// (k << 32 | e*L + l) items and sorted by the generic segmented sort; their
-// lanes emit from that list.  Meshes with a repeated node inside an element
-// or more than 2^25 nodes take the generic item-sort path (edges.cu).
+// before k_edge_chunks: their entries are collected into exact lists,
+// expanded into (k << 32 | e*L + l) items and sorted by the generic
+// segmented sort; their lanes emit from that list.  Meshes with a repeated
+// node inside an element or more than 2^25 nodes take the generic item-sort
+// path (edges.cu).
 #include <cstdlib>
 #include <utility>
 
@@ -107,7 +111,7 @@ __device__ __forceinline__ void load_nodes(const int32_t* el, i64 e, int (&v)[4]
   }
 }
 
-// ---------------------------------------------------------------- P1
+// ---------------------------------------------------------------- entry rows
 // Node v[p] ranks above r other nodes of its element; with r < D it is the
 // origin of D - r of the element's pairs.  Flags: 1 = node id out of range,
 // 2 = repeated node (the generic path handles the reference's (a, a) pairs).
@@ -281,7 +285,7 @@ __global__ void k_big_items(const int32_t* __restrict__ el, const u32* __restric
   if (count && lane == 0) count[b] = out;
 }
 
-// ---------------------------------------------------------------- P3
+// ---------------------------------------------------------------- chunks
 // Decoupled look-back over CTA-tile totals (one warp): returns the exclusive
 // prefix of tile t and publishes its inclusive prefix.  Tiles are taken in
 // ticket order, so every predecessor is running or done; with one status
@@ -755,7 +759,7 @@ static int build_buckets(dm_ctx* c) {
     A.bitems = c->k1_bitems.p;
   }
   // edge count estimate (V + T for a simplicial complex, plus slack); an
-  // overflow re-runs P3 with the exact count
+  // overflow re-runs k_edge_chunks with the exact count
   i64 est = std::min<i64>(M, (nv + nE) + (nv + nE) / 8 + 1024);
   if (const char* t = std::getenv("DUALMESH_K1_EDGE_EST")) est = std::max<i64>(1, std::atoll(t));
   if (c->edges.n < static_cast<size_t>(est)) {
