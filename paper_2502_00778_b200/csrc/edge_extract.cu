@@ -72,7 +72,7 @@ constexpr u64 kItemMask = (1ull << 31) - 1;
 template <int D>
 struct Caps {
   static constexpr int kNe = D == 3 ? 25 : 23;      // row capacity (entries per bucket row)
-  static constexpr int kNarrow = D == 3 ? 21 : 23;  // register path of the narrow P3 kernel
+  static constexpr int kNarrow = D == 3 ? 21 : 23;  // register path of the narrow chunk kernel
   static constexpr int kIncStage = D == 3 ? 1152 : 768;  // items per chunk (entries staged here first)
   static constexpr int kHeadStage = D == 3 ? 288 : 256;  // edges per chunk
 };
@@ -135,7 +135,7 @@ __device__ __forceinline__ int elem_ranks(const int (&v)[4], i64 nv, int (&rk)[4
 }
 
 // Flag 4: some bucket has more than Caps::kNe entries (side path); flag 8:
-// some bucket has more than Caps::kNarrow (the wide P3 kernel).
+// some bucket has more than Caps::kNarrow (the wide chunk kernel).
 template <int D>
 __global__ void k_ent_fill(const int32_t* __restrict__ el, i64 nE, i64 nv, u32* __restrict__ cnt,
                            u32* __restrict__ ent, int* flag) {
