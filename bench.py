@@ -539,7 +539,10 @@ def run_ours(args, world, rank, local, dist):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
-            "extra": {"throughput": {
+            "extra": {"roofline_vs_nominal": {
+                          "nominal_gbs": 8000.0, "element_loop_frac": achieved / 8000.0,
+                          "step_frac": B["metrics"] / (ms_step / 1e3) / 1e9 / 8000.0},
+                      "throughput": {
                           "step_tets_per_s": value, "step_edges_per_s": world * K * ne / (total_ms / 1e3),
                           "element_loop_edges_per_s": ne / (elem_ms / 1e3),
                           "edge_extraction_tets_per_s": mesh.num_elements() / (edges_ms / 1e3),
