@@ -202,6 +202,8 @@ def cpu_rows(config, scale, steps, warmup, serial_reps, trad_reps, threads=None)
     out = (np.empty(3 * e.shape[0]), np.empty(e.shape[0]), np.empty(m.num_nodes()))
     rows = {"grid": f"{n}^3 Kuhn cube, +-0.15h (seed 42), {m.num_elements()} tets, "
                     f"{e.shape[0]} edges", "n_elements": m.num_elements(),
+            "n_nodes": m.num_nodes(), "n_edges": int(e.shape[0]),
+            "n_boundary": m.num_boundary(),
             "host_cpu": cpu_model(), "host_threads": threads,
             "setup_s": {"gen": t1 - t0, "build_edges": t2 - t1, "plan": t3 - t2}}
     try:
@@ -264,7 +266,11 @@ def run_reference(args, world, rank, dist):
             "ms_per_step": rows["mt_step_ms"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.config, args.scale),
-                       "n_elements": rows["n_elements"]},
+                       "n_elements": rows["n_elements"], "n_nodes": rows["n_nodes"],
+                       "n_edges": rows["n_edges"], "n_boundary": rows["n_boundary"],
+                       "nav_variant": "dual-free element loop, serial summation order",
+                       "parallelism": f"host CPU, {th} threads",
+                       "l2": "inputs larger than the host caches (no flush)"},
             "cpu_baseline": {"value": value, "unit": "tets/s", "cores": th, "kind": "port",
                              "sample": sample},
             "cpu_rows": rows,

@@ -498,14 +498,20 @@ struct RingCodes {
 // extra registers cost the loop its unrolling.)
 // SIGNED = false leaves the ring orientation to the caller, which folds it
 // into the 1/12 scale ((-a) * f == a * (-f) exactly: the same bits).
-template <bool SIGNED = true, typename CT, typename TabFn>
+// U: unrolling of the ring loop.  The row-tile kernel is fastest at 4 (C5:
+// 1.42 ms; 1.44 / 1.47 / 1.49 ms at 2 / 3 / 1); the Morton-tile kernel at 2 --
+// left to itself ptxas unrolls its fused-multiply-add loop by 8, whose
+// remainder chain costs rings of 3..11 steps more than it saves (C3: 0.558 ms
+// at 2 against 0.594 / 0.664 / 0.600 / 0.709 at 1 / 3 / 4 / 6; the 2-3-flipped
+// grid 0.629 against 0.647 / 0.665 / 0.698 / 0.749; profiles/r2_ncu_summary.md).
+template <bool SIGNED = true, int U = 0, typename CT, typename TabFn>
 __device__ __forceinline__ void ring_walk(const TabFn& T, const CT& C, double* acc, d4& xk) {
   const int n = C.count();
   xk = T(C.slot(1));
   const d4 mp = T(C.slot(2));
   double dx = mp.x - xk.x, dy = mp.y - xk.y, dz = mp.z - xk.z;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int i = 0; i < n; ++i) {
+  auto step = [&](int i) {
     const d4 m = T(C.raw(3 + i));
     const double ex = m.x - xk.x, ey = m.y - xk.y, ez = m.z - xk.z;
     // cross(d, e) accumulated as two fused multiply-adds per component (6 FP64
@@ -517,6 +523,12 @@ __device__ __forceinline__ void ring_walk(const TabFn& T, const CT& C, double* a
     dx = ex;
     dy = ey;
     dz = ez;
+  };
+  if constexpr (U == 0) {  // the compiler's own choice
+    for (int i = 0; i < n; ++i) step(i);
+  } else {
+#pragma unroll U
+    for (int i = 0; i < n; ++i) step(i);
   }
   if constexpr (SIGNED) {
     const bool neg = C.negative();
@@ -698,7 +710,7 @@ __global__ void __launch_bounds__(kEB, MINB)
           ring_walk_trad(T, C, acc);
           xk = T(C.slot(1));
         } else {
-          ring_walk(T, C, acc, xk);
+          ring_walk<true, (CAP == 256 ? 2 : 0)>(T, C, acc, xk);
         }
         xj = T(C.slot(0));
       } else {
@@ -716,7 +728,7 @@ __global__ void __launch_bounds__(kEB, MINB)
           ring_walk_trad(T, C, acc);
           xk = T(C.slot(1));
         } else {
-          ring_walk(T, C, acc, xk);
+          ring_walk<true, (CAP == 256 ? 2 : 0)>(T, C, acc, xk);
         }
         xj = T(C.slot(0));
       }
@@ -856,7 +868,7 @@ __global__ void __launch_bounds__(kRowTile, MINB)
       } else {
         // the ring's orientation rides on the 1/12 scale (same bits as
         // edge_tail_values on the signed sums, three fewer FP64 negations)
-        ring_walk<false>(T, C, acc, xk);
+        ring_walk<false, 4>(T, C, acc, xk);
         xj = T(C.slot(0));
         const double f = C.negative() ? -(1.0 / 12.0) : (1.0 / 12.0);
         nv[0] = acc[0] * f;
