@@ -189,6 +189,12 @@ int dm_sync(dm_ctx* ctx); /* waits for the ctx stream and the pipelined copies *
  * [0] element loop, [1] boundary pass, [2] edge-volume loop, [3] total. */
 int dm_set_timing(dm_ctx* ctx, int enable);
 int dm_get_timings(dm_ctx* ctx, float* ms, int n);
+/* enable > 1 keeps the phase events of the last `enable` steps (a step = one
+ * dm_navs + dm_volumes pair), so a caller can time a run of back-to-back
+ * steps without synchronising inside it: dm_get_step_timings waits for the
+ * last recorded step and returns up to max_steps rows of the four values
+ * above, oldest first (ms[4 * s + i]); *n_steps = rows written. */
+int dm_get_step_timings(dm_ctx* ctx, float* ms, int max_steps, int* n_steps);
 int64_t dm_kernel_launches(const dm_ctx* ctx);
 /* Which element-loop kernels the plan enables: info[0] ring path built (1: Morton
  * tiles, rings.cu; 2: row tiles, rowplan.cu),

@@ -92,6 +92,7 @@ CAPI = {
     "dm_sync": (C.c_int, [P]),
     "dm_set_timing": (C.c_int, [P, C.c_int]),
     "dm_get_timings": (C.c_int, [P, FP, C.c_int]),
+    "dm_get_step_timings": (C.c_int, [P, FP, C.c_int, C.POINTER(C.c_int)]),
     "dm_kernel_launches": (C.c_int64, [P]),
     "dm_plan_info": (C.c_int, [P, I64P]),
     "dm_plan_side_edges": (C.c_int, [P, I64P]),

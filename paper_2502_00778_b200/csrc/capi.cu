@@ -112,6 +112,8 @@ void dm_destroy(dm_ctx* c) {
       }
     for (auto& e : c->ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : c->ev_ring)
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {c->ev_h2d, c->ev_comp, c->ev_out[0], c->ev_out[1]})
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
@@ -364,6 +366,43 @@ int dm_sync(dm_ctx* c) {
 int dm_set_timing(dm_ctx* c, int enable) {
   if (!c) return DM_ERR_INVALID_ARG;
   c->timing = enable != 0;
+  // enable > 1: a ring of per-step phase events (dm_get_step_timings)
+  const int steps = enable > 1 ? enable : 0;
+  if (steps != c->ring_steps) {
+    DM_CK(c, cudaStreamSynchronize(c->stream));
+    for (cudaEvent_t e : c->ev_ring) cudaEventDestroy(e);
+    c->ev_ring.clear();
+    c->ring_steps = 0;
+    if (steps > 0) {
+      c->ev_ring.resize(static_cast<size_t>(4 * steps), nullptr);
+      for (cudaEvent_t& e : c->ev_ring) DM_CK(c, cudaEventCreate(&e));
+      c->ring_steps = steps;
+    }
+  }
+  c->ring_pos = 0;
+  return DM_OK;
+}
+
+int dm_get_step_timings(dm_ctx* c, float* ms, int max_steps, int* n_steps) {
+  if (!c || !ms || !n_steps || max_steps < 0) return DM_ERR_INVALID_ARG;
+  if (!c->timing || c->ring_steps == 0) return fail(c, DM_ERR_STATE, "step timing ring disabled");
+  const long long have = c->ring_pos < c->ring_steps ? c->ring_pos : c->ring_steps;
+  const long long n = have < max_steps ? have : max_steps;
+  *n_steps = static_cast<int>(n);
+  if (n == 0) return DM_OK;
+  DM_CK(c, cudaStreamSynchronize(c->stream));
+  for (long long s = 0; s < n; ++s) {  // the newest n steps, oldest first
+    const size_t slot = static_cast<size_t>((c->ring_pos - n + s) % c->ring_steps);
+    const cudaEvent_t* e = c->ev_ring.data() + 4 * slot;
+    auto el = [&](int a, int b) {
+      float v = 0.f;
+      return cudaEventElapsedTime(&v, e[a], e[b]) == cudaSuccess ? v : -1.f;
+    };
+    ms[4 * s] = el(0, 1);
+    ms[4 * s + 1] = el(1, 2);
+    ms[4 * s + 2] = el(2, 3);
+    ms[4 * s + 3] = el(0, 3);
+  }
   return DM_OK;
 }
 

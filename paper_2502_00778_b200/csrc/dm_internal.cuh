@@ -9,6 +9,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <vector>
 #include <cstdlib>
 #include <type_traits>
 #include <cstdio>
@@ -278,6 +279,10 @@ struct dm_ctx {
 
   // timing
   bool timing = false;
+  // ring of per-step phase events (dm_set_timing(enable > 1)): 4 per step
+  std::vector<cudaEvent_t> ev_ring;
+  int ring_steps = 0;
+  long long ring_pos = 0;  // steps recorded so far (slot = ring_pos % ring_steps)
   cudaEvent_t ev[8] = {nullptr};
   float last_ms[4] = {0, 0, 0, 0};
   dm::i64 launches = 0;
@@ -566,7 +571,15 @@ int read_flag(dm_ctx* c, int* value);
 
 // Timing helpers: record event slot i when timing is enabled.
 inline void tmark(dm_ctx* c, int i) {
-  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+  if (!c->timing) return;
+  if (c->ring_steps > 0) {
+    // marks 0..2 come from dm_navs, 2 (again) and 3 from dm_volumes: the
+    // step's row is complete at mark 3
+    const size_t slot = static_cast<size_t>(c->ring_pos % c->ring_steps);
+    cudaEventRecord(c->ev_ring[4 * slot + i], c->stream);
+    if (i == 3) ++c->ring_pos;
+  }
+  cudaEventRecord(c->ev[i], c->stream);
 }
 
 }  // namespace dm

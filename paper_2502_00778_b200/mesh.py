@@ -350,6 +350,19 @@ class Engine:
     def set_timing(self, on: bool):
         self._ck(self._lib.dm_set_timing(self._c, 1 if on else 0), "dm_set_timing")
 
+    def set_step_timing(self, steps: int):
+        """Keep the phase events of the last `steps` steps (dm_set_timing(enable > 1))."""
+        self._ck(self._lib.dm_set_timing(self._c, max(2, int(steps))), "dm_set_timing")
+
+    def step_timings(self, max_steps: int) -> np.ndarray:
+        """Rows [element loop, boundary pass, volume loop, total] (ms) of the newest
+        recorded steps, oldest first (dm_get_step_timings; waits for the stream)."""
+        ms = (C.c_float * (4 * max_steps))()
+        n = C.c_int(0)
+        self._ck(self._lib.dm_get_step_timings(self._c, ms, max_steps, C.byref(n)),
+                 "dm_get_step_timings")
+        return np.array(ms[:4 * n.value], dtype=np.float64).reshape(-1, 4)
+
     def timings(self) -> list[float]:
         ms = (C.c_float * 4)()
         self._ck(self._lib.dm_get_timings(self._c, ms, 4), "dm_get_timings")

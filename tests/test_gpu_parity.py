@@ -585,6 +585,35 @@ def test_async_step_after_unsynced_calls(engine):
             lib.dm_host_free(p)
 
 
+def test_step_timing_ring(engine):
+    """dm_set_timing(enable > 1) keeps the phase events of the last steps, so a run of
+    back-to-back steps is timed without synchronising inside it (bench.py)."""
+    m = meshgen.tet_cube(12, amp=0.15)
+    engine.set_mesh(m)
+    engine.build_edges()
+    DF, G, E = _lib.DM_NAV_DUALFREE, _lib.DM_VARIANT_GATHER, _lib.DM_VOL_EDGE
+    engine.navs(DF, G)
+    engine.volumes(E)
+    want = engine.get_navs().copy()
+    engine.set_step_timing(3)
+    assert engine.step_timings(8).shape == (0, 4)
+    for _ in range(5):
+        engine.navs(DF, G)
+        engine.volumes(E)
+    t = engine.step_timings(8)
+    assert t.shape == (3, 4)  # the newest three of five
+    assert (t > 0).all() and (t[:, 3] >= t[:, :3].sum(axis=1) * 0.99).all(), t
+    assert engine.step_timings(2).shape == (2, 4)
+    engine.set_timing(True)  # back to the single-slot form
+    engine.navs(DF, G)
+    engine.volumes(E)
+    assert len(engine.timings()) == 4
+    with pytest.raises(Exception):
+        engine.step_timings(2)
+    engine.set_timing(False)
+    assert np.array_equal(engine.get_navs(), want)
+
+
 def test_set_coords_checks_length(engine):
     m = meshgen.baseline_config("C2", 8)
     engine.set_mesh(m)
