@@ -182,6 +182,21 @@ int build_edges_impl(dm_ctx* c) {
   c->have_edges = c->have_in = c->have_bedge = c->have_n2e = c->have_ifl = c->have_tables =
       c->have_rings = false;
   c->have_navs = c->have_vols = false;
+  if (c->nE == 0) {
+    // no elements: the reference returns an empty edge list whose origin CSR
+    // is nv + 1 zeros (mesh.cpp:256-285)
+    c->ne = 0;
+    DM_CK(c, c->os.ensure(static_cast<size_t>(c->nv + 1)));
+    DM_CK(c, cudaMemsetAsync(c->os.p, 0, (c->nv + 1) * sizeof(u32), c->stream));
+    DM_CK(c, c->edges.ensure(0));
+    DM_CK(c, c->inc_ptr.ensure(1));
+    DM_CK(c, cudaMemsetAsync(c->inc_ptr.p, 0, sizeof(int32_t), c->stream));
+    DM_CK(c, c->inc.ensure(0));
+    DM_CK(c, c->e2l.ensure(0));
+    DM_CK(c, cudaStreamSynchronize(c->stream));
+    c->have_edges = true;
+    return DM_OK;
+  }
   // DUALMESH_K1_LEGACY=1: the item-sort path for every mesh (A/B and tests)
   const char* legacy = std::getenv("DUALMESH_K1_LEGACY");
   if (!(legacy && *legacy == '1')) {

@@ -1407,6 +1407,15 @@ int navs_impl(dm_ctx* c, int algo, int variant) {
     return fail(c, DM_ERR_INVALID_ARG, "unknown nav algorithm");
   if (variant < DM_VARIANT_GATHER || variant > DM_VARIANT_GATHER_EXACT)
     return fail(c, DM_ERR_INVALID_ARG, "unknown nav variant");
+  if (c->ne == 0) {  // a mesh without elements has no edges: empty fields
+    DM_CK(c, c->navs.ensure(0));
+    DM_CK(c, c->svals.ensure(0));
+    c->svals_pos = false;
+    c->have_navs = true;
+    c->navs_algo = algo;
+    c->have_vols = false;
+    return DM_OK;
+  }
   int st = ensure_bedge(c);
   if (st) return st;
   if (variant == DM_VARIANT_GATHER) {

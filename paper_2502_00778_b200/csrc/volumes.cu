@@ -127,6 +127,15 @@ int compute_element_volumes(dm_ctx* c) {
 int volumes_impl(dm_ctx* c, int algo) {
   const i64 nv = c->nv;
   DM_CK(c, c->vols.ensure(static_cast<size_t>(nv)));
+  if (algo != DM_VOL_EDGE && algo != DM_VOL_ELEMENT)
+    return fail(c, DM_ERR_INVALID_ARG, "unknown volume algorithm");
+  if (algo == DM_VOL_EDGE && !c->have_navs)
+    return fail(c, DM_ERR_STATE, "edge-based volumes need navs first");
+  if (c->nE == 0) {  // no elements: every dual volume is an empty sum
+    if (nv > 0) DM_CK(c, cudaMemsetAsync(c->vols.p, 0, nv * sizeof(double), c->stream));
+    c->have_vols = true;
+    return DM_OK;
+  }
   if (algo == DM_VOL_EDGE) {
     if (!c->have_navs) return fail(c, DM_ERR_STATE, "edge-based volumes need navs first");
     int st = ensure_incoming(c);

@@ -92,6 +92,9 @@ def corrupted_meshes():
     t.elements.reshape(-1, 3)[3] = t.elements.reshape(-1, 3)[3][[0, 2, 1]]
     out["tri_inverted"] = t
     out["ftri_flipped"] = Mesh(2, [0, 0, 1, 0, 0, 1], [0, 2, 1], [0, 1, 1, 2, 2, 0])
+    # no elements (the reference accepts them: nothing to violate)
+    out["empty_tet"] = Mesh(3, np.arange(12.0), np.zeros(0, np.int32))
+    out["empty_tri"] = Mesh(2, np.arange(8.0), np.zeros(0, np.int32))
     return out
 
 
@@ -124,6 +127,25 @@ def test_derive_and_edges_match_reference(probe, name, scale):
     np.testing.assert_array_equal(go, o)
     for el in (0, m.num_elements() // 2, m.num_elements() - 1):
         assert probe.probe_element_volume(*_a(m), el) == r.element_volume(el)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_cpp_api_mesh_without_elements(probe, dim):
+    """build_edges / derive_boundary_faces on a mesh without elements: empty results, like
+    the reference (mesh.cpp:256-285, 287-330)."""
+    m = Mesh(dim, np.arange(dim * 5, dtype=np.float64), np.zeros(0, np.int32))
+    r = RefMesh(m)
+    want = r.derive_boundary()
+    got = np.empty(64, np.int32)
+    n = probe.probe_derive(*_a(m), got.ctypes.data_as(C.POINTER(C.c_int32)), got.size)
+    assert n == want.size == 0
+    e, o = r.build_edges()
+    ge = np.empty((8, 2), np.int32)
+    go = np.full(m.num_nodes() + 1, 7, np.uint64)
+    ne = probe.probe_build_edges(*_a(m), ge.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 go.ctypes.data_as(C.POINTER(C.c_uint64)), ge.shape[0])
+    assert ne == e.shape[0] == 0
+    np.testing.assert_array_equal(go, o)
 
 
 @pytest.mark.parametrize("name,scale", [("C1", 4), ("C2", 4), ("C4", 8)])

@@ -140,6 +140,35 @@ def test_2d_fan_side_path(engine, oracle, monkeypatch, n):
     assert_same(got, extract(engine, m))
 
 
+@pytest.mark.parametrize("dim,nv", [(3, 4), (2, 4), (3, 0), (2, 0)])
+def test_mesh_without_elements(engine, oracle, dim, nv):
+    """The reference's build_edges accepts a mesh without elements (an empty edge list over
+    nv + 1 zero offsets, mesh.cpp:256-285); every entry point follows with empty fields."""
+    from paper_2502_00778_b200 import _lib
+    m = Mesh(dim, np.arange(dim * nv, dtype=np.float64), np.zeros(0, np.int32))
+    got = extract(engine, m)
+    e, o = oracle.build_edges(m)
+    e2l, ip, inc = oracle.edge_maps(m, e, o)
+    assert e.shape == (0, 2) and o.shape == (nv + 1,)
+    assert_same(got, (e, o, e2l, ip, inc))
+    for algo in (_lib.DM_NAV_DUALFREE, _lib.DM_NAV_TRADITIONAL):
+        for var in (_lib.DM_VARIANT_GATHER, _lib.DM_VARIANT_GATHER_EXACT,
+                    _lib.DM_VARIANT_SCATTER):
+            engine.navs(algo, var)
+            assert engine.get_navs().size == 0
+            engine.volumes(_lib.DM_VOL_EDGE)
+            np.testing.assert_array_equal(engine.get_volumes(), np.zeros(nv))
+    engine.volumes(_lib.DM_VOL_ELEMENT)
+    np.testing.assert_array_equal(engine.get_volumes(), oracle.volumes_element(m))
+    r, _ = engine.check_closure()
+    assert r == 0.0
+    # and the context still serves a real mesh afterwards
+    k = meshgen.tet_cube(4, amp=0.1)
+    got = extract(engine, k)
+    e, o = oracle.build_edges(k)
+    np.testing.assert_array_equal(got[0], e)
+
+
 def test_single_element(engine, oracle):
     for m in (Mesh(3, np.array([0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0, 1], np.float64),
                    np.array([0, 1, 2, 3], np.int32), np.zeros(0, np.int32)),
