@@ -857,6 +857,11 @@ int ensure_rings(dm_ctx* c) {
   clk.mark("boundary edges");
   if (c->dim != 3) {
     c->ring_ok = false;
+    c->row_plan = false;
+    c->plan_colored = false;
+    c->ring_max_nodes = 0;
+    c->ring_fail = 0;
+    c->n_side = 0;
     c->have_rings = true;
     return DM_OK;
   }
