@@ -110,3 +110,65 @@ def test_more_than_2_pow_25_nodes(engine, oracle):
     x = np.zeros(3 * big)
     x.reshape(-1, 3)[ids] = k.coords.reshape(-1, 3)
     _check_against_oracle(engine, oracle, Mesh(3, x, ids[k.elements], ids[k.boundary]))
+
+
+def test_side_list_overflow_falls_back(engine, oracle):
+    """More irregular edges than the side list holds (2^20): the ring path is not used, the
+    whole mesh runs on the serial-order kernels -- same bits as the oracle."""
+    rng = np.random.default_rng(11)
+    nv, ne = 6000, 1500000
+    el = rng.integers(0, nv, size=(ne, 4), dtype=np.int32)
+    srt = np.sort(el, 1)
+    el = el[(srt[:, 1:] != srt[:, :-1]).all(1)]
+    m = Mesh(3, rng.random(3 * nv), el.reshape(-1), np.zeros(0, np.int32))
+    engine.set_mesh(m)
+    engine.build_edges()
+    e, o = oracle.build_edges(m)
+    np.testing.assert_array_equal(engine.edges().edges, e)
+    want = oracle.navs_dualfree(m, e, o)
+    engine.navs(_lib.DM_NAV_DUALFREE, _lib.DM_VARIANT_GATHER)
+    assert not engine.plan_info()["ring_ok"]
+    np.testing.assert_array_equal(engine.get_navs(), want)
+    engine.volumes(_lib.DM_VOL_EDGE)
+    np.testing.assert_array_equal(engine.get_volumes(), oracle.volumes_edge(m, e, want))
+
+
+def test_two_contexts_on_two_threads(oracle):
+    """One context per host thread (C-ABI threading rule), both on the device at once."""
+    import threading
+
+    from paper_2502_00778_b200 import Engine, meshgen
+    meshes = {"a": meshgen.tet_cube(20, amp=0.15),
+              "b": meshgen.permute(meshgen.tet_cube(18, amp=0.1))}
+    res, err = {}, []
+
+    def work(tag):
+        try:
+            en = Engine(0)
+            en.set_mesh(meshes[tag])
+            en.build_edges()
+            out = []
+            for _ in range(5):
+                en.navs()
+                en.volumes()
+                out.append((en.get_navs().copy(), en.get_volumes().copy()))
+            res[tag] = out
+            en.close()
+        except Exception as ex:  # surfaced below
+            err.append((tag, ex))
+
+    th = [threading.Thread(target=work, args=(t,)) for t in meshes]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not err, err
+    for tag, m in meshes.items():
+        e, o = oracle.build_edges(m)
+        w = oracle.navs_dualfree(m, e, o)
+        wv = oracle.volumes_edge(m, e, w)
+        for n, v in res[tag]:
+            assert np.abs(n - w).max() / np.abs(w).max() <= 1e-12
+            assert np.abs(v - wv).max() <= 1e-12 * np.abs(wv).max()
+            np.testing.assert_array_equal(n, res[tag][0][0])  # run-to-run bitwise
+            np.testing.assert_array_equal(v, res[tag][0][1])
