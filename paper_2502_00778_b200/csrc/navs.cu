@@ -416,19 +416,7 @@ __device__ __forceinline__ void pipe_issue(SM& S, int b, int tile, const int4& m
       }
     }
   }
-  if constexpr ((OPT & 128) != 0) {
-    // the tile's code block (contiguous, a multiple of 32 bytes) in one TMA
-    // bulk copy completing on full[b]; thread 0 is the extra arrival
-    if (t == 0) {
-      if (m.y <= SM::kCodeBytes && m.y > 0) {
-        mbar_arrive_expect_tx(&S.full[b], static_cast<unsigned>(m.y));
-        bulk_g2s(&S.cd[b][0], rcodes + 32 * static_cast<i64>(m.x), static_cast<unsigned>(m.y),
-                 &S.full[b]);
-      } else {
-        mbar_arrive(&S.full[b]);
-      }
-    }
-  } else if (m.y <= SM::kCodeBytes) {
+  if (m.y <= SM::kCodeBytes) {
     // code blocks are multiples of 32 bytes: 16-byte pieces
     const uint4* src = reinterpret_cast<const uint4*>(rcodes + 32 * static_cast<i64>(m.x));
     for (int w = t; w < m.y / 16; w += kEB) {
