@@ -715,6 +715,37 @@ def test_twice_c5_scale():
         eng.close()
 
 
+def test_largest_supported_scale_and_the_limit():
+    """384^3 (339.7 M tets, 397.7 M edges: L * N_E = 2.04e9, just under the 2^31 items of the
+    device layout; ~86 GB on the device) runs the default path with the SPEC identities; 400^3
+    is refused with DM_ERR_UNSUPPORTED, not a fault."""
+    from paper_2502_00778_b200 import DualMeshError, Engine
+    eng = Engine(0)
+    try:
+        eng.gen_tet_box(384, 384, 384, None, 0, 0.15, 42)
+        assert eng.build_edges() == 397689984
+        eng.navs(DF, GATHER)
+        eng.volumes(EDGE)
+        assert eng.plan_info()["ring_ok"] and eng.plan_info()["tiles"] == "row"
+        r, ri = eng.check_closure()
+        assert r <= 1e-13 and ri <= 1e-13
+        rel, sv, _ = eng.check_total_volume()
+        assert rel <= 1e-12 and abs(sv - 1.0) <= 1e-12
+    finally:
+        eng.close()
+    eng = Engine(0)
+    try:
+        eng.gen_tet_box(400, 400, 400, None, 0, 0.15, 42)
+        with pytest.raises(DualMeshError) as ei:
+            eng.build_edges()
+        assert "32-bit item space" in str(ei.value)
+        # the context is still usable
+        eng.gen_tet_box(8, 8, 8, None, 0, 0.15, 42)
+        assert eng.build_edges() > 0
+    finally:
+        eng.close()
+
+
 @pytest.mark.parametrize("name,scale", [("C2", 1), ("C4", 4), ("C5", 2), ("C3", 4)])
 def test_row_and_morton_plans_same_bits(name, scale, monkeypatch, oracle):
     """Both tilings of the ring walk (rowplan.cu row tiles, rings.cu Morton
