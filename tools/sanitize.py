@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Small pass over every kernel family for compute-sanitizer (memcheck / synccheck /
+"""Small pass over every kernel family (also usable under compute-sanitizer where the pool allows it: memcheck / synccheck /
 initcheck / racecheck): row tiles, Morton tiles, flipped topology, the side list, 2D,
 every navs variant, both volume algorithms, the checks and a plan rebuild.
 
