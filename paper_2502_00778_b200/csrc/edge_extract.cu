@@ -31,7 +31,7 @@
 // before k_edge_chunks: their entries are collected into exact lists,
 // expanded into (k << 32 | e*L + l) items and sorted by the generic
 // segmented sort; their lanes emit from that list.  Meshes with a repeated
-// node inside an element or more than 2^25 nodes take the generic item-sort
+// node inside an element or an element spanning 2^25 node ids take the generic item-sort
 // path (edges.cu).
 #include <cstdlib>
 #include <utility>
@@ -130,12 +130,15 @@ __device__ __forceinline__ int elem_ranks(const int (&v)[4], i64 nv, int (&rk)[4
       if (q != p) {
         rk[p] += v[q] < v[p];
         if (q > p && v[q] == v[p]) bad |= 2;
+        // the item keys hold k - j in 25 bits (k_edge_chunks)
+        if (!(bad & 1) && static_cast<i64>(v[q]) - v[p] >= (1ll << 25)) bad |= 16;
       }
   return bad;
 }
 
 // Flag 4: some bucket has more than Caps::kNe entries (side path); flag 8:
-// some bucket has more than Caps::kNarrow (the wide chunk kernel).
+// some bucket has more than Caps::kNarrow (the wide chunk kernel); flag 16
+// (elem_ranks): an element spans node ids 2^25 or more apart (generic path).
 template <int D>
 __global__ void k_ent_fill(const int32_t* __restrict__ el, i64 nE, i64 nv, u32* __restrict__ cnt,
                            u32* __restrict__ ent, int* flag) {
@@ -702,7 +705,7 @@ static int build_buckets(dm_ctx* c) {
   DM_CK(c, cudaStreamSynchronize(c->stream));
   if (hflag & 1)
     return fail(c, DM_ERR_INVALID_ARG, "an element references a node id outside [0, n_nodes)");
-  if (hflag & 2) return kK1Unsupported;
+  if (hflag & (2 | 16)) return kK1Unsupported;
   A.el = c->elems.p;
   A.cnt = c->fill.p;
   A.ent = c->k1_ent.p;
@@ -797,7 +800,9 @@ static int build_buckets(dm_ctx* c) {
 }
 
 int build_edges_buckets(dm_ctx* c) {
-  if (c->nv > (1ll << 25) || c->nv < 1) return kK1Unsupported;
+  // (any node count the device layout takes: what the item keys limit is the
+  // node-id span of an element, k - j < 2^25, flagged by k_ent_fill)
+  if (c->nv < 1) return kK1Unsupported;
   return c->dim == 3 ? build_buckets<3>(c) : build_buckets<2>(c);
 }
 

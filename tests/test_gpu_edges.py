@@ -169,6 +169,37 @@ def test_mesh_without_elements(engine, oracle, dim, nv):
     np.testing.assert_array_equal(got[0], e)
 
 
+def test_buckets_beyond_2_pow_25_nodes(monkeypatch):
+    """330^3 (35.9 M nodes > 2^25, 215.6 M tets): the bucket path (its item keys hold the
+    node-id span k - j in 25 bits, not the node id) against the item sort -- checksums of every
+    output, one array on the host at a time."""
+    import zlib
+
+    def sums(legacy):
+        if legacy:
+            monkeypatch.setenv("DUALMESH_K1_LEGACY", "1")
+        eng = Engine(0)
+        try:
+            eng.gen_tet_box(330, 330, 330, None, 0, 0.15, 42)
+            out = [eng.build_edges()]
+            el = eng.edges()
+            out += [zlib.crc32(el.edges.tobytes()), zlib.crc32(el.origin_start.tobytes())]
+            del el
+            a = eng.e2l()
+            out.append(zlib.crc32(a.tobytes()))
+            del a
+            ip, inc = eng.incidence()
+            out += [zlib.crc32(ip.tobytes()), zlib.crc32(inc.tobytes())]
+            return out
+        finally:
+            eng.close()
+            monkeypatch.delenv("DUALMESH_K1_LEGACY", raising=False)
+
+    got = sums(False)
+    assert got[0] == 252540090
+    assert got == sums(True)
+
+
 def test_single_element(engine, oracle):
     for m in (Mesh(3, np.array([0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0, 1], np.float64),
                    np.array([0, 1, 2, 3], np.int32), np.zeros(0, np.int32)),

@@ -100,13 +100,21 @@ def test_side_list_overflow_and_wide_tables(engine, oracle):
     assert engine.side_edges() > 100000 and engine.plan_info()["ring_max_tile_nodes"] > 256
 
 
-def test_more_than_2_pow_25_nodes(engine, oracle):
-    """Node ids beyond the bucket path's 25-bit keys: K1 takes the generic item sort."""
+@pytest.mark.parametrize("layout", ["spread", "split"])
+def test_more_than_2_pow_25_nodes(engine, oracle, layout):
+    """More than 2^25 node ids.  "spread": the cube's nodes at sorted random ids (element spans
+    stay small: K1's bucket path, whose item keys hold k - j in 25 bits); "split": half of them
+    moved beyond 2^25, so elements span more than the keys hold and K1 takes the generic item
+    sort.  Both against the oracle."""
     from paper_2502_00778_b200 import meshgen
     k = meshgen.tet_cube(10, amp=0.1)
     rng = np.random.default_rng(5)
-    big = (1 << 25) + 1000
-    ids = np.sort(rng.choice(big, k.num_nodes(), replace=False))
+    big = (1 << 25) + 2000
+    n = k.num_nodes()
+    if layout == "spread":
+        ids = np.sort(rng.choice(big, n, replace=False))
+    else:
+        ids = np.concatenate([np.arange(n // 2), (1 << 25) + 500 + np.arange(n - n // 2)])
     x = np.zeros(3 * big)
     x.reshape(-1, 3)[ids] = k.coords.reshape(-1, 3)
     _check_against_oracle(engine, oracle, Mesh(3, x, ids[k.elements], ids[k.boundary]))
