@@ -16,6 +16,7 @@ namespace dm {
 constexpr int kRingTooLong = 4;     // more than kRingMax incidences
 constexpr int kRingNonManifold = 8; // the walk does not consume every incident element
 constexpr int kRingMixedSign = 16;  // inconsistently oriented fan
+constexpr int kRingWideTile = 64;   // a slot beyond the 8-bit table of a tile over 256 nodes
 
 // parity of the permutation taking (a0,a1,a2) to (b0,b1,b2): +1 even, -1 odd
 __device__ __forceinline__ int perm_sign(int a0, int a1, int a2, int b0, int b1, int b2) {

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kTileEdges)
   __syncthreads();
   const int n = s_n;
   if (t == 0) atomicMax(flag + 1, n);
+  if (t == 0 && n > 256) atomicAdd(flag + 3, 1);  // tiles beyond an 8-bit table
   if (n > kTileNodeCap) {
     if (t == 0) atomicOr(flag, 2);
     return;
@@ -179,12 +180,19 @@ __global__ void k_ring_codes(const int2* __restrict__ edges, const int32_t* __re
     if constexpr (W == 2) out[step * 32] = static_cast<uint16_t>(v);
     else out8[step * 32] = static_cast<uint8_t>(v);
   };
-  const RingWalk r = ring_walk_encode(j, k, pb, n, inc, el, [&](int step, int v) {
+  int wide = 0;  // W == 1: a slot beyond the 8-bit table (a tile of more than 256 nodes)
+  RingWalk r = ring_walk_encode(j, k, pb, n, inc, el, [&](int step, int v) {
     const int sl = tslot(list, nl, rank[v]);
+    if (W == 1 && sl > 255) wide = kRingWideTile;
     put(2 + step, (W == 2 && step == 0) ? (sl | (bmark[e] ? 0x8000u : 0u)) : sl);
   });
   // closed: the last ring slot repeats slot(m_0) (word-0 bit 14 / header bit 7)
-  const int sj = tslot(list, nl, rank[j]), sk = tslot(list, nl, rank[k]);
+  int sj = tslot(list, nl, rank[j]), sk = tslot(list, nl, rank[k]);
+  if (W == 1 && (sj > 255 || sk > 255)) {
+    wide = kRingWideTile;
+    sj = sk = 0;  // any table node: the side list recomputes the edge
+  }
+  r.fail |= wide;
   if (r.fail) {  // side list: an empty ring (m_0 := k), k_navs_side recomputes the edge
     if constexpr (W == 2) {
       put(0, sj);
@@ -899,7 +907,7 @@ int ensure_rings(dm_ctx* c) {
   DM_CK(c, cudaMemsetAsync(c->tnode_cnt.p, 0, ntiles * sizeof(u32), c->stream));
   DM_CK(c, c->ring_meta.ensure(static_cast<size_t>(2 * ntiles)));
   DM_CK(c, c->flag.ensure(4));
-  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 3 * sizeof(int), c->stream));
+  DM_CK(c, cudaMemsetAsync(c->flag.p, 0, 4 * sizeof(int), c->stream));
   DM_CK(c, c->side.ensure(kSideCap));
   c->n_side = 0;
   ScratchBuf<int32_t> rank(c->arena, arena_block(c));
@@ -914,10 +922,23 @@ int ensure_rings(dm_ctx* c) {
             c->eperm.p, c->inc_ptr.p, c->inc.p, c->elems.p, rank.p, ne, c->tnodes.p,
             c->tnode_cnt.p, c->flag.p);
   // 8-bit slot codes when every tile table fits 256 nodes, else 16-bit
-  int fl0[2] = {0, 0};
+  int fl0[4] = {0, 0, 0, 0};
   DM_CK(c, cudaMemcpyAsync(fl0, c->flag.p, sizeof(fl0), cudaMemcpyDeviceToHost, c->stream));
   DM_CK(c, cudaStreamSynchronize(c->stream));
   c->code_width = fl0[1] <= 256 ? 1 : 2;
+  // A few tiles just over 256 nodes (where the Morton curve jumps) would put the
+  // whole mesh on 16-bit codes and the two-buffer kernel (256^3 permuted:
+  // one tile of 262 nodes, element loop 3.13 instead of ~2.5 ms).  Plans
+  // without slot colouring keep 8-bit codes then: an edge whose slots pass 255
+  // goes to the side list, its tile reads the table from global memory.
+  // env DUALMESH_WIDE_TILES_MAX: tiles over 256 nodes tolerated per 1000 (default 5).
+  {
+    int per_mille = 5;
+    if (const char* wt = std::getenv("DUALMESH_WIDE_TILES_MAX")) per_mille = std::atoi(wt);
+    if (c->code_width == 2 && c->vol_by_rank && !(fl0[0] & 2) &&
+        static_cast<i64>(fl0[3]) * 1000 <= static_cast<i64>(per_mille) * ntiles)
+      c->code_width = 1;
+  }
   clk.mark("tile nodes");
   ScratchBuf<u32> wstart(c->arena, arena_block(c));
   DM_CK(c, wstart.ensure(static_cast<size_t>(nwarps + 1)));

@@ -180,3 +180,22 @@ def test_two_contexts_on_two_threads(oracle):
             assert np.abs(v - wv).max() <= 1e-12 * np.abs(wv).max()
             np.testing.assert_array_equal(n, res[tag][0][0])  # run-to-run bitwise
             np.testing.assert_array_equal(v, res[tag][0][1])
+
+
+def test_wide_tiles_keep_8_bit_codes(engine, oracle, monkeypatch):
+    """Tiles of more than 256 nodes in a plan with 8-bit ring codes (tolerated when they are
+    few; forced here for every tile of a soup): edges whose slots pass 255 ride the side list,
+    their tiles read the table from global memory -- results against the oracle."""
+    monkeypatch.setenv("DUALMESH_WIDE_TILES_MAX", "1000")
+    rng = np.random.default_rng(21)
+    nv, ne = 3000, 200000
+    el = np.stack([rng.choice(nv, 4, replace=False) for _ in range(ne)]).astype(np.int32)
+    m = Mesh(3, rng.random(3 * nv), el.reshape(-1), np.zeros(0, np.int32))
+    _check_against_oracle(engine, oracle, m)
+    info = engine.plan_info()
+    assert info["ring_ok"] and info["ring_max_tile_nodes"] > 256 and info["ring_fail_bits"] & 64
+    assert engine.side_edges() > 0
+    e, o = oracle.build_edges(m)
+    wt = oracle.navs_traditional(m, e, o)
+    engine.navs(_lib.DM_NAV_TRADITIONAL, _lib.DM_VARIANT_GATHER)
+    assert np.abs(engine.get_navs() - wt).max() / np.abs(wt).max() <= 1e-12
