@@ -928,14 +928,15 @@ int ensure_rings(dm_ctx* c) {
   c->code_width = fl0[1] <= 256 ? 1 : 2;
   // A few tiles just over 256 nodes (where the Morton curve jumps) would put the
   // whole mesh on 16-bit codes and the two-buffer kernel (256^3 permuted:
-  // one tile of 262 nodes, element loop 3.13 instead of ~2.5 ms).  Plans
-  // without slot colouring keep 8-bit codes then: an edge whose slots pass 255
-  // goes to the side list, its tile reads the table from global memory.
+  // one tile of 262 nodes, element loop 3.13 instead of ~2.5 ms).  The plan
+  // keeps 8-bit codes then: an edge whose slots pass 255 goes to the side
+  // list, its tile reads the table from global memory (the slot colouring
+  // leaves such tiles alone).
   // env DUALMESH_WIDE_TILES_MAX: tiles over 256 nodes tolerated per 1000 (default 5).
   {
     int per_mille = 5;
     if (const char* wt = std::getenv("DUALMESH_WIDE_TILES_MAX")) per_mille = std::atoi(wt);
-    if (c->code_width == 2 && c->vol_by_rank && !(fl0[0] & 2) &&
+    if (c->code_width == 2 && !(fl0[0] & 2) &&
         static_cast<i64>(fl0[3]) * 1000 <= static_cast<i64>(per_mille) * ntiles)
       c->code_width = 1;
   }
