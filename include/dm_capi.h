@@ -202,7 +202,8 @@ int64_t dm_kernel_launches(const dm_ctx* ctx);
  * [4] max tile node count (ring path), [5] ring-build bits (2: a Morton tile
  * touches > 1536 nodes and 32: ring codes beyond 64 GB disable the ring path;
  * 4: an edge has > 24 incident elements, 8: a non-manifold fan, 16: an
- * inconsistently oriented fan send those edges to the side list),
+ * inconsistently oriented fan, 64: a table slot beyond 255 in one of a few Morton
+ * tiles over 256 nodes send those edges to the side list),
  * [6] edge-volume pass walks nodes in Morton order (1) or id order (0),
  * [7] tile tables recoloured against bank conflicts (env DUALMESH_PLAN_COLOR=1). */
 int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
@@ -210,7 +211,7 @@ int dm_plan_info(dm_ctx* ctx, int64_t info[8]);
  * describe -- more than 24 incident elements, a non-manifold or inconsistently
  * oriented fan -- evaluated from their element list inside the same dm_navs
  * call (0 when the ring path is not in use).  [5] of dm_plan_info gives the
- * reasons (4 / 8 / 16). */
+ * reasons (4 / 8 / 16 / 64). */
 int dm_plan_side_edges(dm_ctx* ctx, int64_t* n);
 /* Per-step streams of the row-tile element loop (zeros for other plans):
  * out[0] ring-code bytes, [1] node-table fill bytes (24 B per table slot, from
